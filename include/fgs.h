@@ -1,0 +1,205 @@
+/*
+ * fgs.h — C ABI of the B200-native 4D Gaussian Splatting forward path
+ *         (arXiv 2310.08528, "4D Gaussian Splatting for Real-Time Dynamic Scene Rendering").
+ *
+ * The two calls of the paper's problem statement (§4.1):
+ *     G' = G + F(G, t)      ->  fgs_deform   (Gaussian deformation field, §4.2)
+ *     I  = S(M, G')         ->  fgs_render   (differentiable splatting of [3dgs], §3.1)
+ * plus their frame-batched, range (sharded) and debug variants.  Citations: P:n = PAPER.md line n.
+ *
+ * Conventions (all entry points):
+ *  - Every array pointer inside the structs and every image/workspace pointer is a DEVICE pointer
+ *    (cudaMalloc / torch CUDA tensor), fp32 unless stated, C-contiguous, 16-byte aligned.  Struct
+ *    and struct-array arguments themselves (and `ts`) live in HOST memory and are read before the
+ *    call returns.  `stream` is a cudaStream_t (0 = legacy default stream).
+ *  - Ownership: the caller owns every buffer; the library never allocates device memory on these
+ *    paths and keeps no pointer after the call returns (kernels enqueued on `stream` use them).
+ *  - Asynchrony: calls validate arguments synchronously, then enqueue kernels and return.  No call
+ *    except fgs_render_status synchronises.  All calls are CUDA-graph capturable.
+ *  - Errors: an int code, never an exception.  FGS_E_INVALID for bad arguments (null pointers,
+ *    n < 0, sh_degree outside [0,3], width/height <= 0, res/t_res < 2, n_scales outside [1,4],
+ *    feat not in {4,8,...,32}, in_dim != feat*n_scales, in_dim > 64, width not in {32,64,128},
+ *    t not finite or outside [0,1], misaligned pointers, begin/end out of range, workspace too
+ *    small).  FGS_E_CUDA when a launch fails (message in fgs_last_error()).  Instance-capacity
+ *    overflow is data dependent and reported by fgs_render_status as FGS_E_CAPACITY.
+ *  - Data-dependent degeneracies are not validated: NaN or zero quaternions make a Gaussian
+ *    culled (its projected determinant is NaN), never a crash.
+ *  - Reentrant for distinct workspaces; the only global state is one-time kernel attribute setup.
+ */
+#ifndef FGS_H
+#define FGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fgs_stream_t; /* == cudaStream_t */
+
+enum {
+  FGS_OK = 0,
+  FGS_E_INVALID = -1,
+  FGS_E_CUDA = -2,
+  FGS_E_CAPACITY = -3,
+  FGS_E_NOTIMPL = -4
+};
+enum { FGS_MAX_SCALES = 4, FGS_PLANES = 6, FGS_TILE = 16 };
+
+/* Canonical 3D Gaussians G = {X, r, s, sigma, C}. */
+typedef struct {
+  int64_t n;                    /* number of Gaussians (>= 0) */
+  int32_t sh_degree;            /* 0..3; K = (deg+1)^2 SH functions ("k nums of SH functions") */
+  const float* means;           /* [n][3]  X (world)                                              */
+  const float* log_scales;      /* [n][3]  log s; s = exp(.)                                      */
+  const float* quats;           /* [n][4]  r, raw quaternion (w,x,y,z); normalised at render      */
+  const float* opacity_logits;  /* [n]     sigma = sigmoid(.)                                     */
+  const float* sh;              /* [n][K][3] SH coefficients, k = l^2 + l + m                     */
+} fgs_gaussians;
+
+/* Multi-resolution HexPlane R_l(i,j) (Eq. 7).  Plane order
+ * (x,y),(x,z),(y,z),(x,t),(y,t),(z,t); plane (a,b) of scale l is [n_b][n_a][feat] with
+ * n_x = n_y = n_z = res[l] and n_t = t_res (same at every scale).  A mean maps to the grid by
+ * u = clamp((X - bmin)/(bmax - bmin), 0, 1); knot k of an axis of n knots sits at u = k/(n-1). */
+typedef struct {
+  int32_t n_scales;             /* L, 1..4                                                        */
+  int32_t feat;                 /* h, multiple of 4, <= 32                                        */
+  int32_t t_res;                /* temporal knots, >= 2                                           */
+  int32_t res[FGS_MAX_SCALES];  /* spatial knots per scale, >= 2                                  */
+  float bmin[3], bmax[3];       /* world AABB of the field (bmax > bmin)                          */
+  const float* planes[FGS_MAX_SCALES][FGS_PLANES];
+} fgs_hexplanes;
+
+/* phi_d (one Linear + ReLU) and the heads phi_x, phi_r, phi_s (one Linear each).
+ * Row-major [out][in] (PyTorch Linear layout). */
+typedef struct {
+  int32_t in_dim;               /* = feat * n_scales (<= 64)                                      */
+  int32_t width;                /* hidden width W of phi_d: 32, 64 or 128                         */
+  const float *w_d, *b_d;       /* [W][in_dim], [W]                                               */
+  const float *w_x, *b_x;       /* [3][W], [3]                                                    */
+  const float *w_r, *b_r;       /* [4][W], [4]                                                    */
+  const float *w_s, *b_s;       /* [3][W], [3]                                                    */
+} fgs_mlp;
+
+/* Deformed Gaussians G' = {X', s', r', sigma, C}.  fgs_deform writes means, log_scales and
+ * quats (raw: X + dX, log s + ds, r + dr); opacity and SH alias the canonical arrays. */
+typedef struct {
+  int64_t n;
+  int32_t sh_degree;
+  float* means;                 /* [n][3] */
+  float* log_scales;            /* [n][3] */
+  float* quats;                 /* [n][4] */
+  const float* opacity_logits;  /* [n]       (alias of the canonical array)                       */
+  const float* sh;              /* [n][K][3] (alias of the canonical array)                       */
+} fgs_deformed;
+
+/* View matrix M = [R, T] + pinhole intrinsics.  World->camera, row-major, OpenCV axes
+ * (x right, y down, z forward); pixel (px,py) is evaluated at continuous (px,py).  Host struct. */
+typedef struct {
+  float R[9];
+  float t[3];
+  float fx, fy, cx, cy;
+  int32_t width, height;        /* > 0, <= 16384                                                  */
+  float bg[3];                  /* background colour added as T_final * bg                        */
+} fgs_camera;
+
+/* Optional device outputs of fgs_render_debug; any pointer may be NULL. */
+typedef struct {
+  int32_t* radii;               /* [n]          integer pixel radius, 0 if culled                 */
+  int32_t* rect;                /* [n][4]       tile rect x0,y0,x1,y1 ([x0,x1) x [y0,y1)), 0s if culled */
+  float* mean2d;                /* [n][2]       projected mean                                    */
+  uint32_t* depth_key;          /* [n]          IEEE bits of fp32 view-space depth, 0 if culled   */
+  uint32_t* tiles_touched;      /* [n]                                                            */
+  uint32_t* n_instances;        /* [1]          M (un-clamped)                                    */
+  uint32_t* sorted_tile;        /* [max_instances] tile id of each sorted instance                */
+  uint32_t* sorted_gid;         /* [max_instances] Gaussian index of each sorted instance         */
+  uint32_t* ranges;             /* [tiles][2]   [start,end) of each tile's list                   */
+  float* final_T;               /* [H][W]       final transmittance                               */
+  uint32_t* n_contrib;          /* [H][W]       number of composited Gaussians                    */
+  uint32_t* n_evaluated;        /* [H][W]       list entries evaluated before the pixel terminated */
+} fgs_render_aux;
+
+/* ---- deformation field F --------------------------------------------------
+ * For every Gaussian i and time t in [0,1]: f_h = concat_l prod_planes bilinear(R_l(i,j)) at
+ * (X_i, t) (Eq. 7); f_d = ReLU(W_d f_h + b_d); (X', r', s') = (X, r, s) + heads(f_d). */
+int fgs_deform(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+               fgs_deformed* out, fgs_stream_t stream);
+/* Only Gaussians [begin, end) are written (the rest of `out` untouched): the shard of §8(e2).
+ * Results are bit-identical to the same rows of fgs_deform. */
+int fgs_deform_range(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+                     int64_t begin, int64_t end, fgs_deformed* out, fgs_stream_t stream);
+/* n_t times ts[0..n_t) (HOST array) into outs[0..n_t) (HOST array of structs) in one pass that
+ * shares the spatial-plane work across times.  Bit-identical to n_t calls of fgs_deform. */
+int fgs_deform_batch(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
+                     const float* ts, int32_t n_t, fgs_deformed* outs, fgs_stream_t stream);
+
+/* ---- splatting S (§3.1, [3dgs] rasterizer P:728) ----------------------------
+ * Device workspace bytes for ONE frame of n Gaussians at width x height with room for
+ * max_instances (tile, Gaussian) instances; a batch of F frames needs F times this. */
+size_t fgs_render_workspace_bytes(int64_t n, int32_t width, int32_t height, int64_t max_instances);
+/* Renders image [3][height][width] fp32 (CHW, no final clamp).  ws/ws_bytes: device workspace;
+ * the instance capacity is the largest max_instances whose workspace fits in ws_bytes. */
+int fgs_render(const fgs_camera* cam, const fgs_deformed* g, float* image, void* ws, size_t ws_bytes,
+               fgs_stream_t stream);
+/* n_frames frames (all cameras must share width/height); cams, defs and images are HOST arrays,
+ * images[f] a DEVICE pointer.  ws holds n_frames equal per-frame slices of ws_bytes/n_frames. */
+int fgs_render_batch(const fgs_camera* cams, const fgs_deformed* defs, float* const* images,
+                     int32_t n_frames, void* ws, size_t ws_bytes, fgs_stream_t stream);
+/* fgs_render plus the intermediate results in `aux` (debugging and parity tests). */
+int fgs_render_debug(const fgs_camera* cam, const fgs_deformed* g, float* image, void* ws,
+                     size_t ws_bytes, const fgs_render_aux* aux, fgs_stream_t stream);
+/* Synchronises `stream`; FGS_E_CAPACITY if any frame of the last render into `ws` overflowed its
+ * instance capacity (its image is then invalid), else FGS_OK.  n_frames = frames in ws. */
+int fgs_render_status(const void* ws, size_t ws_bytes, int32_t n_frames, fgs_stream_t stream);
+
+/* ---- whole frames (deform + render), the step bench.py times --------------------------------
+ * Frame f deforms G at ts[f] into defs_scratch[f] (device buffers owned by the caller) and renders
+ * it with cams[f] into images[f].  Device pointers everywhere except the host arrays. */
+int fgs_frames(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
+               const float* ts, const fgs_camera* cams, int32_t n_frames, fgs_deformed* defs_scratch,
+               float* const* images, void* ws, size_t ws_bytes, fgs_stream_t stream);
+
+/* ---- end to end with HOST buffers (what e2e in bench.py times) ---------------------------------
+ * Same as fgs_frames, but every array pointer in g_host / field_host / mlp_host and images_host[f]
+ * is a HOST pointer (pinned memory gives asynchronous copies).  The call enqueues the host->device
+ * copies of the model into `dev_ws`, the deform + render of all frames, and the device->host copies
+ * of the images, all on `stream`; the images are valid after the stream synchronises.
+ * dev_ws: device memory of at least fgs_frames_host_workspace_bytes(...) bytes. */
+size_t fgs_frames_host_workspace_bytes(const fgs_gaussians* g_host, const fgs_hexplanes* field_host,
+                                       const fgs_mlp* mlp_host, int32_t n_frames, int32_t width,
+                                       int32_t height, int64_t max_instances);
+int fgs_frames_host(const fgs_gaussians* g_host, const fgs_hexplanes* field_host, const fgs_mlp* mlp_host,
+                    const float* ts, const fgs_camera* cams, int32_t n_frames, float* const* images_host,
+                    void* dev_ws, size_t dev_ws_bytes, fgs_stream_t stream);
+
+/* ---- profiling -------------------------------------------------------------------------------
+ * When enabled, the library records a CUDA event pair around every stage it launches, on the
+ * stream of the call.  fgs_profile_read synchronises those events and writes the accumulated
+ * milliseconds and launch counts per stage into ms[FGS_N_STAGES] / launches[FGS_N_STAGES]
+ * (either may be NULL), then resets them.  Not thread-safe (one profiling client at a time). */
+enum {
+  FGS_STAGE_DEFORM = 0,
+  FGS_STAGE_PREPROCESS,
+  FGS_STAGE_DEPTH_SORT,
+  FGS_STAGE_OFFSETS,
+  FGS_STAGE_DUPLICATE,
+  FGS_STAGE_TILE_SORT,
+  FGS_STAGE_RANGES,
+  FGS_STAGE_BLEND,
+  FGS_N_STAGES
+};
+int fgs_profile_enable(int enable);
+int fgs_profile_read(double* ms, int64_t* launches);
+/* Number of kernels this library has launched since it was loaded (all threads). */
+int64_t fgs_launch_count(void);
+
+/* Message of the last non-OK return on this thread (static storage, never NULL). */
+const char* fgs_last_error(void);
+/* Library version string and the compute capability it was built for ("sm_100a"). */
+const char* fgs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGS_H */

@@ -1,0 +1,501 @@
+// C ABI of libfgs.so (include/fgs.h): argument validation, workspace layout, frame batching.
+// Everything here is host code; the arithmetic of the method lives in deform.cu / render.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fgs_internal.cuh"
+
+namespace fgs {
+namespace {
+
+thread_local std::string g_err = "ok";
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FGS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+#define FGS_CHECK(cond, msg) \
+  do {                       \
+    if (!(cond)) return fail(FGS_E_INVALID, msg); \
+  } while (0)
+
+int check_gaussians(const fgs_gaussians* g) {
+  FGS_CHECK(g, "gaussians is NULL");
+  FGS_CHECK(g->n >= 0 && g->n < (int64_t)1 << 31, "gaussians.n out of range [0, 2^31)");
+  FGS_CHECK(g->sh_degree >= 0 && g->sh_degree <= 3, "sh_degree must be in [0,3]");
+  if (g->n == 0) return FGS_OK;
+  FGS_CHECK(g->means && g->log_scales && g->quats && g->opacity_logits && g->sh, "null Gaussian array");
+  FGS_CHECK(aligned16(g->means) && aligned16(g->log_scales) && aligned16(g->quats) &&
+                aligned16(g->opacity_logits) && aligned16(g->sh),
+            "Gaussian arrays must be 16-byte aligned");
+  return FGS_OK;
+}
+
+int check_field(const fgs_hexplanes* h, const fgs_mlp* m) {
+  FGS_CHECK(h && m, "hexplanes/mlp is NULL");
+  FGS_CHECK(h->n_scales >= 1 && h->n_scales <= FGS_MAX_SCALES, "n_scales must be in [1,4]");
+  FGS_CHECK(h->feat == 4 || h->feat == 8 || h->feat == 16 || h->feat == 32, "feat must be 4, 8, 16 or 32");
+  FGS_CHECK(h->t_res >= 2, "t_res must be >= 2");
+  for (int l = 0; l < h->n_scales; ++l) {
+    FGS_CHECK(h->res[l] >= 2 && h->res[l] <= 4096, "res[l] must be in [2,4096]");
+    for (int p = 0; p < FGS_PLANES; ++p)
+      FGS_CHECK(h->planes[l][p] && aligned16(h->planes[l][p]), "plane pointer NULL or misaligned");
+  }
+  for (int a = 0; a < 3; ++a)
+    FGS_CHECK(isfinite(h->bmin[a]) && isfinite(h->bmax[a]) && h->bmax[a] > h->bmin[a], "bad AABB");
+  FGS_CHECK(m->in_dim == h->feat * h->n_scales, "mlp.in_dim != feat * n_scales");
+  FGS_CHECK(m->in_dim <= 64, "in_dim must be <= 64");
+  FGS_CHECK(m->width == 32 || m->width == 64 || m->width == 128, "mlp.width must be 32, 64 or 128");
+  FGS_CHECK(m->w_d && m->b_d && m->w_x && m->b_x && m->w_r && m->b_r && m->w_s && m->b_s, "null MLP array");
+  FGS_CHECK(aligned16(m->w_d), "w_d must be 16-byte aligned");
+  return FGS_OK;
+}
+
+int check_deformed(const fgs_deformed* d, int64_t n, int sh_degree, bool writable) {
+  FGS_CHECK(d, "deformed is NULL");
+  FGS_CHECK(d->n == n, "deformed.n != gaussians.n");
+  FGS_CHECK(d->sh_degree == sh_degree, "deformed.sh_degree mismatch");
+  if (n == 0) return FGS_OK;
+  FGS_CHECK(d->means && d->log_scales && d->quats, "null deformed output array");
+  FGS_CHECK(aligned16(d->means) && aligned16(d->log_scales) && aligned16(d->quats), "deformed arrays misaligned");
+  if (!writable) FGS_CHECK(d->opacity_logits && d->sh, "null deformed opacity/sh");
+  return FGS_OK;
+}
+
+int check_camera(const fgs_camera* c) {
+  FGS_CHECK(c, "camera is NULL");
+  FGS_CHECK(c->width > 0 && c->height > 0 && c->width <= 16384 && c->height <= 16384, "bad image size");
+  FGS_CHECK(isfinite(c->fx) && isfinite(c->fy) && c->fx > 0 && c->fy > 0, "bad focal length");
+  return FGS_OK;
+}
+
+void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m) {
+  memset(&p, 0, sizeof(p));
+  p.means = g->means; p.log_scales = g->log_scales; p.quats = g->quats;
+  p.n_scales = h->n_scales; p.feat = h->feat; p.t_res = h->t_res;
+  for (int l = 0; l < FGS_MAX_SCALES; ++l) {
+    p.res[l] = h->res[l];
+    for (int q = 0; q < FGS_PLANES; ++q) p.planes[l][q] = l < h->n_scales ? h->planes[l][q] : nullptr;
+  }
+  for (int a = 0; a < 3; ++a) { p.bmin[a] = h->bmin[a]; p.ext[a] = h->bmax[a] - h->bmin[a]; }
+  p.in_dim = m->in_dim; p.width = m->width;
+  p.w_d = m->w_d; p.b_d = m->b_d; p.w_x = m->w_x; p.b_x = m->b_x;
+  p.w_r = m->w_r; p.b_r = m->b_r; p.w_s = m->w_s; p.b_s = m->b_s;
+}
+
+int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
+                int64_t begin, int64_t end, fgs_deformed* outs, cudaStream_t s) {
+  int rc;
+  if ((rc = check_gaussians(g)) != FGS_OK) return rc;
+  if ((rc = check_field(h, m)) != FGS_OK) return rc;
+  FGS_CHECK(ts && outs && n_t >= 0, "null times/outputs");
+  FGS_CHECK(begin >= 0 && begin <= end && end <= g->n, "begin/end out of range");
+  for (int f = 0; f < n_t; ++f) {
+    FGS_CHECK(isfinite(ts[f]) && ts[f] >= 0.f && ts[f] <= 1.f, "t must be finite and in [0,1]");
+    if ((rc = check_deformed(&outs[f], g->n, g->sh_degree, true)) != FGS_OK) return rc;
+  }
+  if (end == begin || n_t == 0) return FGS_OK;
+  DeformBatch p;
+  fill_deform(p, g, h, m);
+  p.begin = begin; p.end = end;
+  for (int f0 = 0; f0 < n_t; f0 += kMaxFrames) {
+    p.n_t = std::min(kMaxFrames, n_t - f0);
+    for (int f = 0; f < p.n_t; ++f) {
+      p.t[f] = ts[f0 + f];
+      p.out_means[f] = outs[f0 + f].means;
+      p.out_log_scales[f] = outs[f0 + f].log_scales;
+      p.out_quats[f] = outs[f0 + f].quats;
+    }
+    cudaError_t e = launch_deform(p, s);
+    if (e != cudaSuccess) return cuda_fail(e, "deform launch");
+  }
+  return FGS_OK;
+}
+
+__global__ void fill_bg_kernel(float* img, int w, int h, float r, float g, float b, float* fT, uint32_t* nc,
+                               uint32_t* ne) {
+  const size_t hw = (size_t)w * h;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hw; i += (size_t)gridDim.x * blockDim.x) {
+    img[i] = r; img[hw + i] = g; img[2 * hw + i] = b;
+    if (fT) fT[i] = 1.f;
+    if (nc) nc[i] = 0;
+    if (ne) ne[i] = 0;
+  }
+}
+
+int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* images, int n_frames, void* ws,
+                size_t ws_bytes, const fgs_render_aux* aux, cudaStream_t s) {
+  FGS_CHECK(cams && defs && images && n_frames >= 0, "null camera/deformed/image arrays");
+  if (n_frames == 0) return FGS_OK;
+  int rc;
+  for (int f = 0; f < n_frames; ++f) {
+    if ((rc = check_camera(&cams[f])) != FGS_OK) return rc;
+    FGS_CHECK(cams[f].width == cams[0].width && cams[f].height == cams[0].height,
+              "all frames of a batch must share width/height");
+    if ((rc = check_deformed(&defs[f], defs[0].n, defs[0].sh_degree, false)) != FGS_OK) return rc;
+    FGS_CHECK(images[f] && aligned16(images[f]), "image pointer NULL or misaligned");
+  }
+  FGS_CHECK(defs[0].n >= 0 && defs[0].n < ((int64_t)1 << 31), "n out of range");
+  FGS_CHECK(defs[0].sh_degree >= 0 && defs[0].sh_degree <= 3, "sh_degree must be in [0,3]");
+  const int W = cams[0].width, H = cams[0].height;
+  const int64_t n = defs[0].n;
+  FGS_CHECK(ws && aligned16(ws), "workspace NULL or misaligned");
+  const size_t per = (ws_bytes / (size_t)n_frames) & ~(size_t)255;
+  const int64_t cap = capacity_for(n, W, H, per);
+  FGS_CHECK(cap > 0 || n == 0, "workspace too small (see fgs_render_workspace_bytes)");
+  if (n == 0) {
+    for (int f = 0; f < n_frames; ++f) {
+      fill_bg_kernel<<<64, 256, 0, s>>>(images[f], W, H, cams[f].bg[0], cams[f].bg[1], cams[f].bg[2],
+                                        aux ? aux->final_T : nullptr, aux ? aux->n_contrib : nullptr,
+                                        aux ? aux->n_evaluated : nullptr);
+      // counters of an empty frame: zero instances, no overflow
+      cudaMemsetAsync((char*)ws + (size_t)f * per, 0, 64, s);
+    }
+    if (aux && aux->n_instances) cudaMemsetAsync(aux->n_instances, 0, 4, s);
+    if (aux && aux->ranges) cudaMemsetAsync(aux->ranges, 0, sizeof(uint32_t) * 2 * ((W + 15) / 16) * ((H + 15) / 16), s);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? FGS_OK : cuda_fail(e, "background fill");
+  }
+  RenderBatch local;
+  memset(&local, 0, sizeof(local));
+  local.L = make_layout(n, W, H, cap);
+  local.n = n;
+  local.sh_degree = defs[0].sh_degree;
+  local.width = W; local.height = H;
+  local.gx = local.L.gx; local.gy = local.L.gy; local.ntiles = local.L.ntiles;
+  local.ws_stride = per;
+  for (int f0 = 0; f0 < n_frames; f0 += kMaxFrames) {
+    local.n_frames = std::min(kMaxFrames, n_frames - f0);
+    local.ws = (char*)ws + (size_t)f0 * per;
+    for (int f = 0; f < local.n_frames; ++f) {
+      const fgs_camera& c = cams[f0 + f];
+      FrameCam& fc = local.cam[f];
+      memcpy(fc.R, c.R, sizeof(fc.R));
+      memcpy(fc.t, c.t, sizeof(fc.t));
+      fc.fx = c.fx; fc.fy = c.fy; fc.cx = c.cx; fc.cy = c.cy;
+      memcpy(fc.bg, c.bg, sizeof(fc.bg));
+      const fgs_deformed& d = defs[f0 + f];
+      local.means[f] = d.means; local.log_scales[f] = d.log_scales; local.quats[f] = d.quats;
+      local.opacity[f] = d.opacity_logits; local.sh[f] = d.sh;
+      local.image[f] = images[f0 + f];
+      local.final_T[f] = (aux && f0 + f == 0) ? aux->final_T : nullptr;
+      local.n_contrib[f] = (aux && f0 + f == 0) ? aux->n_contrib : nullptr;
+      local.n_eval[f] = (aux && f0 + f == 0) ? aux->n_evaluated : nullptr;
+    }
+    cudaError_t e = launch_render(local, s);
+    if (e != cudaSuccess) return cuda_fail(e, "render launch");
+    if (aux && f0 == 0) {
+      e = launch_debug_copy(local, *aux, s);
+      if (e != cudaSuccess) return cuda_fail(e, "debug copy");
+    }
+  }
+  return FGS_OK;
+}
+
+struct ProfRec { int stage; cudaEvent_t a, b; };
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<ProfRec> pending;
+  cudaEvent_t open[FGS_N_STAGES] = {};
+  double ms[FGS_N_STAGES] = {};
+  int64_t count[FGS_N_STAGES] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profiler& prof() { static Profiler p; return p; }
+std::atomic<int64_t> g_launches{0};
+
+}  // namespace
+
+void prof_mark(int stage, bool begin, cudaStream_t s) {
+  Profiler& P = prof();
+  if (!P.on || stage < 0 || stage >= FGS_N_STAGES) return;
+  std::lock_guard<std::mutex> lk(P.mu);
+  cudaEvent_t e = P.get();
+  cudaEventRecord(e, s);
+  if (begin) {
+    P.open[stage] = e;
+  } else if (P.open[stage]) {
+    P.pending.push_back({stage, P.open[stage], e});
+    P.open[stage] = nullptr;
+  }
+}
+
+void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+WsLayout make_layout(int64_t n, int width, int height, int64_t cap) {
+  WsLayout L;
+  L.n = n; L.cap = cap; L.width = width; L.height = height;
+  L.gx = (width + kTile - 1) / kTile;
+  L.gy = (height + kTile - 1) / kTile;
+  L.ntiles = L.gx * L.gy;
+  const int64_t items = std::max<int64_t>(std::max<int64_t>(n, cap), 1);
+  L.hist_tiles = (items + kSortTile - 1) / kSortTile;
+  L.scan_tiles = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  const size_t nn = (size_t)std::max<int64_t>(n, 1);
+  const size_t cc = (size_t)std::max<int64_t>(cap, 1);
+  L.cnt = take(64);
+  L.keys0 = take(4 * nn); L.vals0 = take(4 * nn); L.keys1 = take(4 * nn); L.vals1 = take(4 * nn);
+  L.tt = take(4 * nn);
+  L.rect = take(8 * nn);
+  L.rec = take(48 * nn);
+  L.radii = take(4 * nn);
+  L.offs = take(4 * nn);
+  L.partial = take(4 * (size_t)L.scan_tiles);
+  L.ranges = take(8 * (size_t)L.ntiles);
+  L.hist = take(4 * 256 * (size_t)L.hist_tiles);
+  L.ikey0 = take(4 * cc); L.ival0 = take(4 * cc); L.ikey1 = take(4 * cc); L.ival1 = take(4 * cc);
+  L.total = o;
+  return L;
+}
+
+int64_t capacity_for(int64_t n, int width, int height, size_t bytes) {
+  // total(cap) is non-decreasing in cap: binary search the largest cap that fits.
+  if (make_layout(n, width, height, 1).total > bytes) return 0;
+  int64_t lo = 1, hi = (int64_t)(bytes / 16) + 1;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (make_layout(n, width, height, mid).total <= bytes) lo = mid; else hi = mid - 1;
+  }
+  return std::min<int64_t>(lo, (int64_t)0xFFFFFFF0);
+}
+
+}  // namespace fgs
+
+using namespace fgs;
+
+extern "C" {
+
+int fgs_deform(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+               fgs_deformed* out, fgs_stream_t stream) {
+  if (!g) return fail(FGS_E_INVALID, "gaussians is NULL");
+  return deform_impl(g, field, mlp, &t, 1, 0, g->n, out, (cudaStream_t)stream);
+}
+
+int fgs_deform_range(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+                     int64_t begin, int64_t end, fgs_deformed* out, fgs_stream_t stream) {
+  return deform_impl(g, field, mlp, &t, 1, begin, end, out, (cudaStream_t)stream);
+}
+
+int fgs_deform_batch(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, const float* ts,
+                     int32_t n_t, fgs_deformed* outs, fgs_stream_t stream) {
+  if (!g) return fail(FGS_E_INVALID, "gaussians is NULL");
+  return deform_impl(g, field, mlp, ts, n_t, 0, g->n, outs, (cudaStream_t)stream);
+}
+
+size_t fgs_render_workspace_bytes(int64_t n, int32_t width, int32_t height, int64_t max_instances) {
+  if (n < 0 || width <= 0 || height <= 0 || max_instances < 1) return 0;
+  return make_layout(n, width, height, max_instances).total;
+}
+
+int fgs_render(const fgs_camera* cam, const fgs_deformed* g, float* image, void* ws, size_t ws_bytes,
+               fgs_stream_t stream) {
+  return render_impl(cam, g, &image, 1, ws, ws_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int fgs_render_batch(const fgs_camera* cams, const fgs_deformed* defs, float* const* images, int32_t n_frames,
+                     void* ws, size_t ws_bytes, fgs_stream_t stream) {
+  return render_impl(cams, defs, images, n_frames, ws, ws_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int fgs_render_debug(const fgs_camera* cam, const fgs_deformed* g, float* image, void* ws, size_t ws_bytes,
+                     const fgs_render_aux* aux, fgs_stream_t stream) {
+  if (!aux) return fail(FGS_E_INVALID, "aux is NULL");
+  return render_impl(cam, g, &image, 1, ws, ws_bytes, aux, (cudaStream_t)stream);
+}
+
+int fgs_render_status(const void* ws, size_t ws_bytes, int32_t n_frames, fgs_stream_t stream) {
+  if (!ws || n_frames <= 0) return fail(FGS_E_INVALID, "bad workspace/n_frames");
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  const size_t per = (ws_bytes / (size_t)n_frames) & ~(size_t)255;
+  for (int f = 0; f < n_frames; ++f) {
+    uint32_t flag = 0;
+    e = cudaMemcpy(&flag, (const char*)ws + (size_t)f * per + 8, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "status read");
+    if (flag) return fail(FGS_E_CAPACITY, "instance capacity overflow in frame " + std::to_string(f));
+  }
+  return FGS_OK;
+}
+
+int fgs_frames(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, const float* ts,
+               const fgs_camera* cams, int32_t n_frames, fgs_deformed* defs_scratch, float* const* images,
+               void* ws, size_t ws_bytes, fgs_stream_t stream) {
+  if (!g) return fail(FGS_E_INVALID, "gaussians is NULL");
+  int rc = deform_impl(g, field, mlp, ts, n_frames, 0, g->n, defs_scratch, (cudaStream_t)stream);
+  if (rc != FGS_OK) return rc;
+  return render_impl(cams, defs_scratch, images, n_frames, ws, ws_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int fgs_profile_enable(int enable) {
+  Profiler& P = prof();
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.on = enable != 0;
+  return FGS_OK;
+}
+
+int fgs_profile_read(double* ms, int64_t* launches) {
+  Profiler& P = prof();
+  std::lock_guard<std::mutex> lk(P.mu);
+  for (const ProfRec& r : P.pending) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "profile event sync");
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    P.ms[r.stage] += t;
+    P.count[r.stage] += 1;
+    P.pool.push_back(r.a);
+    P.pool.push_back(r.b);
+  }
+  P.pending.clear();
+  for (int i = 0; i < FGS_N_STAGES; ++i) {
+    if (ms) ms[i] = P.ms[i];
+    if (launches) launches[i] = P.count[i];
+    P.ms[i] = 0.0;
+    P.count[i] = 0;
+  }
+  return FGS_OK;
+}
+
+int64_t fgs_launch_count(void) { return g_launches.load(); }
+
+// ---- end to end with host buffers -------------------------------------------------------------
+namespace {
+struct HostLayout {
+  size_t means, log_scales, quats, opac, sh, planes[FGS_MAX_SCALES][FGS_PLANES], mlp[8], defs, images, render;
+  size_t plane_bytes[FGS_MAX_SCALES][FGS_PLANES], mlp_bytes[8];
+  size_t per_def, per_img, per_render, total;
+};
+HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, int F, int W, int H,
+                       int64_t cap) {
+  HostLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
+  const size_t n = (size_t)g->n, K = (size_t)(g->sh_degree + 1) * (g->sh_degree + 1);
+  L.means = take(12 * n); L.log_scales = take(12 * n); L.quats = take(16 * n); L.opac = take(4 * n);
+  L.sh = take(12 * K * n);
+  for (int l = 0; l < h->n_scales; ++l)
+    for (int p = 0; p < FGS_PLANES; ++p) {
+      const size_t nb = p < 3 ? (size_t)h->res[l] : (size_t)h->t_res;
+      L.plane_bytes[l][p] = nb * (size_t)h->res[l] * (size_t)h->feat * 4;
+      L.planes[l][p] = take(L.plane_bytes[l][p]);
+    }
+  const size_t Wd = (size_t)m->width, In = (size_t)m->in_dim;
+  const size_t mb[8] = {Wd * In * 4, Wd * 4, 3 * Wd * 4, 12, 4 * Wd * 4, 16, 3 * Wd * 4, 12};
+  for (int i = 0; i < 8; ++i) { L.mlp_bytes[i] = mb[i]; L.mlp[i] = take(mb[i]); }
+  L.per_def = align256(12 * n) * 2 + align256(16 * n);
+  L.defs = take(L.per_def * (size_t)F);
+  L.per_img = align256((size_t)3 * W * H * 4);
+  L.images = take(L.per_img * (size_t)F);
+  L.per_render = make_layout(g->n, W, H, cap).total;
+  L.render = take(L.per_render * (size_t)F);
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+size_t fgs_frames_host_workspace_bytes(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
+                                       int32_t n_frames, int32_t width, int32_t height, int64_t max_instances) {
+  if (!g || !field || !mlp || n_frames <= 0 || width <= 0 || height <= 0 || max_instances < 1) return 0;
+  if (g->n < 0 || field->n_scales < 1 || field->n_scales > FGS_MAX_SCALES) return 0;
+  return host_layout(g, field, mlp, n_frames, width, height, max_instances).total;
+}
+
+int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_mlp* mh, const float* ts,
+                    const fgs_camera* cams, int32_t F, float* const* images_host, void* dev_ws,
+                    size_t dev_ws_bytes, fgs_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  FGS_CHECK(gh && hh && mh && ts && cams && images_host && dev_ws && F > 0, "null argument");
+  int rc;
+  if ((rc = check_gaussians(gh)) != FGS_OK) return rc;
+  if ((rc = check_field(hh, mh)) != FGS_OK) return rc;
+  if ((rc = check_camera(&cams[0])) != FGS_OK) return rc;
+  for (int f = 0; f < F; ++f) FGS_CHECK(images_host[f], "null host image");
+  const int W = cams[0].width, H = cams[0].height;
+  const HostLayout L0 = host_layout(gh, hh, mh, F, W, H, 1);
+  FGS_CHECK(dev_ws_bytes >= L0.total, "device workspace too small");
+  const size_t fixed = L0.total - L0.per_render * (size_t)F;
+  const int64_t cap = capacity_for(gh->n, W, H, ((dev_ws_bytes - fixed) / (size_t)F) & ~(size_t)255);
+  FGS_CHECK(cap > 0, "device workspace too small");
+  const HostLayout L = host_layout(gh, hh, mh, F, W, H, cap);
+  char* d = (char*)dev_ws;
+  const size_t n = (size_t)gh->n, K = (size_t)(gh->sh_degree + 1) * (gh->sh_degree + 1);
+  auto h2d = [&](size_t off, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(d + off, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  cudaError_t e = cudaSuccess;
+  if (n) {
+    e = h2d(L.means, gh->means, 12 * n);
+    if (e == cudaSuccess) e = h2d(L.log_scales, gh->log_scales, 12 * n);
+    if (e == cudaSuccess) e = h2d(L.quats, gh->quats, 16 * n);
+    if (e == cudaSuccess) e = h2d(L.opac, gh->opacity_logits, 4 * n);
+    if (e == cudaSuccess) e = h2d(L.sh, gh->sh, 12 * K * n);
+  }
+  fgs_hexplanes hd = *hh;
+  for (int l = 0; l < hh->n_scales && e == cudaSuccess; ++l)
+    for (int p = 0; p < FGS_PLANES && e == cudaSuccess; ++p) {
+      e = h2d(L.planes[l][p], hh->planes[l][p], L.plane_bytes[l][p]);
+      hd.planes[l][p] = (const float*)(d + L.planes[l][p]);
+    }
+  fgs_mlp md = *mh;
+  const float* srcs[8] = {mh->w_d, mh->b_d, mh->w_x, mh->b_x, mh->w_r, mh->b_r, mh->w_s, mh->b_s};
+  const float** dsts[8] = {&md.w_d, &md.b_d, &md.w_x, &md.b_x, &md.w_r, &md.b_r, &md.w_s, &md.b_s};
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
+    e = h2d(L.mlp[i], srcs[i], L.mlp_bytes[i]);
+    *dsts[i] = (const float*)(d + L.mlp[i]);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
+  fgs_gaussians gd = *gh;
+  gd.means = (const float*)(d + L.means); gd.log_scales = (const float*)(d + L.log_scales);
+  gd.quats = (const float*)(d + L.quats); gd.opacity_logits = (const float*)(d + L.opac);
+  gd.sh = (const float*)(d + L.sh);
+  std::vector<fgs_deformed> defs(F);
+  std::vector<float*> imgs(F);
+  for (int f = 0; f < F; ++f) {
+    char* base = d + L.defs + (size_t)f * L.per_def;
+    defs[f].n = gh->n; defs[f].sh_degree = gh->sh_degree;
+    defs[f].means = (float*)base;
+    defs[f].log_scales = (float*)(base + align256(12 * n));
+    defs[f].quats = (float*)(base + 2 * align256(12 * n));
+    defs[f].opacity_logits = gd.opacity_logits; defs[f].sh = gd.sh;
+    imgs[f] = (float*)(d + L.images + (size_t)f * L.per_img);
+  }
+  rc = fgs_frames(&gd, &hd, &md, ts, cams, F, defs.data(), imgs.data(), d + L.render, L.per_render * (size_t)F,
+                  stream);
+  if (rc != FGS_OK) return rc;
+  for (int f = 0; f < F; ++f) {
+    e = cudaMemcpyAsync(images_host[f], imgs[f], (size_t)3 * W * H * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+  }
+  return FGS_OK;
+}
+
+const char* fgs_last_error(void) { return g_err.c_str(); }
+
+
+const char* fgs_version(void) { return "fgs 0.1 (4D-GS forward, sm_100a)"; }
+
+}  // extern "C"

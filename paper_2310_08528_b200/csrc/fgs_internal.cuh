@@ -1,0 +1,102 @@
+// Internal declarations shared by the sm_100a kernels of libfgs.so (never by the oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fgs.h"
+
+namespace fgs {
+
+constexpr int kTile = FGS_TILE;              // 16x16 pixel tiles ([3dgs] rasterizer, reading R8)
+constexpr int kMaxFrames = 32;               // frames per launch (kernel-parameter table)
+constexpr int kSortThreads = 256;            // radix sort CTA
+constexpr int kSortItems = 8;                // items per thread
+constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per sort tile
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;   // 4096 per scan tile
+
+// Per-frame workspace layout (all offsets in bytes from the frame's slice, 256-B aligned).
+struct WsLayout {
+  int64_t n = 0, cap = 0;
+  int width = 0, height = 0, gx = 0, gy = 0, ntiles = 0;
+  int64_t hist_tiles = 0;    // max sort tiles (over n and cap)
+  int64_t scan_tiles = 0;    // scan tiles over n
+  size_t cnt = 0;            // uint32[8]: 0 n, 1 M clamped, 2 overflow, 3 M raw
+  size_t keys0 = 0, vals0 = 0, keys1 = 0, vals1 = 0;    // uint32[n] depth sort ping-pong
+  size_t tt = 0;             // uint32[n] tiles_touched
+  size_t rect = 0;           // uint2[n]  (x0 | y0<<16, x1 | y1<<16)
+  size_t rec = 0;            // float4[n][3] blend records
+  size_t radii = 0;          // int32[n]
+  size_t offs = 0;           // uint32[n] exclusive scan of tiles_touched in depth order
+  size_t partial = 0;        // uint32[scan_tiles]
+  size_t ikey0 = 0, ival0 = 0, ikey1 = 0, ival1 = 0;    // uint32[cap] tile sort ping-pong
+  size_t hist = 0;           // uint32[256 * hist_tiles]
+  size_t ranges = 0;         // uint2[ntiles]
+  size_t total = 0;
+};
+
+WsLayout make_layout(int64_t n, int width, int height, int64_t cap);
+// Largest capacity whose layout fits in `bytes` (0 if none).
+int64_t capacity_for(int64_t n, int width, int height, size_t bytes);
+
+// Frame batch table passed by value to the render kernels.
+struct FrameCam {
+  float R[9], t[3];
+  float fx, fy, cx, cy;
+  float bg[3];
+};
+struct RenderBatch {
+  int n_frames;
+  int64_t n;
+  int sh_degree;
+  int width, height, gx, gy, ntiles;
+  char* ws;                  // frame f slice = ws + f * ws_stride
+  size_t ws_stride;
+  WsLayout L;
+  FrameCam cam[kMaxFrames];
+  const float* means[kMaxFrames];
+  const float* log_scales[kMaxFrames];
+  const float* quats[kMaxFrames];
+  const float* opacity[kMaxFrames];
+  const float* sh[kMaxFrames];
+  float* image[kMaxFrames];
+  float* final_T[kMaxFrames];      // optional
+  uint32_t* n_contrib[kMaxFrames]; // optional
+  uint32_t* n_eval[kMaxFrames];    // optional
+};
+
+// Deformation launch (times batched over frames of the same model).
+struct DeformBatch {
+  int n_t;
+  int64_t begin, end;        // Gaussian range
+  const float* means;
+  const float* log_scales;
+  const float* quats;
+  int n_scales, feat, t_res;
+  int res[FGS_MAX_SCALES];
+  float bmin[3], ext[3];
+  const float* planes[FGS_MAX_SCALES][FGS_PLANES];
+  int in_dim, width;
+  const float *w_d, *b_d, *w_x, *b_x, *w_r, *b_r, *w_s, *b_s;
+  float t[kMaxFrames];
+  float* out_means[kMaxFrames];
+  float* out_log_scales[kMaxFrames];
+  float* out_quats[kMaxFrames];
+};
+
+// Kernel launchers (return cudaError_t of the launch).
+cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);
+cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
+cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
+
+// Profiling / launch accounting (api.cu).
+void prof_mark(int stage, bool begin, cudaStream_t s);
+void note_launches(int64_t k);
+
+template <typename T>
+__host__ __device__ inline T* ws_ptr(char* base, size_t stride, int f, size_t off) {
+  return reinterpret_cast<T*>(base + (size_t)f * stride + off);
+}
+
+}  // namespace fgs

@@ -1,0 +1,345 @@
+"""Thin ctypes binding of libfgs.so (include/fgs.h) — argument marshalling only.
+
+Every step of the path runs in the sm_100a kernels of libfgs.so; this module only
+builds the C structs from torch CUDA tensors (device memory) and passes
+`torch.cuda.current_stream()`.  There is no CPU fallback: if the library cannot
+be loaded the calls raise.  Function names are the C ABI's.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfgs.so")
+
+FGS_OK, FGS_E_INVALID, FGS_E_CUDA, FGS_E_CAPACITY, FGS_E_NOTIMPL = 0, -1, -2, -3, -4
+MAX_SCALES, PLANES, TILE = 4, 6, 16
+
+
+class FgsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"fgs error {code}: {msg}")
+        self.code = code
+
+
+class fgs_gaussians(ctypes.Structure):
+    _fields_ = [("n", c_int64), ("sh_degree", c_int32), ("means", c_void_p), ("log_scales", c_void_p),
+                ("quats", c_void_p), ("opacity_logits", c_void_p), ("sh", c_void_p)]
+
+
+class fgs_hexplanes(ctypes.Structure):
+    _fields_ = [("n_scales", c_int32), ("feat", c_int32), ("t_res", c_int32),
+                ("res", c_int32 * MAX_SCALES), ("bmin", c_float * 3), ("bmax", c_float * 3),
+                ("planes", (c_void_p * PLANES) * MAX_SCALES)]
+
+
+class fgs_mlp(ctypes.Structure):
+    _fields_ = [("in_dim", c_int32), ("width", c_int32)] + [
+        (k, c_void_p) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")]
+
+
+class fgs_deformed(ctypes.Structure):
+    _fields_ = [("n", c_int64), ("sh_degree", c_int32), ("means", c_void_p), ("log_scales", c_void_p),
+                ("quats", c_void_p), ("opacity_logits", c_void_p), ("sh", c_void_p)]
+
+
+class fgs_camera(ctypes.Structure):
+    _fields_ = [("R", c_float * 9), ("t", c_float * 3), ("fx", c_float), ("fy", c_float),
+                ("cx", c_float), ("cy", c_float), ("width", c_int32), ("height", c_int32),
+                ("bg", c_float * 3)]
+
+
+class fgs_render_aux(ctypes.Structure):
+    _fields_ = [(k, c_void_p) for k in ("radii", "rect", "mean2d", "depth_key", "tiles_touched",
+                                        "n_instances", "sorted_tile", "sorted_gid", "ranges",
+                                        "final_T", "n_contrib", "n_evaluated")]
+
+
+_LIB = None
+EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_batch", "fgs_render_workspace_bytes",
+           "fgs_render", "fgs_render_batch", "fgs_render_debug", "fgs_render_status", "fgs_frames",
+           "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_profile_enable", "fgs_profile_read",
+           "fgs_launch_count", "fgs_last_error", "fgs_version")
+STAGES = ("deform", "preprocess", "depth_sort", "offsets", "duplicate", "tile_sort", "ranges", "blend")
+
+
+def lib():
+    """Load libfgs.so (raises if it is missing: there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise FgsError(FGS_E_CUDA, f"{LIB_PATH} not built: run `python -m paper_2310_08528_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P = POINTER
+        L.fgs_deform.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float, P(fgs_deformed), c_void_p]
+        L.fgs_deform_range.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float, c_int64, c_int64,
+                                       P(fgs_deformed), c_void_p]
+        L.fgs_deform_batch.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(c_float), c_int32,
+                                       P(fgs_deformed), c_void_p]
+        L.fgs_render_workspace_bytes.argtypes = [c_int64, c_int32, c_int32, c_int64]
+        L.fgs_render_workspace_bytes.restype = c_size_t
+        L.fgs_render.argtypes = [P(fgs_camera), P(fgs_deformed), c_void_p, c_void_p, c_size_t, c_void_p]
+        L.fgs_render_batch.argtypes = [P(fgs_camera), P(fgs_deformed), P(c_void_p), c_int32, c_void_p, c_size_t,
+                                       c_void_p]
+        L.fgs_render_debug.argtypes = [P(fgs_camera), P(fgs_deformed), c_void_p, c_void_p, c_size_t,
+                                       P(fgs_render_aux), c_void_p]
+        L.fgs_render_status.argtypes = [c_void_p, c_size_t, c_int32, c_void_p]
+        L.fgs_frames.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(c_float), P(fgs_camera),
+                                 c_int32, P(fgs_deformed), P(c_void_p), c_void_p, c_size_t, c_void_p]
+        L.fgs_frames_host_workspace_bytes.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_int32,
+                                                      c_int32, c_int32, c_int64]
+        L.fgs_frames_host_workspace_bytes.restype = c_size_t
+        L.fgs_frames_host.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(c_float), P(fgs_camera),
+                                      c_int32, P(c_void_p), c_void_p, c_size_t, c_void_p]
+        L.fgs_profile_enable.argtypes = [c_int]
+        L.fgs_profile_read.argtypes = [P(ctypes.c_double), P(c_int64)]
+        L.fgs_launch_count.restype = c_int64
+        L.fgs_last_error.restype = c_char_p
+        L.fgs_version.restype = c_char_p
+        for name in EXPORTS:
+            if name not in ("fgs_render_workspace_bytes", "fgs_frames_host_workspace_bytes", "fgs_launch_count",
+                            "fgs_last_error", "fgs_version"):
+                getattr(L, name).restype = c_int
+        _LIB = L
+    return _LIB
+
+
+def _check(rc):
+    if rc != FGS_OK:
+        raise FgsError(rc, lib().fgs_last_error().decode())
+    return rc
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return c_void_p(0 if t is None else t.data_ptr())
+
+
+# ---------------------------------------------------------------- the C calls
+def fgs_deform(g, field, mlp, t, out, stream=None):
+    return _check(lib().fgs_deform(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
+                                   ctypes.byref(out), _stream(stream)))
+
+
+def fgs_deform_range(g, field, mlp, t, begin, end, out, stream=None):
+    return _check(lib().fgs_deform_range(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
+                                         c_int64(begin), c_int64(end), ctypes.byref(out), _stream(stream)))
+
+
+def fgs_deform_batch(g, field, mlp, ts: Sequence[float], outs: Sequence[fgs_deformed], stream=None):
+    n = len(ts)
+    tarr = (c_float * max(n, 1))(*[float(x) for x in ts])
+    oarr = (fgs_deformed * max(n, 1))(*outs)
+    return _check(lib().fgs_deform_batch(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), tarr, n, oarr,
+                                         _stream(stream)))
+
+
+def fgs_render_workspace_bytes(n, width, height, max_instances):
+    return int(lib().fgs_render_workspace_bytes(n, width, height, max_instances))
+
+
+def fgs_render(cam, g, image, ws, stream=None):
+    return _check(lib().fgs_render(ctypes.byref(cam), ctypes.byref(g), _ptr(image), _ptr(ws), ws.numel(),
+                                   _stream(stream)))
+
+
+def fgs_render_batch(cams, defs, images, ws, stream=None):
+    F = len(cams)
+    carr = (fgs_camera * max(F, 1))(*cams)
+    darr = (fgs_deformed * max(F, 1))(*defs)
+    iarr = (c_void_p * max(F, 1))(*[im.data_ptr() for im in images])
+    return _check(lib().fgs_render_batch(carr, darr, iarr, F, _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def fgs_render_debug(cam, g, image, ws, aux, stream=None):
+    return _check(lib().fgs_render_debug(ctypes.byref(cam), ctypes.byref(g), _ptr(image), _ptr(ws), ws.numel(),
+                                         ctypes.byref(aux), _stream(stream)))
+
+
+def fgs_render_status(ws, n_frames=1, stream=None):
+    return _check(lib().fgs_render_status(_ptr(ws), ws.numel(), n_frames, _stream(stream)))
+
+
+def fgs_frames(g, field, mlp, ts, cams, defs_scratch, images, ws, stream=None):
+    F = len(ts)
+    tarr = (c_float * max(F, 1))(*[float(x) for x in ts])
+    carr = (fgs_camera * max(F, 1))(*cams)
+    darr = (fgs_deformed * max(F, 1))(*defs_scratch)
+    iarr = (c_void_p * max(F, 1))(*[im.data_ptr() for im in images])
+    return _check(lib().fgs_frames(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), tarr, carr, F, darr,
+                                   iarr, _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def fgs_frames_host_workspace_bytes(g_host, field_host, mlp_host, n_frames, width, height, max_instances):
+    return int(lib().fgs_frames_host_workspace_bytes(ctypes.byref(g_host), ctypes.byref(field_host),
+                                                     ctypes.byref(mlp_host), n_frames, width, height,
+                                                     max_instances))
+
+
+def fgs_frames_host(g_host, field_host, mlp_host, ts, cams, images_host, dev_ws, stream=None):
+    """images_host: list of pinned CPU float32 tensors [3,H,W]; dev_ws: device uint8 tensor."""
+    F = len(ts)
+    tarr = (c_float * max(F, 1))(*[float(x) for x in ts])
+    carr = (fgs_camera * max(F, 1))(*cams)
+    iarr = (c_void_p * max(F, 1))(*[im.data_ptr() for im in images_host])
+    return _check(lib().fgs_frames_host(ctypes.byref(g_host), ctypes.byref(field_host), ctypes.byref(mlp_host),
+                                        tarr, carr, F, iarr, _ptr(dev_ws), dev_ws.numel(), _stream(stream)))
+
+
+def fgs_profile_enable(enable=True):
+    return _check(lib().fgs_profile_enable(1 if enable else 0))
+
+
+def fgs_profile_read():
+    """Returns {stage: (ms, launches)} accumulated since the last read (synchronises)."""
+    ms = (ctypes.c_double * len(STAGES))()
+    cnt = (c_int64 * len(STAGES))()
+    _check(lib().fgs_profile_read(ms, cnt))
+    return {name: (ms[i], cnt[i]) for i, name in enumerate(STAGES)}
+
+
+def fgs_launch_count():
+    return int(lib().fgs_launch_count())
+
+
+def fgs_last_error():
+    return lib().fgs_last_error().decode()
+
+
+def fgs_version():
+    return lib().fgs_version().decode()
+
+
+# ---------------------------------------------------------------- marshalling helpers
+def make_camera(cam) -> fgs_camera:
+    """inputs.Camera -> fgs_camera (host struct)."""
+    c = fgs_camera()
+    c.R[:] = [float(v) for v in np.asarray(cam.R, np.float32).ravel()]
+    c.t[:] = [float(v) for v in np.asarray(cam.t, np.float32).ravel()]
+    c.fx, c.fy, c.cx, c.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.bg[:] = [float(v) for v in np.asarray(cam.bg, np.float32).ravel()]
+    return c
+
+
+class HostScene:
+    """A Scene's arrays in pinned host memory + C structs whose pointers are HOST pointers
+    (the inputs of fgs_frames_host, i.e. the end-to-end path)."""
+
+    def __init__(self, scene):
+        import torch
+
+        def T(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).pin_memory()
+
+        self.scene = scene
+        self.n = scene.n
+        self.arrays = {k: T(getattr(scene, k)) for k in ("means", "log_scales", "quats", "opacity_logits", "sh")}
+        a = self.arrays
+        self.g = fgs_gaussians(self.n, scene.sh_degree, a["means"].data_ptr(), a["log_scales"].data_ptr(),
+                               a["quats"].data_ptr(), a["opacity_logits"].data_ptr(), a["sh"].data_ptr())
+        f = scene.field
+        self.planes = [[T(P) for P in ps] for ps in f.planes]
+        hp = fgs_hexplanes()
+        hp.n_scales, hp.feat, hp.t_res = len(f.res), f.feat, f.t_res
+        for l, R in enumerate(f.res):
+            hp.res[l] = R
+            for p in range(PLANES):
+                hp.planes[l][p] = self.planes[l][p].data_ptr()
+        hp.bmin[:] = [float(v) for v in f.bmin]
+        hp.bmax[:] = [float(v) for v in f.bmax]
+        self.field = hp
+        m = scene.mlp
+        self.mlp_t = {k: T(getattr(m, k)) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")}
+        mm = fgs_mlp()
+        mm.in_dim, mm.width = m.in_dim, m.width
+        for k, v in self.mlp_t.items():
+            setattr(mm, k, v.data_ptr())
+        self.mlp = mm
+        self.cams = [make_camera(c) for c in scene.cameras]
+        self.times = [float(t) for t in scene.times]
+
+    def h2d_bytes(self):
+        tot = sum(v.numel() * 4 for v in self.arrays.values())
+        tot += sum(P.numel() * 4 for ps in self.planes for P in ps)
+        tot += sum(v.numel() * 4 for v in self.mlp_t.values())
+        return tot
+
+
+class DeviceScene:
+    """A Scene's arrays resident in device memory (torch tensors) + the C structs over them."""
+
+    def __init__(self, scene, device="cuda"):
+        import torch
+
+        def T(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device)
+
+        self.scene = scene
+        self.device = device
+        self.n = scene.n
+        self.sh_degree = scene.sh_degree
+        self.means, self.log_scales, self.quats = T(scene.means), T(scene.log_scales), T(scene.quats)
+        self.opacity_logits, self.sh = T(scene.opacity_logits), T(scene.sh)
+        f = scene.field
+        self.planes = [[T(P) for P in ps] for ps in f.planes]
+        m = scene.mlp
+        self.mlp_t = {k: T(getattr(m, k)) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")}
+        self.g = fgs_gaussians(self.n, self.sh_degree, self.means.data_ptr(), self.log_scales.data_ptr(),
+                               self.quats.data_ptr(), self.opacity_logits.data_ptr(), self.sh.data_ptr())
+        hp = fgs_hexplanes()
+        hp.n_scales, hp.feat, hp.t_res = len(f.res), f.feat, f.t_res
+        for l, R in enumerate(f.res):
+            hp.res[l] = R
+            for p in range(PLANES):
+                hp.planes[l][p] = self.planes[l][p].data_ptr()
+        hp.bmin[:] = [float(v) for v in f.bmin]
+        hp.bmax[:] = [float(v) for v in f.bmax]
+        self.field = hp
+        mm = fgs_mlp()
+        mm.in_dim, mm.width = m.in_dim, m.width
+        for k, v in self.mlp_t.items():
+            setattr(mm, k, v.data_ptr())
+        self.mlp = mm
+        self.cams = [make_camera(c) for c in scene.cameras]
+        self.times = [float(t) for t in scene.times]
+
+    def alloc_deformed(self, n_frames=1):
+        """Device output buffers for n_frames deformations; returns (structs, tensors)."""
+        import torch
+        outs, tens = [], []
+        for _ in range(n_frames):
+            X = torch.empty((self.n, 3), dtype=torch.float32, device=self.device)
+            S = torch.empty((self.n, 3), dtype=torch.float32, device=self.device)
+            Q = torch.empty((self.n, 4), dtype=torch.float32, device=self.device)
+            tens.append({"means": X, "log_scales": S, "quats": Q})
+            d = self.deformed_struct(X, S, Q)
+            d._keep = (X, S, Q)        # the struct owns its device buffers (raw pointers inside)
+            outs.append(d)
+        return outs, tens
+
+    def deformed_struct(self, means, log_scales, quats) -> fgs_deformed:
+        return fgs_deformed(self.n, self.sh_degree, means.data_ptr(), log_scales.data_ptr(), quats.data_ptr(),
+                            self.opacity_logits.data_ptr(), self.sh.data_ptr())
+
+    def canonical_struct(self) -> fgs_deformed:
+        """G itself as an fgs_deformed (render the undeformed scene, e.g. the warm-up / static case)."""
+        return self.deformed_struct(self.means, self.log_scales, self.quats)
+
+    def alloc_workspace(self, n_frames=1, max_instances=None, width=None, height=None):
+        import torch
+        W = self.scene.cameras[0].width if width is None else width
+        H = self.scene.cameras[0].height if height is None else height
+        cap = max(16 * self.n, 1024) if max_instances is None else max_instances
+        per = fgs_render_workspace_bytes(self.n, W, H, cap)
+        return torch.empty(per * n_frames, dtype=torch.uint8, device=self.device)

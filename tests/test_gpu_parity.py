@@ -1,0 +1,203 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star):
+  * deformed means / log-scales / raw quats: max |err| <= 1e-4 (also on the stress heads N(0,1));
+  * integer work (radii, rects, tiles_touched, depth keys, per-tile ordered lists) bit-exact except
+    boundary Gaussians (within 1e-5 px of a tile-rule boundary, see oracle.render.BAND_PX);
+  * pixels: PSNR >= 60 dB over all pixels, max |err| <= 2e-3 over pixels whose blend decisions are
+    not within relative 1e-4 of a threshold (reading P1).
+Integer and pixel checks feed BOTH sides the GPU's fp32 G' (so the deform tolerance cannot move
+rects).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import render as OR
+from paper_2310_08528_b200 import fgs
+from paper_2310_08528_b200.inputs import make_scene, with_heads, with_max_opacity
+
+from gpu_util import compare_integer_work, compare_pixels, ensure_lib, gpu_deform, gpu_render_debug
+
+pytestmark = pytest.mark.gpu
+
+DEFORM_TOL = 1e-4
+PIX_TOL = 2e-3
+PSNR_MIN = 60.0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    ensure_lib()
+
+
+def _ds(scene):
+    return fgs.DeviceScene(scene)
+
+
+def _deform_err(scene, g, t):
+    ref = oracle.deform_ref(scene, t)
+    return max(float(np.max(np.abs(g[k].astype(np.float64) - ref[k]))) for k in ref)
+
+
+@pytest.mark.parametrize("variant", ["tiny", "tiny_stress", "dnerf_sub", "dnerf_sub_stress", "hyper_sub"])
+def test_deform_matches_oracle(variant):
+    if variant.startswith("tiny"):
+        s = make_scene("tiny", n=2011)                       # ragged last tile of 64
+    elif variant.startswith("dnerf"):
+        s = make_scene("dnerf", n=20_003, n_frames=3)
+    else:
+        s = make_scene("hypernerf", n=5_000, n_frames=2)
+    if variant.endswith("stress"):
+        s = with_heads(s, 1.0, seed=7, bias_sigma=0.5)
+    ds = _ds(s)
+    for t in list(s.times[:2]) + [0.0, 1.0]:
+        _, g, _ = gpu_deform(ds, float(t))
+        err = _deform_err(s, g, float(t))
+        assert err <= DEFORM_TOL, (variant, float(t), err)
+
+
+def test_deform_range_and_batch_bit_identical():
+    s = with_heads(make_scene("dnerf", n=9_001, n_frames=5), 0.3, seed=3)
+    ds = _ds(s)
+    t = float(s.times[2])
+    _, full, _ = gpu_deform(ds, t)
+    for (b, e) in ((0, 9001), (100, 4567), (4567, 9001), (63, 64)):
+        _, part, _ = gpu_deform(ds, t, b, e)
+        for k in full:
+            assert np.array_equal(part[k][b:e], full[k][b:e]), (k, b, e)
+            assert np.all(np.isnan(part[k][:b])) and np.all(np.isnan(part[k][e:]))
+    outs, tens = ds.alloc_deformed(len(s.times))
+    fgs.fgs_deform_batch(ds.g, ds.field, ds.mlp, [float(x) for x in s.times], outs)
+    for f, tf in enumerate(s.times):
+        _, single, _ = gpu_deform(ds, float(tf))
+        for k in single:
+            assert np.array_equal(tens[f][k].cpu().numpy(), single[k]), (f, k)
+
+
+def test_zero_heads_identity_on_gpu():
+    s = with_heads(make_scene("tiny"), 0.0)
+    ds = _ds(s)
+    _, g, _ = gpu_deform(ds, 0.37)
+    assert np.array_equal(g["means"], s.means) and np.array_equal(g["quats"], s.quats)
+    assert np.array_equal(g["log_scales"], s.log_scales)
+
+
+def _render_parity(scene, frame=0, tiles_subset=None, check_tiles=True):
+    ds = _ds(scene)
+    cam = scene.cameras[frame]
+    dstruct, g, _ = gpu_deform(ds, float(scene.times[frame]))
+    out = gpu_render_debug(ds, cam, dstruct)
+    assert out["status"] == fgs.FGS_OK
+    ref = OR.render_ref(g, scene.opacity_logits, scene.sh, scene.sh_degree, cam, tiles_subset=tiles_subset)
+    ints = compare_integer_work(out, ref["pre"], (ref["tiles"], ref["gids"], ref["ranges"]))
+    assert out["M"] == len(ref["tiles"]) or ints["n_boundary"] > 0
+    for k in ("radii", "rect", "tiles_touched", "depth_key"):
+        assert ints[k] == 0, ints
+    if check_tiles:
+        assert ints["tile_lists"] == 0, ints
+    pix = compare_pixels(out["image"], ref["image"], ref["flagged"])
+    assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, pix
+    m = np.isfinite(ref["final_T"])
+    assert np.max(np.abs(out["final_T"][m] - ref["final_T"][m])) <= PIX_TOL
+    return out, ref, ints, pix
+
+
+@pytest.mark.parametrize("W,H", [(64, 64), (70, 50), (33, 100)])
+def test_render_tiny_matches_oracle(W, H):
+    s = make_scene("tiny", width=W, height=H)
+    _render_parity(s)
+
+
+def test_render_tiny_stress_heads():
+    _render_parity(with_heads(make_scene("tiny", width=72, height=56), 0.2, seed=11))
+
+
+def test_render_low_opacity_bruteforce():
+    """north_star: tiled == brute force over all Gaussians at opacity <= 0.017 (oracle side), GPU == both."""
+    s = with_max_opacity(make_scene("tiny", n=800, width=48, height=40), 0.017)
+    out, ref, _, _ = _render_parity(s)
+    bf = OR.render_ref_bruteforce(oracle.deform_ref(s, float(s.times[0])), s.opacity_logits, s.sh, 0,
+                                  s.cameras[0], rect_predicate=False)
+    assert np.max(np.abs(out["image"] - bf["image"])) <= PIX_TOL
+
+
+def test_render_dnerf_full_size_sampled():
+    """D config at full size (100k, 800x800, SH 3): all integer work bit-exact (outside boundary
+    Gaussians); pixels on 60 sampled tiles + the busiest tiles."""
+    s = make_scene("dnerf", n_frames=2)
+    rng = np.random.default_rng(0)
+    tiles = sorted(set(rng.choice(2500, 50, replace=False).tolist()) | {1224, 1225, 1275})
+    _render_parity(s, frame=1, tiles_subset=tiles)
+
+
+def test_static_render_bit_identical_on_gpu():
+    """north_star: zero heads -> fgs_render(fgs_deform(G, t)) == fgs_render(G) bit-exact."""
+    s = with_heads(make_scene("tiny", width=80, height=72), 0.0)
+    ds = _ds(s)
+    dstruct, _, _ = gpu_deform(ds, 0.37)
+    a = gpu_render_debug(ds, s.cameras[0], dstruct)
+    b = gpu_render_debug(ds, s.cameras[0], ds.canonical_struct())
+    assert np.array_equal(a["image"], b["image"])
+
+
+def test_determinism_and_batch_equals_single():
+    import torch
+    s = make_scene("dnerf", n=30_000, width=256, height=200, n_frames=4)
+    ds = _ds(s)
+    outs, tens = ds.alloc_deformed(4)
+    fgs.fgs_deform_batch(ds.g, ds.field, ds.mlp, ds.times, outs)
+    ws = ds.alloc_workspace(4)
+    imgs = [torch.empty((3, 200, 256), device="cuda") for _ in range(4)]
+    fgs.fgs_render_batch(ds.cams, outs, imgs, ws)
+    fgs.fgs_render_status(ws, 4)
+    first = [im.cpu().numpy() for im in imgs]
+    fgs.fgs_render_batch(ds.cams, outs, imgs, ws)
+    for a, im in zip(first, imgs):
+        assert np.array_equal(a, im.cpu().numpy())
+    for f in range(4):
+        ws1 = ds.alloc_workspace(1)
+        im = torch.empty((3, 200, 256), device="cuda")
+        fgs.fgs_render(ds.cams[f], outs[f], im, ws1)
+        assert np.array_equal(im.cpu().numpy(), first[f])
+    # fgs_frames (deform + render in one call) gives the same images
+    scratch, _ = ds.alloc_deformed(4)
+    imgs2 = [torch.empty((3, 200, 256), device="cuda") for _ in range(4)]
+    fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, scratch, imgs2, ws)
+    for a, im in zip(first, imgs2):
+        assert np.array_equal(a, im.cpu().numpy())
+
+
+def test_empty_and_single_gaussian():
+    import torch
+    s = make_scene("tiny", n=0, width=40, height=24)
+    ds = _ds(s)
+    img = torch.full((3, 24, 40), float("nan"), device="cuda")
+    ws = ds.alloc_workspace(1)
+    fgs.fgs_render(ds.cams[0], ds.canonical_struct(), img, ws)
+    fgs.fgs_render_status(ws)
+    assert torch.all(img == 0)
+    s1 = make_scene("tiny", n=1, width=40, height=24)
+    _render_parity(s1)
+
+
+def test_capacity_overflow_reported():
+    import torch
+    s = make_scene("tiny")
+    ds = _ds(s)
+    ws = ds.alloc_workspace(1, max_instances=100)
+    img = torch.empty((3, 64, 64), device="cuda")
+    fgs.fgs_render(ds.cams[0], ds.canonical_struct(), img, ws)
+    with pytest.raises(fgs.FgsError) as e:
+        fgs.fgs_render_status(ws)
+    assert e.value.code == fgs.FGS_E_CAPACITY
+
+
+def test_nan_and_degenerate_gaussians_are_culled():
+    s = with_heads(make_scene("tiny", n=300), 0.0)   # zero heads: the zero quaternions survive deform
+    s.quats[:10] = 0.0            # zero quaternion -> NaN covariance -> culled
+    s.means[10:20] = np.nan
+    out, ref, _, _ = _render_parity(s, check_tiles=True)
+    assert np.all(out["radii"][:20] == 0) and np.all(out["tiles_touched"][:20] == 0)
