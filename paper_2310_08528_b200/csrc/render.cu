@@ -179,13 +179,21 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
     col[1] = fmaf(basis[k], __ldg(sh + 3 * k + 1), col[1]);
     col[2] = fmaf(basis[k], __ldg(sh + 3 * k + 2), col[2]);
   }
-  // ---- blend record: mean2d as hi/lo fp32 pairs (dx exact to ~1e-11 px), conic, opacity, rgb ----
+  // ---- blend record: mean2d as hi/lo fp32 pairs, conic pre-scaled to the log2 domain ----
+  //   p2 = A' dx^2 + B' dx dy + C' dy^2 = power * log2(e);  alpha = min(0.99, 2^(p2 + log2 o))
   const float mxh = (float)mx, myh = (float)my;
   const float mxl = (float)(mx - (double)mxh), myl = (float)(my - (double)myh);
   const double opac = 1.0 / (1.0 + exp(-(double)b.opacity[f][i]));
-  rec[3 * i + 0] = make_float4(mxh, myh, (float)(cc / det), (float)(-bb / det));
-  rec[3 * i + 1] = make_float4((float)(a / det), (float)opac, fmaxf(col[0], 0.f), fmaxf(col[1], 0.f));
-  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, 0.f);
+  const double L2E = 1.4426950408889634;
+  rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * L2E * cc / det), (float)(L2E * bb / det));
+  rec[3 * i + 1] = make_float4((float)(-0.5 * L2E * a / det), (float)log2(opac), fmaxf(col[0], 0.f),
+                               fmaxf(col[1], 0.f));
+  // Conservative per-Gaussian cull radius^2 for the blend's warp-box test: for any pixel at distance
+  // d from the mean, alpha <= o exp(-d^2 / (2 lambda_max(Sigma2))), so alpha < 1/255 (skipped anyway)
+  // whenever d^2 > 2 lambda_max (ln(255 o) + 0.01); margins cover fp32 evaluation error.
+  const double lam_max = mid + sqrt(fmax(0.0, mid * mid - det));
+  const double r2 = (2.0 * log(255.0 * opac) + 0.02) * lam_max * (1.0 + 1e-4) + 1e-3;
+  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, (float)r2);
 }
 
 // ------------------------------------------------------------------------------ radix sort
@@ -459,48 +467,81 @@ __global__ void ranges_kernel(const __grid_constant__ RenderBatch b, size_t keys
 
 // ------------------------------------------------------------------------------ blend (Eq. 4)
 __global__ void __launch_bounds__(256) blend_kernel(const __grid_constant__ RenderBatch b, size_t vals_off) {
+  // One CTA per 16x16 tile; warp w owns the 8x4 pixel box ((w&1)*8, (w>>1)*4) of the tile so that a
+  // per-warp conservative alpha bound can skip Gaussians for all 32 of its pixels at once.
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % b.gx, ty = tile / b.gx;
-  const int pxi = tx * kTile + (threadIdx.x & 15);
-  const int pyi = ty * kTile + (threadIdx.x >> 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bx0 = (warp & 1) * 8, by0 = (warp >> 1) * 4;          // box origin, tile-relative
+  const int pxi = tx * kTile + bx0 + (lane & 7);
+  const int pyi = ty * kTile + by0 + (lane >> 3);
   const bool inside = pxi < b.width && pyi < b.height;
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const uint32_t* gids = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, vals_off);
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
-  __shared__ float4 s0[256], s1[256], s2[256];
-  const float pxf = (float)pxi, pyf = (float)pyi;
+  __shared__ float4 s0[256], s1[256];
+  __shared__ float s2b[256], s2r[256];
+  const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
+  const float lx = (float)(bx0 + (lane & 7)), ly = (float)(by0 + (lane >> 3));   // tile-relative pixel
+  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, byh = (float)(by0 + 3);
   float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  uint32_t ncon = 0, neval = 0;
+  uint32_t ncon = 0, nev = rg.y - rg.x;     // list entries reached before termination (E basis)
   bool done = !inside;
   for (uint32_t start = rg.x; start < rg.y; start += 256) {
     if (__syncthreads_count(done) == 256) break;
     const uint32_t idx = start + threadIdx.x;
     if (idx < rg.y) {
       const uint32_t g = gids[idx];
-      s0[threadIdx.x] = rec[3 * g + 0];
+      float4 a = rec[3 * g + 0];
+      const float4 c = rec[3 * g + 2];
+      // tile-relative mean: (hi - origin) is exact, + lo keeps ~1e-6 px
+      a.x = (a.x - tx0) + c.y;
+      a.y = (a.y - ty0) + c.z;
+      s0[threadIdx.x] = a;
       s1[threadIdx.x] = rec[3 * g + 1];
-      s2[threadIdx.x] = rec[3 * g + 2];
+      s2b[threadIdx.x] = c.x;
+      s2r[threadIdx.x] = c.w;
     }
     __syncthreads();
     const int cnt = (int)min(256u, rg.y - start);
-    for (int j = 0; j < cnt && !done; ++j) {
-      ++neval;
-      const float4 a = s0[j], bq = s1[j], cq = s2[j];
-      const float dx = (a.x - pxf) + cq.y;       // m.x - px with the hi/lo split of m.x
-      const float dy = (a.y - pyf) + cq.z;
-      const float power = -0.5f * (a.z * dx * dx + bq.x * dy * dy) - a.w * dx * dy;
-      if (power > 0.f) continue;
-      const float alpha = fminf(kAlphaMax, bq.y * __expf(power));
-      if (alpha < kAlphaMin) continue;
-      const float test_T = T * (1.f - alpha);
-      if (test_T < kTMin) { done = true; break; }
-      const float w = alpha * T;
-      C0 = fmaf(bq.z, w, C0);
-      C1 = fmaf(bq.w, w, C1);
-      C2 = fmaf(cq.x, w, C2);
-      T = test_T;
-      ++ncon;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      if (__all_sync(0xffffffffu, done)) break;
+      // ---- warp-level cull: lane tests Gaussian c0+lane against the warp's pixel box ----
+      const int jt = c0 + lane;
+      bool need = false;
+      if (jt < cnt) {
+        const float4 a = s0[jt];
+        const float ddx = fmaxf(fmaxf(bxl - a.x, a.x - bxh), 0.f);
+        const float ddy = fmaxf(fmaxf(byl - a.y, a.y - byh), 0.f);
+        need = ddx * ddx + ddy * ddy <= s2r[jt];
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, need);
+      while (m) {
+        const int j = c0 + __ffs(m) - 1;
+        m &= m - 1;
+        if (done) continue;
+        const float4 a = s0[j];
+        const float dx = a.x - lx, dy = a.y - ly;
+        // p2 = power * log2(e) = A' dx^2 + B' dx dy + C' dy^2
+        const float4 q = s1[j];
+        const float p2 = fmaf(dx, fmaf(a.z, dx, a.w * dy), q.x * dy * dy);
+        if (p2 > 0.f) continue;
+        const float alpha = fminf(kAlphaMax, exp2f(p2 + q.y));
+        if (alpha < kAlphaMin) continue;
+        const float test_T = T * (1.f - alpha);
+        if (test_T < kTMin) {
+          done = true;
+          nev = start + j - rg.x + 1;
+          continue;
+        }
+        const float w = alpha * T;
+        C0 = fmaf(q.z, w, C0);
+        C1 = fmaf(q.w, w, C1);
+        C2 = fmaf(s2b[j], w, C2);
+        T = test_T;
+        ++ncon;
+      }
     }
     __syncthreads();
   }
@@ -514,7 +555,7 @@ __global__ void __launch_bounds__(256) blend_kernel(const __grid_constant__ Rend
     img[2 * hw + pix] = C2 + T * c.bg[2];
     if (b.final_T[f]) b.final_T[f][pix] = T;
     if (b.n_contrib[f]) b.n_contrib[f][pix] = ncon;
-    if (b.n_eval[f]) b.n_eval[f][pix] = neval;
+    if (b.n_eval[f]) b.n_eval[f][pix] = nev;
   }
 }
 
