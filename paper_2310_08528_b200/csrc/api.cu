@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -98,6 +99,15 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.w_r = m->w_r; p.b_r = m->b_r; p.w_s = m->w_s; p.b_s = m->b_s;
 }
 
+// FGS_DEFORM=simt selects the SIMT FP32 deform kernel (A/B comparison); default is tcgen05.
+bool use_simt_deform() {
+  static const bool simt = [] {
+    const char* e = getenv("FGS_DEFORM");
+    return e && strcmp(e, "simt") == 0;
+  }();
+  return simt;
+}
+
 int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
                 int64_t begin, int64_t end, fgs_deformed* outs, cudaStream_t s) {
   int rc;
@@ -121,7 +131,7 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
       p.out_log_scales[f] = outs[f0 + f].log_scales;
       p.out_quats[f] = outs[f0 + f].quats;
     }
-    cudaError_t e = launch_deform(p, s);
+    cudaError_t e = use_simt_deform() ? launch_deform(p, s) : launch_deform_tc(p, s);
     if (e != cudaSuccess) return cuda_fail(e, "deform launch");
   }
   return FGS_OK;

@@ -86,7 +86,8 @@ struct DeformBatch {
 };
 
 // Kernel launchers (return cudaError_t of the launch).
-cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);
+cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);      // SIMT FP32 (deform.cu)
+cudaError_t launch_deform_tc(const DeformBatch& p, cudaStream_t s);   // tcgen05 3xTF32 (deform_tc.cu)
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
 
