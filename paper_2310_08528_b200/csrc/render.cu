@@ -466,96 +466,125 @@ __global__ void ranges_kernel(const __grid_constant__ RenderBatch b, size_t keys
 }
 
 // ------------------------------------------------------------------------------ blend (Eq. 4)
-__global__ void __launch_bounds__(256) blend_kernel(const __grid_constant__ RenderBatch b, size_t vals_off) {
-  // One CTA per 16x16 tile; warp w owns the 8x4 pixel box ((w&1)*8, (w>>1)*4) of the tile so that a
-  // per-warp conservative alpha bound can skip Gaussians for all 32 of its pixels at once.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Eq. 4 for one pixel and one Gaussian, branch-free (the warp stays converged).
+// p2 = power * log2(e); the Gaussian is skipped if p2 > 0 or alpha < 1/255 (R9); the pixel stops
+// (without adding the Gaussian) when T (1 - alpha) < 1e-4 (R9).
+struct PixelState {
+  float T, c0, c1, c2;
+  bool done;
+  uint32_t ncon, nev;
+};
+
+__device__ __forceinline__ void blend_step(PixelState& s, float p2, float lo, float r, float g, float bch,
+                                           uint32_t pos) {
+  const float alpha = fminf(kAlphaMax, ex2_approx(p2 + lo));
+  const bool ok = !s.done && !(p2 > 0.f) && !(alpha < kAlphaMin);
+  const float test_T = s.T * (1.f - alpha);
+  const bool stop = ok && test_T < kTMin;
+  const bool add = ok && !stop;
+  if (stop) { s.done = true; s.nev = pos; }
+  const float w = add ? alpha * s.T : 0.f;
+  s.c0 = fmaf(r, w, s.c0);
+  s.c1 = fmaf(g, w, s.c1);
+  s.c2 = fmaf(bch, w, s.c2);
+  s.T = add ? test_T : s.T;
+  s.ncon += add ? 1u : 0u;
+}
+
+template <bool DBG>
+__global__ void __launch_bounds__(128) blend_kernel(const __grid_constant__ RenderBatch b, size_t vals_off) {
+  // One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 pixel box ((w&1)*8, (w>>1)*8); each lane
+  // two pixels (x, y) and (x, y+4).  Per batch of 256 Gaussians (smem), each warp tests 32 Gaussians
+  // at a time against a conservative alpha bound over its box (lane-parallel + ballot) and then
+  // evaluates only the survivors for its 64 pixels, in list order.
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % b.gx, ty = tile / b.gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int bx0 = (warp & 1) * 8, by0 = (warp >> 1) * 4;          // box origin, tile-relative
-  const int pxi = tx * kTile + bx0 + (lane & 7);
-  const int pyi = ty * kTile + by0 + (lane >> 3);
-  const bool inside = pxi < b.width && pyi < b.height;
+  const int bx0 = (warp & 1) * 8, by0 = (warp >> 1) * 8;          // box origin, tile-relative
+  const int lxi = bx0 + (lane & 7), lyi = by0 + (lane >> 3);
+  const int pxi = tx * kTile + lxi, pyA = ty * kTile + lyi, pyB = pyA + 4;
+  const bool inA = pxi < b.width && pyA < b.height;
+  const bool inB = pxi < b.width && pyB < b.height;
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const uint32_t* gids = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, vals_off);
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
   __shared__ float4 s0[256], s1[256];
-  __shared__ float s2b[256], s2r[256];
+  __shared__ float2 s2[256];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
-  const float lx = (float)(bx0 + (lane & 7)), ly = (float)(by0 + (lane >> 3));   // tile-relative pixel
-  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, byh = (float)(by0 + 3);
-  float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  uint32_t ncon = 0, nev = rg.y - rg.x;     // list entries reached before termination (E basis)
-  bool done = !inside;
+  const float lx = (float)lxi, ly = (float)lyi;
+  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, byh = (float)(by0 + 7);
+  PixelState A{1.f, 0.f, 0.f, 0.f, !inA, 0u, rg.y - rg.x};
+  PixelState B{1.f, 0.f, 0.f, 0.f, !inB, 0u, rg.y - rg.x};
   for (uint32_t start = rg.x; start < rg.y; start += 256) {
-    if (__syncthreads_count(done) == 256) break;
-    const uint32_t idx = start + threadIdx.x;
-    if (idx < rg.y) {
-      const uint32_t g = gids[idx];
-      float4 a = rec[3 * g + 0];
-      const float4 c = rec[3 * g + 2];
-      // tile-relative mean: (hi - origin) is exact, + lo keeps ~1e-6 px
-      a.x = (a.x - tx0) + c.y;
-      a.y = (a.y - ty0) + c.z;
-      s0[threadIdx.x] = a;
-      s1[threadIdx.x] = rec[3 * g + 1];
-      s2b[threadIdx.x] = c.x;
-      s2r[threadIdx.x] = c.w;
+    if (__syncthreads_count(A.done && B.done) == 128) break;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t idx = start + threadIdx.x + 128 * k;
+      if (idx < rg.y) {
+        const uint32_t g = gids[idx];
+        float4 a = rec[3 * g + 0];
+        const float4 c = rec[3 * g + 2];
+        a.x = (a.x - tx0) + c.y;      // tile-relative mean: exact hi difference + lo part
+        a.y = (a.y - ty0) + c.z;
+        s0[threadIdx.x + 128 * k] = a;
+        s1[threadIdx.x + 128 * k] = rec[3 * g + 1];
+        s2[threadIdx.x + 128 * k] = make_float2(c.x, c.w);
+      }
     }
     __syncthreads();
     const int cnt = (int)min(256u, rg.y - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (__all_sync(0xffffffffu, done)) break;
-      // ---- warp-level cull: lane tests Gaussian c0+lane against the warp's pixel box ----
+      if (__all_sync(0xffffffffu, A.done && B.done)) break;
       const int jt = c0 + lane;
       bool need = false;
       if (jt < cnt) {
         const float4 a = s0[jt];
         const float ddx = fmaxf(fmaxf(bxl - a.x, a.x - bxh), 0.f);
         const float ddy = fmaxf(fmaxf(byl - a.y, a.y - byh), 0.f);
-        need = ddx * ddx + ddy * ddy <= s2r[jt];
+        need = ddx * ddx + ddy * ddy <= s2[jt].y;
       }
       uint32_t m = __ballot_sync(0xffffffffu, need);
       while (m) {
         const int j = c0 + __ffs(m) - 1;
         m &= m - 1;
-        if (done) continue;
-        const float4 a = s0[j];
-        const float dx = a.x - lx, dy = a.y - ly;
-        // p2 = power * log2(e) = A' dx^2 + B' dx dy + C' dy^2
-        const float4 q = s1[j];
-        const float p2 = fmaf(dx, fmaf(a.z, dx, a.w * dy), q.x * dy * dy);
-        if (p2 > 0.f) continue;
-        const float alpha = fminf(kAlphaMax, exp2f(p2 + q.y));
-        if (alpha < kAlphaMin) continue;
-        const float test_T = T * (1.f - alpha);
-        if (test_T < kTMin) {
-          done = true;
-          nev = start + j - rg.x + 1;
-          continue;
-        }
-        const float w = alpha * T;
-        C0 = fmaf(q.z, w, C0);
-        C1 = fmaf(q.w, w, C1);
-        C2 = fmaf(s2b[j], w, C2);
-        T = test_T;
-        ++ncon;
+        const float4 a = s0[j], q = s1[j];
+        const float bch = s2[j].x;
+        const float dx = a.x - lx;
+        const float dyA = a.y - ly, dyB = dyA - 4.f;
+        const float adx = a.z * dx;                         // A' dx, shared by both pixels
+        const float pA = fmaf(dx, fmaf(a.w, dyA, adx), q.x * dyA * dyA);
+        const float pB = fmaf(dx, fmaf(a.w, dyB, adx), q.x * dyB * dyB);
+        const uint32_t pos = start + j - rg.x + 1;
+        blend_step(A, pA, q.y, q.z, q.w, bch, pos);
+        blend_step(B, pB, q.y, q.z, q.w, bch, pos);
       }
     }
     __syncthreads();
   }
-  if (inside) {
-    const size_t hw = (size_t)b.width * b.height;
-    const size_t pix = (size_t)pyi * b.width + pxi;
-    float* img = b.image[f];
-    const FrameCam& c = b.cam[f];
-    img[pix] = C0 + T * c.bg[0];
-    img[hw + pix] = C1 + T * c.bg[1];
-    img[2 * hw + pix] = C2 + T * c.bg[2];
-    if (b.final_T[f]) b.final_T[f][pix] = T;
-    if (b.n_contrib[f]) b.n_contrib[f][pix] = ncon;
-    if (b.n_eval[f]) b.n_eval[f][pix] = nev;
+  const size_t hw = (size_t)b.width * b.height;
+  float* img = b.image[f];
+  const FrameCam& cm = b.cam[f];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const PixelState& s = k ? B : A;
+    const bool in = k ? inB : inA;
+    if (!in) continue;
+    const size_t pix = (size_t)(k ? pyB : pyA) * b.width + pxi;
+    img[pix] = s.c0 + s.T * cm.bg[0];
+    img[hw + pix] = s.c1 + s.T * cm.bg[1];
+    img[2 * hw + pix] = s.c2 + s.T * cm.bg[2];
+    if (DBG) {
+      if (b.final_T[f]) b.final_T[f][pix] = s.T;
+      if (b.n_contrib[f]) b.n_contrib[f][pix] = s.ncon;
+      if (b.n_eval[f]) b.n_eval[f][pix] = s.nev;
+    }
   }
 }
 
@@ -647,7 +676,11 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   note_launches(2);
   prof_mark(FGS_STAGE_RANGES, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);
-  blend_kernel<<<dim3(b.ntiles, F), 256, 0, s>>>(b, vfin);
+  const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0];
+  if (dbg)
+    blend_kernel<true><<<dim3(b.ntiles, F), 128, 0, s>>>(b, vfin);
+  else
+    blend_kernel<false><<<dim3(b.ntiles, F), 128, 0, s>>>(b, vfin);
   note_launches(1);
   prof_mark(FGS_STAGE_BLEND, false, s);
   return cudaGetLastError();
