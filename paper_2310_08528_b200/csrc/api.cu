@@ -99,13 +99,26 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.w_r = m->w_r; p.b_r = m->b_r; p.w_s = m->w_s; p.b_s = m->b_s;
 }
 
-// FGS_DEFORM=simt selects the SIMT FP32 deform kernel (A/B comparison); default is tcgen05.
-bool use_simt_deform() {
-  static const bool simt = [] {
+// FGS_DEFORM = simt | tc1 | tc2 forces a deform kernel (A/B comparison).  Default: tc2 (TMEM-resident,
+// frame-outer) when the field fits its line buffer, else tc1.
+int deform_choice() {
+  static const int c = [] {
     const char* e = getenv("FGS_DEFORM");
-    return e && strcmp(e, "simt") == 0;
+    if (!e) return 0;
+    if (strcmp(e, "simt") == 0) return 1;
+    if (strcmp(e, "tc1") == 0) return 2;
+    if (strcmp(e, "tc2") == 0) return 3;
+    return 0;
   }();
-  return simt;
+  return c;
+}
+
+cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
+  switch (deform_choice()) {
+    case 1: return launch_deform(p, s);
+    case 2: return launch_deform_tc(p, s);
+    default: return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
+  }
 }
 
 int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
@@ -131,7 +144,7 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
       p.out_log_scales[f] = outs[f0 + f].log_scales;
       p.out_quats[f] = outs[f0 + f].quats;
     }
-    cudaError_t e = use_simt_deform() ? launch_deform(p, s) : launch_deform_tc(p, s);
+    cudaError_t e = launch_deform_any(p, s);
     if (e != cudaSuccess) return cuda_fail(e, "deform launch");
   }
   return FGS_OK;

@@ -88,6 +88,8 @@ struct DeformBatch {
 // Kernel launchers (return cudaError_t of the launch).
 cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);      // SIMT FP32 (deform.cu)
 cudaError_t launch_deform_tc(const DeformBatch& p, cudaStream_t s);   // tcgen05 3xTF32 (deform_tc.cu)
+cudaError_t launch_deform_tc2(const DeformBatch& p, cudaStream_t s);  // TMEM-resident v2 (deform_tc2.cu)
+bool deform_tc2_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
 
