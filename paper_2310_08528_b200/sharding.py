@@ -1,0 +1,143 @@
+"""Multi-GPU plumbing for the per-frame 4D-GS path — SURVEY.md §8(e), BASELINE.json north_star.
+
+Two ways to use one 8xB200 box (one process per GPU, torch.distributed):
+
+(e1) frame-batch split — `frame_split(n_frames, rank, world)`: a batch of (t, view) frames is cut into
+     contiguous per-rank chunks; every rank holds a replica of G, the HexPlane and the MLP and renders
+     its own frames.  No collective on the data path.
+
+(e2) Gaussian-sharded deformation — `ShardedDeform`: rank r deforms only the contiguous Gaussian slice
+     `shard_range(n, r, world)` (fgs_deform_range, bit-identical to the same rows of an unsharded
+     fgs_deform because every Gaussian's arithmetic is independent of the shard), then the deformed
+     attributes X', r', s' (40 B per Gaussian) are assembled on every rank with
+     `all_gather_into_tensor` (NCCL over NVLink/NVSwitch).  The gather is issued async_op so the caller
+     can render the previous time while it is in flight (the one exchange step of the path).
+
+Host logic only: every arithmetic step of the method runs in libfgs.so (or, in the CPU tests, in a
+deform callback supplied by the test); this module partitions, allocates and exchanges.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+# Attribute widths of the deformed arrays fgs_deform writes (include/fgs.h fgs_deformed).
+DEFORMED_FIELDS: Tuple[Tuple[str, int], ...] = (("means", 3), ("log_scales", 3), ("quats", 4))
+
+
+def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous Gaussian slice [begin, end) of `rank`: equal chunks of ceil(n / world) rows, the last
+    rank(s) short (possibly empty).  Equal chunk size is what all_gather_into_tensor needs."""
+    if world < 1 or not (0 <= rank < world) or n < 0:
+        raise ValueError(f"bad shard ({n=}, {rank=}, {world=})")
+    chunk = -(-n // world) if n else 0
+    begin = min(n, rank * chunk)
+    return begin, min(n, begin + chunk)
+
+
+def padded_rows(n: int, world: int) -> int:
+    """Rows of the gather buffers: world * ceil(n / world) >= n."""
+    return world * (-(-n // world)) if n else 0
+
+
+def frame_split(n_frames: int, rank: int, world: int) -> List[int]:
+    """(e1) frame indices of `rank`: contiguous chunks, sizes differing by at most one."""
+    if world < 1 or not (0 <= rank < world) or n_frames < 0:
+        raise ValueError(f"bad split ({n_frames=}, {rank=}, {world=})")
+    base, extra = divmod(n_frames, world)
+    begin = rank * base + min(rank, extra)
+    return list(range(begin, begin + base + (1 if rank < extra else 0)))
+
+
+def views_of_times(n_times: int, n_views: int, rank: int, world: int) -> List[Tuple[int, int]]:
+    """(e2) multi-view batch: frames (time k, view v), frame id k * n_views + v.  Views are split across
+    ranks (each rank renders its views at EVERY time), so all ranks need G'(t_k) for every k — the case
+    in which sharding the deformation by Gaussian pays."""
+    vs = frame_split(n_views, rank, world)
+    return [(k, v) for k in range(n_times) for v in vs]
+
+
+class ShardedDeform:
+    """Gaussian-sharded deformation with an all-gather of the deformed attributes.
+
+    Buffers: for each slot (time) three tensors [rows][3|3|4] float32 on `device`, rows =
+    padded_rows(n, world); rows >= n are padding that no fgs_render reads (the fgs_deformed struct
+    keeps n).  Rank r's shard is rows [r*chunk, (r+1)*chunk), of which [begin, end) are real.
+
+    deform_fn(slot, t, begin, end, bufs) must write rows [begin, end) of `bufs` (the CUDA path calls
+    fgs_deform_range; CPU tests pass a callback).  gather(slot) all-gathers the three arrays
+    (in place: each rank's input is its own chunk of the output).
+    """
+
+    def __init__(self, n: int, world: int, rank: int, device, n_slots: int = 2, group=None):
+        import torch
+        self.n, self.world, self.rank, self.group = n, world, rank, group
+        self.rows = padded_rows(n, world)
+        self.chunk = self.rows // world if world else 0
+        self.begin, self.end = shard_range(n, rank, world)
+        self.bufs: List[dict] = []
+        for _ in range(n_slots):
+            # padding rows are zero-filled once so a gathered buffer never holds uninitialised memory
+            self.bufs.append({k: torch.zeros((max(self.rows, 1), w), dtype=torch.float32, device=device)
+                              for k, w in DEFORMED_FIELDS})
+
+    def deform(self, slot: int, t: float, deform_fn: Callable[[int, float, int, int, dict], None]) -> None:
+        if self.end > self.begin:
+            deform_fn(slot, t, self.begin, self.end, self.bufs[slot])
+
+    def gather(self, slot: int, async_op: bool = True):
+        """all_gather_into_tensor of the three deformed arrays of `slot`; returns the work handles
+        (wait() them, or let the NCCL stream ordering do it, before rendering the slot)."""
+        import torch.distributed as dist
+        works = []
+        if self.world == 1 or self.rows == 0:
+            return works
+        c0 = self.rank * self.chunk
+        for k, _ in DEFORMED_FIELDS:
+            out = self.bufs[slot][k]
+            w = dist.all_gather_into_tensor(out, out[c0:c0 + self.chunk], group=self.group, async_op=async_op)
+            if w is not None:
+                works.append(w)
+        return works
+
+    def arrays(self, slot: int) -> dict:
+        """The first n rows of the gathered arrays of `slot` (views)."""
+        return {k: v[:self.n] for k, v in self.bufs[slot].items()}
+
+
+def fgs_range_deformer(ds, stream=None) -> Callable[[int, float, int, int, dict], None]:
+    """deform_fn for ShardedDeform running fgs_deform_range (libfgs.so) on a fgs.DeviceScene."""
+    from . import fgs
+
+    def run(slot, t, begin, end, bufs):
+        d = ds.deformed_struct(bufs["means"], bufs["log_scales"], bufs["quats"])
+        fgs.fgs_deform_range(ds.g, ds.field, ds.mlp, float(t), begin, end, d, stream)
+
+    return run
+
+
+def sharded_frames(ds, sd: ShardedDeform, times: Sequence[float], views: Sequence, images: Sequence,
+                   ws, deform_fn=None) -> None:
+    """(e2) pipeline over times: deform shard + async all-gather of t_{k+1} are issued before the render
+    of t_k, so the NVLink transfer overlaps the render.  views[k] = list of (camera struct, image index)
+    this rank renders at time k.  Needs sd.bufs to have >= 2 slots."""
+    from . import fgs
+    deform_fn = deform_fn or fgs_range_deformer(ds)
+    K = len(times)
+    if K == 0:
+        return
+    sd.deform(0, times[0], deform_fn)
+    pending = sd.gather(0)
+    for k in range(K):
+        slot = k % len(sd.bufs)
+        for w in pending:
+            w.wait()                        # current stream waits for the gather of slot k
+        nxt = []
+        if k + 1 < K:
+            sd.deform((k + 1) % len(sd.bufs), times[k + 1], deform_fn)
+            nxt = sd.gather((k + 1) % len(sd.bufs))
+        a = sd.bufs[slot]
+        d = ds.deformed_struct(a["means"], a["log_scales"], a["quats"])
+        cams = [c for c, _ in views[k]]
+        if cams:
+            fgs.fgs_render_batch(cams, [d] * len(cams), [images[i] for _, i in views[k]], ws)
+        pending = nxt

@@ -1,0 +1,124 @@
+"""Multi-GPU host logic on CPU: partitions, and the Gaussian-sharded deformation +
+all-gather assembled by `ShardedDeform` over world_size-2 gloo process groups.
+
+The per-rank "kernel" here is the fp64 oracle deform of the rank's slice (cast to fp32, the dtype of
+the CUDA outputs), so what is tested is exactly the host logic: who deforms which rows, the padded
+in-place all-gather, and the (e2) pipeline order.  The CUDA side (fgs_deform_range bit-identical to
+the unsharded rows) is tested in test_gpu_parity.py::test_deform_range_and_batch_bit_identical.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2310_08528_b200.sharding import (ShardedDeform, frame_split, padded_rows, shard_range,
+                                            views_of_times)
+
+
+@pytest.mark.parametrize("n,world", [(0, 2), (1, 2), (7, 2), (8, 4), (100_003, 8), (5, 8)])
+def test_shard_range_partitions(n, world):
+    got = [shard_range(n, r, world) for r in range(world)]
+    covered = [i for b, e in got for i in range(b, e)] if n < 1000 else None
+    if covered is not None:
+        assert covered == list(range(n))
+    assert got[0][0] == 0 and got[-1][1] == n
+    for (b0, e0), (b1, e1) in zip(got, got[1:]):
+        assert e0 == b1 or (b1 == e1 == n)
+    chunk = padded_rows(n, world) // world if n else 0
+    assert all(e - b <= chunk for b, e in got)
+    assert padded_rows(n, world) >= n and padded_rows(n, world) % world == 0
+
+
+@pytest.mark.parametrize("F,world", [(20, 1), (20, 3), (64, 8), (3, 8), (0, 2)])
+def test_frame_split_partitions(F, world):
+    parts = [frame_split(F, r, world) for r in range(world)]
+    assert sum(parts, []) == list(range(F))
+    sizes = [len(p) for p in parts]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_views_of_times_cover_every_frame_once():
+    world, K, V = 4, 8, 8
+    frames = sorted(k * V + v for r in range(world) for k, v in views_of_times(K, V, r, world))
+    assert frames == list(range(K * V))
+
+
+def test_bad_partition_args():
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+    with pytest.raises(ValueError):
+        frame_split(10, 0, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, times, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2310_08528_b200.inputs import make_scene
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = make_scene("tiny", n=n)
+        sd = ShardedDeform(n, world, rank, "cpu", n_slots=2)
+        calls = []
+
+        def deform_fn(slot, t, b, e, bufs):
+            calls.append((slot, b, e))
+            ref = oracle.deform_ref(s, t, begin=b, end=e)
+            for k in bufs:
+                bufs[k][b:e] = torch.from_numpy(ref[k].astype(np.float32))
+
+        out = []
+        for k, t in enumerate(times):
+            slot = k % 2
+            sd.deform(slot, t, deform_fn)
+            for w in sd.gather(slot, async_op=True):
+                w.wait()
+            out.append({kk: v.clone().numpy() for kk, v in sd.arrays(slot).items()})
+        q.put((rank, calls, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2000, 2001, 1])
+def test_sharded_deform_allgather_gloo(n):
+    import multiprocessing as mp
+
+    import oracle
+    from paper_2310_08528_b200.inputs import make_scene
+
+    world, times = 2, [0.0, 0.37, 1.0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, times, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict()
+    for _ in range(world):
+        rank, calls, out = q.get(timeout=240)
+        res[rank] = (calls, out)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s = make_scene("tiny", n=n)
+    for rank in range(world):
+        calls, out = res[rank]
+        b, e = shard_range(n, rank, world)
+        assert all((cb, ce) == (b, e) for _, cb, ce in calls)       # each rank deforms only its slice
+        for k, t in enumerate(times):
+            ref = oracle.deform_ref(s, t)
+            for key in ref:
+                assert out[k][key].shape == ref[key].shape
+                assert np.array_equal(out[k][key], ref[key].astype(np.float32)), (rank, k, key)
