@@ -226,8 +226,7 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
                         "frac": work / t / fp32_peak, "traffic": None,
                         "algorithmic": f"9 inst x {E:.3g} evaluated + 4 x {C:.3g} contributing pairs per frame"}
     M = counts.get("instances_per_frame")
-    t_sort = stage_ms.get("depth_sort", 0) + stage_ms.get("tile_sort", 0) + stage_ms.get("duplicate", 0) + \
-        stage_ms.get("offsets", 0) + stage_ms.get("ranges", 0)
+    t_sort = stage_ms.get("tile_scan", 0) + stage_ms.get("duplicate", 0) + stage_ms.get("tile_sort", 0)
     if t_sort > 0 and M:
         by = (16 * M + 16 * N) * F
         steps = max(stage_launches.get("blend", 1), 1)
@@ -267,12 +266,14 @@ def run_fgs(args, scene, rank, world, local_rank):
     # work counts of this workload (deterministic; one debug render per frame, untimed)
     counts = {"sms": torch.cuda.get_device_properties(dev).multi_processor_count}
     if rank == 0:
-        Ev, Cv, Mv = [], [], []
+        Ev, Cv, Mv, Wv, Tv = [], [], [], [], []
         for fi in range(F):
             ne = torch.zeros((H, W), dtype=torch.int32, device=dev)
             nc = torch.zeros((H, W), dtype=torch.int32, device=dev)
             ni = torch.zeros(1, dtype=torch.int32, device=dev)
-            aux = fgs.fgs_render_aux(n_evaluated=ne.data_ptr(), n_contrib=nc.data_ptr(), n_instances=ni.data_ptr())
+            bw = torch.zeros(2, dtype=torch.int64, device=dev)
+            aux = fgs.fgs_render_aux(n_evaluated=ne.data_ptr(), n_contrib=nc.data_ptr(), n_instances=ni.data_ptr(),
+                                     blend_work=bw.data_ptr())
             ws1 = ds.alloc_workspace(1, cap)
             im = torch.empty((3, H, W), device=dev)
             fgs.fgs_render_debug(ds.cams[fi], outs[fi], im, ws1, aux)
@@ -280,9 +281,12 @@ def run_fgs(args, scene, rank, world, local_rank):
             Ev.append(int(ne.sum()))
             Cv.append(int(nc.sum()))
             Mv.append(int(ni[0]))
+            Wv.append(int(bw[0]) * 32)
+            Tv.append(int(bw[1]))
             del ws1
         counts.update(evaluated_per_frame=float(np.mean(Ev)), contrib_per_frame=float(np.mean(Cv)),
-                      instances_per_frame=float(np.mean(Mv)))
+                      instances_per_frame=float(np.mean(Mv)), blend_pixel_evals_per_frame=float(np.mean(Wv)),
+                      blend_warp_tests_per_frame=float(np.mean(Tv)))
 
     clocks = ClockSampler(local_rank)
     fgs.fgs_profile_enable(True)

@@ -118,6 +118,9 @@ typedef struct {
   float* final_T;               /* [H][W]       final transmittance                               */
   uint32_t* n_contrib;          /* [H][W]       number of composited Gaussians                    */
   uint32_t* n_evaluated;        /* [H][W]       list entries evaluated before the pixel terminated */
+  uint64_t* blend_work;         /* [2] (accumulated, caller zeroes): [0] (warp, Gaussian) pairs the
+                                 * blend evaluated after its per-warp cull, [1] pairs it tested; a warp
+                                 * covers 64 pixels, so [0] * 64 bounds the pixel evaluations           */
 } fgs_render_aux;
 
 /* ---- deformation field F --------------------------------------------------
@@ -179,20 +182,28 @@ int fgs_frames_host(const fgs_gaussians* g_host, const fgs_hexplanes* field_host
  * milliseconds and launch counts per stage into ms[FGS_N_STAGES] / launches[FGS_N_STAGES]
  * (either may be NULL), then resets them.  Not thread-safe (one profiling client at a time). */
 enum {
-  FGS_STAGE_DEFORM = 0,
-  FGS_STAGE_PREPROCESS,
-  FGS_STAGE_DEPTH_SORT,
-  FGS_STAGE_OFFSETS,
-  FGS_STAGE_DUPLICATE,
-  FGS_STAGE_TILE_SORT,
-  FGS_STAGE_RANGES,
-  FGS_STAGE_BLEND,
+  FGS_STAGE_DEFORM = 0,         /* HexPlane sampling + phi_d + heads (a1-a3)                        */
+  FGS_STAGE_PREPROCESS,         /* counter clear + preprocess incl. per-tile instance counts (a4)   */
+  FGS_STAGE_TILE_SCAN,          /* scan of the tile counts -> ranges (a7)                           */
+  FGS_STAGE_DUPLICATE,          /* key duplication into tile buckets (a5)                           */
+  FGS_STAGE_TILE_SORT,          /* global-memory sort of tile lists longer than the smem cap (a6)   */
+  FGS_STAGE_BLEND,              /* per-tile (depth, index) sort in smem (a6) + alpha blending (a8)  */
   FGS_N_STAGES
 };
 int fgs_profile_enable(int enable);
 int fgs_profile_read(double* ms, int64_t* launches);
 /* Number of kernels this library has launched since it was loaded (all threads). */
 int64_t fgs_launch_count(void);
+
+/* ---- tuning (process-global; change only while no call of this library is enqueueing) --------
+ * FGS_TUNE_TILE_SORT_CAP: tile lists of at most this many instances are sorted by (depth, index) in
+ * the blend kernel's shared memory; longer lists by the global-memory sort (FGS_STAGE_TILE_SORT).
+ * Range [1, 1024], default 1024.  Results are identical for every value (tests lower it to exercise
+ * the long-list path).  fgs_set_tuning returns FGS_E_INVALID for an unknown key or a value out of
+ * range; fgs_get_tuning returns -1 for an unknown key. */
+enum { FGS_TUNE_TILE_SORT_CAP = 0 };
+int fgs_set_tuning(int32_t key, int64_t value);
+int64_t fgs_get_tuning(int32_t key);
 
 /* Message of the last non-OK return on this thread (static storage, never NULL). */
 const char* fgs_last_error(void);

@@ -201,6 +201,9 @@ int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* 
   local.sh_degree = defs[0].sh_degree;
   local.width = W; local.height = H;
   local.gx = local.L.gx; local.gy = local.L.gy; local.ntiles = local.L.ntiles;
+  local.sort_cap = tile_sort_cap();
+  local.debug = aux != nullptr;
+  local.blend_work = aux ? (unsigned long long*)aux->blend_work : nullptr;
   local.ws_stride = per;
   for (int f0 = 0; f0 < n_frames; f0 += kMaxFrames) {
     local.n_frames = std::min(kMaxFrames, n_frames - f0);
@@ -273,24 +276,23 @@ WsLayout make_layout(int64_t n, int width, int height, int64_t cap) {
   L.gx = (width + kTile - 1) / kTile;
   L.gy = (height + kTile - 1) / kTile;
   L.ntiles = L.gx * L.gy;
-  const int64_t items = std::max<int64_t>(std::max<int64_t>(n, cap), 1);
-  L.hist_tiles = (items + kSortTile - 1) / kSortTile;
-  L.scan_tiles = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align256(o + bytes); return at; };
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
   const size_t cc = (size_t)std::max<int64_t>(cap, 1);
+  const size_t nt = (size_t)L.ntiles;
   L.cnt = take(64);
-  L.keys0 = take(4 * nn); L.vals0 = take(4 * nn); L.keys1 = take(4 * nn); L.vals1 = take(4 * nn);
+  L.keys = take(4 * nn);
   L.tt = take(4 * nn);
   L.rect = take(8 * nn);
   L.rec = take(48 * nn);
   L.radii = take(4 * nn);
-  L.offs = take(4 * nn);
-  L.partial = take(4 * (size_t)L.scan_tiles);
-  L.ranges = take(8 * (size_t)L.ntiles);
-  L.hist = take(4 * 256 * (size_t)L.hist_tiles);
-  L.ikey0 = take(4 * cc); L.ival0 = take(4 * cc); L.ikey1 = take(4 * cc); L.ival1 = take(4 * cc);
+  L.tile_count = take(4 * nt);
+  L.cursor = take(4 * nt);
+  L.ranges = take(8 * nt);
+  L.long_list = take(4 * nt);
+  L.inst = take(8 * cc);
+  L.inst2 = take(8 * cc);
   L.total = o;
   return L;
 }
@@ -305,6 +307,11 @@ int64_t capacity_for(int64_t n, int width, int height, size_t bytes) {
   }
   return std::min<int64_t>(lo, (int64_t)0xFFFFFFF0);
 }
+
+namespace {
+std::atomic<int> g_tile_sort_cap{kBlendSortMax};
+}
+int tile_sort_cap() { return g_tile_sort_cap.load(std::memory_order_relaxed); }
 
 }  // namespace fgs
 
@@ -404,6 +411,21 @@ int fgs_profile_read(double* ms, int64_t* launches) {
 }
 
 int64_t fgs_launch_count(void) { return g_launches.load(); }
+
+int fgs_set_tuning(int32_t key, int64_t value) {
+  switch (key) {
+    case FGS_TUNE_TILE_SORT_CAP:
+      FGS_CHECK(value >= 1 && value <= kBlendSortMax, "tile sort cap must be in [1, 1024]");
+      g_tile_sort_cap.store((int)value);
+      return FGS_OK;
+    default:
+      return fail(FGS_E_INVALID, "unknown tuning key");
+  }
+}
+
+int64_t fgs_get_tuning(int32_t key) {
+  return key == FGS_TUNE_TILE_SORT_CAP ? (int64_t)tile_sort_cap() : -1;
+}
 
 // ---- end to end with host buffers -------------------------------------------------------------
 namespace {

@@ -9,30 +9,28 @@ namespace fgs {
 
 constexpr int kTile = FGS_TILE;              // 16x16 pixel tiles ([3dgs] rasterizer, reading R8)
 constexpr int kMaxFrames = 32;               // frames per launch (kernel-parameter table)
-constexpr int kSortThreads = 256;            // radix sort CTA
-constexpr int kSortItems = 8;                // items per thread
-constexpr int kSortTile = kSortThreads * kSortItems;   // 2048 keys per sort tile
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;   // 4096 per scan tile
+constexpr int kScanThreads = 1024;           // tile-count scan CTA (one per frame)
+constexpr int kBlendThreads = 128;           // blend CTA: 4 warps x 8x8 pixel boxes of a 16x16 tile
+constexpr int kBlendSortMax = 1024;          // longest tile list the blend sorts in shared memory
+constexpr int kLargeSortThreads = 256;       // global-memory sort of longer lists
+constexpr int kLargeSortChunk = 2048;        // its shared-memory run length
 
 // Per-frame workspace layout (all offsets in bytes from the frame's slice, 256-B aligned).
 struct WsLayout {
   int64_t n = 0, cap = 0;
   int width = 0, height = 0, gx = 0, gy = 0, ntiles = 0;
-  int64_t hist_tiles = 0;    // max sort tiles (over n and cap)
-  int64_t scan_tiles = 0;    // scan tiles over n
-  size_t cnt = 0;            // uint32[8]: 0 n, 1 M clamped, 2 overflow, 3 M raw
-  size_t keys0 = 0, vals0 = 0, keys1 = 0, vals1 = 0;    // uint32[n] depth sort ping-pong
+  size_t cnt = 0;            // uint32[16]: 0 n, 1 M clamped to cap, 2 overflow flag, 3 M raw, 4 long lists
+  size_t keys = 0;           // uint32[n] depth key (IEEE bits of fp32 view depth), gid order
   size_t tt = 0;             // uint32[n] tiles_touched
   size_t rect = 0;           // uint2[n]  (x0 | y0<<16, x1 | y1<<16)
   size_t rec = 0;            // float4[n][3] blend records
   size_t radii = 0;          // int32[n]
-  size_t offs = 0;           // uint32[n] exclusive scan of tiles_touched in depth order
-  size_t partial = 0;        // uint32[scan_tiles]
-  size_t ikey0 = 0, ival0 = 0, ikey1 = 0, ival1 = 0;    // uint32[cap] tile sort ping-pong
-  size_t hist = 0;           // uint32[256 * hist_tiles]
-  size_t ranges = 0;         // uint2[ntiles]
+  size_t tile_count = 0;     // uint32[ntiles] instances per tile (atomics in preprocess)
+  size_t cursor = 0;         // uint32[ntiles] scatter cursors
+  size_t ranges = 0;         // uint2[ntiles]  [start, end) of each tile's list (clamped to cap)
+  size_t long_list = 0;      // uint32[ntiles] tiles whose lists exceed the warp-sort cap (count in cnt[4])
+  size_t inst = 0;           // uint64[cap] instances (depth_key << 32 | gid), bucketed by tile
+  size_t inst2 = 0;          // uint64[cap] scratch of the long-list sort
   size_t total = 0;
 };
 
@@ -51,6 +49,8 @@ struct RenderBatch {
   int64_t n;
   int sh_degree;
   int width, height, gx, gy, ntiles;
+  int sort_cap;              // lists longer than this are sorted by the global-memory path
+  int debug;                 // 1: blend writes each tile's sorted list back (fgs_render_debug)
   char* ws;                  // frame f slice = ws + f * ws_stride
   size_t ws_stride;
   WsLayout L;
@@ -64,6 +64,7 @@ struct RenderBatch {
   float* final_T[kMaxFrames];      // optional
   uint32_t* n_contrib[kMaxFrames]; // optional
   uint32_t* n_eval[kMaxFrames];    // optional
+  unsigned long long* blend_work;  // optional [2], frame 0 of a debug render
 };
 
 // Deformation launch (times batched over frames of the same model).
@@ -92,6 +93,9 @@ cudaError_t launch_deform_tc2(const DeformBatch& p, cudaStream_t s);  // TMEM-re
 bool deform_tc2_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
+
+// Tuning knobs (api.cu, fgs_set_tuning).
+int tile_sort_cap();
 
 // Profiling / launch accounting (api.cu).
 void prof_mark(int stage, bool begin, cudaStream_t s);

@@ -1,20 +1,26 @@
-// Tile-based splatting S(M, G') on sm_100a — PAPER.md §3.1 with the [3dgs]
-// rasterizer conventions the paper renders with; readings R1-R20 in DESIGN.md.
+// Tile-based splatting S(M, G') on sm_100a — PAPER.md §3.1 with the [3dgs] rasterizer
+// conventions the paper renders with; readings R1-R20 in DESIGN.md.
 //
-// Per frame (frames of a batch run in the same launches, blockIdx.y = frame):
-//   preprocess   Eq. 2 covariance, Eq. 3 EWA projection, conic, radius, tile rect, depth key,
-//                SH colour.  Decision geometry (everything that yields an integer: depth key,
-//                radius, rect) in fp64 with the oracle's fixed summation order for the depth.
-//   depth sort   stable LSD radix sort (4 x 8-bit digits) of the N depth keys, values = index.
-//   offsets      exclusive scan of tiles_touched in depth order -> instance offsets, M.
-//   duplicate    each kept Gaussian emits (tile, index) for every tile of its rect, in depth order.
-//   tile sort    stable LSD radix sort of the instances by tile id (<= 8-bit digits).  Because the
-//                input is already in (depth, index) order, the result is sorted by
-//                (tile, depth, index) — the [3dgs] 64-bit key order, reading R14.
-//   ranges       per-tile [start, end) by boundary detection on the sorted tile ids.
-//   blend        Eq. 4 front-to-back per pixel, 16x16 CTA per tile, records staged in smem.
+// Per frame (the frames of a batch share every launch, blockIdx.y = frame):
+//   clear        zero the per-tile instance counters.
+//   preprocess   Eq. 2 covariance, Eq. 3 EWA projection, conic, radius, tile rect, depth key, SH
+//                colour; every kept Gaussian adds 1 to the counter of each tile of its rect (RED).
+//                Decision geometry (depth key, radius, rect) in fp64 with the oracle's fixed
+//                summation order, so the integer work is bit-exact against the fp64 oracle.
+//   tile scan    exclusive scan of the tile counters -> per-tile ranges [start, end),
+//                scatter cursors, M and the capacity-overflow flag.
+//   duplicate    each kept Gaussian writes one 64-bit instance (depth_key << 32 | gid) into every
+//                tile bucket of its rect, at an atomically claimed slot.  The order
+//                inside a bucket is arbitrary here; the sort below makes it unique.
+//   tile sort    (a6) every tile's list sorted ascending by (depth key, gid): lists of up to
+//                sort_cap instances by a bitonic sort in the blend CTA's shared memory, longer
+//                lists by long_sort_kernel (shared-memory runs + merge-path merges in global memory).
+//                Result: the [3dgs] (tile, depth, index) order (reading R14), without global passes.
+//   blend        Eq. 4 front to back per pixel; 16x16 tile per CTA.
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <limits.h>
 
 #include <algorithm>
 
@@ -24,13 +30,14 @@ namespace fgs {
 
 namespace {
 
-constexpr float kNear = 0.2f;             // R6
+constexpr float kNear = 0.2f;               // R6
 constexpr float kAlphaMin = 1.0f / 255.0f;  // R9
-constexpr float kTMin = 1e-4f;            // R9
-constexpr float kAlphaMax = 0.99f;        // R9
-constexpr double kDilation = 0.3;         // R5
-constexpr double kLambdaFloor = 0.1;      // R7
-constexpr double kFovClamp = 1.3;         // R4
+constexpr float kTMin = 1e-4f;              // R9
+constexpr float kAlphaMax = 0.99f;          // R9
+constexpr double kDilation = 0.3;           // R5
+constexpr double kLambdaFloor = 0.1;        // R7
+constexpr double kFovClamp = 1.3;           // R4
+constexpr double kLog2e = 1.4426950408889634;
 
 // Real SH constants (CS phase, [3dgs] table; reading R10).
 constexpr float SH_C0 = 0.28209479177387814f;
@@ -47,22 +54,99 @@ __device__ __forceinline__ uint32_t* cnt_ptr(const RenderBatch& b, int f) {
   return ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.cnt);
 }
 
+// ------------------------------------------------------------------------------ clear
+__global__ void clear_kernel(const __grid_constant__ RenderBatch b) {
+  const int f = blockIdx.y;
+  uint32_t* tc = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tile_count);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < b.ntiles; t += gridDim.x * blockDim.x) tc[t] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 16) cnt_ptr(b, f)[threadIdx.x] = threadIdx.x == 0 ? (uint32_t)b.n : 0u;
+}
+
 // ------------------------------------------------------------------------------ preprocess
+// SH coefficients of Gaussian i ([K][3] fp32) -> colour (step 12).  DEG is the SH degree.
+template <int DEG>
+__device__ __forceinline__ void sh_colour(const float* __restrict__ sh, float X, float Y, float Z, float col[3]) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  float c[3 * K];
+  if constexpr ((3 * K) % 4 == 0) {            // 16-B aligned rows (K = 4, 16): vector loads
+#pragma unroll
+    for (int q = 0; q < 3 * K / 4; ++q) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(sh) + q);
+      c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) c[q] = __ldg(sh + q);
+  }
+  float basis[K];
+  basis[0] = SH_C0;
+  if constexpr (DEG >= 1) { basis[1] = -SH_C1 * Y; basis[2] = SH_C1 * Z; basis[3] = -SH_C1 * X; }
+  if constexpr (DEG >= 2) {
+    const float xx = X * X, yy = Y * Y, zz = Z * Z;
+    basis[4] = SH_C2_0 * X * Y;
+    basis[5] = SH_C2_1 * Y * Z;
+    basis[6] = SH_C2_2 * (2.f * zz - xx - yy);
+    basis[7] = SH_C2_3 * X * Z;
+    basis[8] = SH_C2_4 * (xx - yy);
+    if constexpr (DEG >= 3) {
+      basis[9] = SH_C3_0 * Y * (3.f * xx - yy);
+      basis[10] = SH_C3_1 * X * Y * Z;
+      basis[11] = SH_C3_2 * Y * (4.f * zz - xx - yy);
+      basis[12] = SH_C3_3 * Z * (2.f * zz - 3.f * xx - 3.f * yy);
+      basis[13] = SH_C3_4 * X * (4.f * zz - xx - yy);
+      basis[14] = SH_C3_5 * Z * (xx - yy);
+      basis[15] = SH_C3_6 * X * (xx - 3.f * yy);
+    }
+  }
+  col[0] = col[1] = col[2] = 0.5f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    col[0] = fmaf(basis[k], c[3 * k + 0], col[0]);
+    col[1] = fmaf(basis[k], c[3 * k + 1], col[1]);
+    col[2] = fmaf(basis[k], c[3 * k + 2], col[2]);
+  }
+}
+
+// CTA-level aggregation of per-tile atomics.  The CTA's kept Gaussians are bounded by the tile box
+// [bx0,bx1) x [by0,by1); when it holds at most kAggTiles tiles (spatially ordered models: a CTA's
+// Gaussians are neighbours), per-tile sums are formed in shared memory and each touched tile gets one
+// global atomic; otherwise every instance goes to global memory directly.
+constexpr int kAggTiles = 2048;
+struct AggBox {
+  int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ AggBox cta_rect_union(bool kept, int x0, int y0, int x1, int y1, int* sbox) {
+  if (threadIdx.x == 0) { sbox[0] = INT_MAX; sbox[1] = INT_MAX; sbox[2] = INT_MIN; sbox[3] = INT_MIN; }
+  __syncthreads();
+  if (kept) {
+    atomicMin(sbox + 0, x0); atomicMin(sbox + 1, y0);
+    atomicMax(sbox + 2, x1); atomicMax(sbox + 3, y1);
+  }
+  __syncthreads();
+  AggBox r{sbox[0], sbox[1], sbox[2], sbox[3]};
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ bool agg_fits(const AggBox& r) {
+  return r.x1 > r.x0 && (int64_t)(r.x1 - r.x0) * (r.y1 - r.y0) <= kAggTiles;
+}
+
+template <int DEG>
 __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t* cnt = cnt_ptr(b, f);
-  if (i == 0) { cnt[0] = (uint32_t)b.n; cnt[1] = 0; cnt[2] = 0; cnt[3] = 0; }
-  if (i >= b.n) return;
-  uint32_t* keys = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.keys0);
-  uint32_t* vals = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.vals0);
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i0 < b.n;
+  const int64_t i = valid ? i0 : b.n - 1;     // out-of-range threads mirror the last Gaussian, write nothing
+  uint32_t* keys = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.keys);
   uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tt);
   uint2* rect = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.rect);
   int32_t* radii = ws_ptr<int32_t>(b.ws, b.ws_stride, f, b.L.radii);
   float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
+  uint32_t* tile_count = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tile_count);
   const FrameCam& c = b.cam[f];
 
-  vals[i] = (uint32_t)i;
   // ---- step 3: p = R X + t with the oracle's summation order (products exact in fp64) ----
   const float* Xp = b.means[f] + 3 * i;
   const double x = Xp[0], y = Xp[1], z = Xp[2];
@@ -73,8 +157,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   // ---- steps 1-2: activation and Sigma = R S S^T R^T (Eq. 2) ----
   const float* ls = b.log_scales[f] + 3 * i;
   const double s0 = exp((double)ls[0]), s1 = exp((double)ls[1]), s2 = exp((double)ls[2]);
-  const float* qp = b.quats[f] + 4 * i;
-  double qw = qp[0], qx = qp[1], qy = qp[2], qz = qp[3];
+  const float4 qv = *reinterpret_cast<const float4*>(b.quats[f] + 4 * i);
+  double qw = qv.x, qx = qv.y, qy = qv.z, qz = qv.w;
   const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
   qw /= qn; qx /= qn; qy /= qn; qz /= qn;
   const double r00 = 1 - 2 * (qy * qy + qz * qz), r01 = 2 * (qx * qy - qw * qz), r02 = 2 * (qx * qz + qw * qy);
@@ -116,7 +200,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   keep = keep && (det > 0.0);
   // ---- step 8: radius ----
   const double mid = 0.5 * (a + cc);
-  const double lam1 = mid + sqrt(fmax(kLambdaFloor, mid * mid - det));
+  const double disc = sqrt(fmax(kLambdaFloor, mid * mid - det));
+  const double lam1 = mid + disc;
   const double rad = ceil(3.0 * sqrt(lam1));
   // ---- step 9: mean2d ----
   const double mx = fx * px / pz + (double)c.cx;
@@ -131,8 +216,28 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
     y1 = (int)fmin(gyd, fmax(0.0, trunc((my + rad + (kTile - 1)) / kTile)));
     keep = (x1 - x0) * (y1 - y0) > 0;
   }
+  keep = keep && valid;
+  // ---- instance counts per tile (the bucket sizes of the duplication) ----
+  __shared__ int sbox[4];
+  __shared__ uint32_t scount[kAggTiles];
+  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
+  if (agg_fits(box)) {
+    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    for (int q = threadIdx.x; q < area; q += blockDim.x) scount[q] = 0;
+    __syncthreads();
+    if (keep)
+      for (int ty = y0; ty < y1; ++ty)
+        for (int tx = x0; tx < x1; ++tx) atomicAdd(scount + (ty - box.y0) * bw + (tx - box.x0), 1u);
+    __syncthreads();
+    for (int q = threadIdx.x; q < area; q += blockDim.x)
+      if (scount[q]) atomicAdd(tile_count + (box.y0 + q / bw) * b.gx + box.x0 + q % bw, scount[q]);
+  } else if (keep) {
+    for (int ty = y0; ty < y1; ++ty)
+      for (int tx = x0; tx < x1; ++tx) atomicAdd(tile_count + ty * b.gx + tx, 1u);
+  }
+  if (!valid) return;
   if (!keep) {
-    keys[i] = 0xFFFFFFFFu;
+    keys[i] = 0u;
     tt[i] = 0;
     rect[i] = make_uint2(0, 0);
     radii[i] = 0;
@@ -147,93 +252,31 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   const double cxw = -((double)c.R[0] * c.t[0] + (double)c.R[3] * c.t[1] + (double)c.R[6] * c.t[2]);
   const double cyw = -((double)c.R[1] * c.t[0] + (double)c.R[4] * c.t[1] + (double)c.R[7] * c.t[2]);
   const double czw = -((double)c.R[2] * c.t[0] + (double)c.R[5] * c.t[1] + (double)c.R[8] * c.t[2]);
-  double dx = x - cxw, dy = y - cyw, dz = z - czw;
+  const double dx = x - cxw, dy = y - cyw, dz = z - czw;
   const double dn = sqrt(dx * dx + dy * dy + dz * dz);
-  const float X = (float)(dx / dn), Y = (float)(dy / dn), Z = (float)(dz / dn);
-  const int deg = b.sh_degree;
-  const int K = (deg + 1) * (deg + 1);
-  const float* sh = b.sh[f] + (size_t)i * K * 3;
-  float basis[16];
-  basis[0] = SH_C0;
-  if (deg >= 1) { basis[1] = -SH_C1 * Y; basis[2] = SH_C1 * Z; basis[3] = -SH_C1 * X; }
-  if (deg >= 2) {
-    const float xx = X * X, yy = Y * Y, zz = Z * Z;
-    basis[4] = SH_C2_0 * X * Y;
-    basis[5] = SH_C2_1 * Y * Z;
-    basis[6] = SH_C2_2 * (2.f * zz - xx - yy);
-    basis[7] = SH_C2_3 * X * Z;
-    basis[8] = SH_C2_4 * (xx - yy);
-    if (deg >= 3) {
-      basis[9] = SH_C3_0 * Y * (3.f * xx - yy);
-      basis[10] = SH_C3_1 * X * Y * Z;
-      basis[11] = SH_C3_2 * Y * (4.f * zz - xx - yy);
-      basis[12] = SH_C3_3 * Z * (2.f * zz - 3.f * xx - 3.f * yy);
-      basis[13] = SH_C3_4 * X * (4.f * zz - xx - yy);
-      basis[14] = SH_C3_5 * Z * (xx - yy);
-      basis[15] = SH_C3_6 * X * (xx - 3.f * yy);
-    }
-  }
-  float col[3] = {0.5f, 0.5f, 0.5f};
-  for (int k = 0; k < K; ++k) {
-    col[0] = fmaf(basis[k], __ldg(sh + 3 * k + 0), col[0]);
-    col[1] = fmaf(basis[k], __ldg(sh + 3 * k + 1), col[1]);
-    col[2] = fmaf(basis[k], __ldg(sh + 3 * k + 2), col[2]);
-  }
+  float col[3];
+  sh_colour<DEG>(b.sh[f] + (size_t)i * (DEG + 1) * (DEG + 1) * 3, (float)(dx / dn), (float)(dy / dn),
+                 (float)(dz / dn), col);
   // ---- blend record: mean2d as hi/lo fp32 pairs, conic pre-scaled to the log2 domain ----
-  //   p2 = A' dx^2 + B' dx dy + C' dy^2 = power * log2(e);  alpha = min(0.99, 2^(p2 + log2 o))
+  //   p2 = a2 dx^2 + b2 dx dy + c2 dy^2 = power * log2(e);  alpha = min(0.99, 2^(p2 + log2 o))
   const float mxh = (float)mx, myh = (float)my;
   const float mxl = (float)(mx - (double)mxh), myl = (float)(my - (double)myh);
   const double opac = 1.0 / (1.0 + exp(-(double)b.opacity[f][i]));
-  const double L2E = 1.4426950408889634;
-  rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * L2E * cc / det), (float)(L2E * bb / det));
-  rec[3 * i + 1] = make_float4((float)(-0.5 * L2E * a / det), (float)log2(opac), fmaxf(col[0], 0.f),
-                               fmaxf(col[1], 0.f));
-  // Conservative per-Gaussian cull radius^2 for the blend's warp-box test: for any pixel at distance
-  // d from the mean, alpha <= o exp(-d^2 / (2 lambda_max(Sigma2))), so alpha < 1/255 (skipped anyway)
-  // whenever d^2 > 2 lambda_max (ln(255 o) + 0.01); margins cover fp32 evaluation error.
+  // Ellipse cull threshold (blend): q2 = -p2 >= 0; alpha >= 1/255 needs q2 <= log2(255 o).  The
+  // margin covers the fp32 evaluation of q2 in the blend and in the cull test, whose relative
+  // error grows with the conic's condition number kappa = lambda_max / lambda_min of Sigma2.
+  const double lam_min = fmax(mid - sqrt(fmax(0.0, mid * mid - det)), 1e-30);
   const double lam_max = mid + sqrt(fmax(0.0, mid * mid - det));
-  const double r2 = (2.0 * log(255.0 * opac) + 0.02) * lam_max * (1.0 + 1e-4) + 1e-3;
-  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, (float)r2);
+  const double thr2 = log2(255.0 * opac);
+  const double thr_keep = thr2 + (fabs(thr2) + 1.0) * (2e-3 + 4e-6 * (lam_max / lam_min));
+  rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * kLog2e * cc / det), (float)(kLog2e * bb / det));
+  rec[3 * i + 1] = make_float4((float)(-0.5 * kLog2e * a / det), (float)log2(opac), fmaxf(col[0], 0.f),
+                               fmaxf(col[1], 0.f));
+  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, (float)thr_keep);
 }
 
-// ------------------------------------------------------------------------------ radix sort
-struct SortArgs {
-  char* ws;
-  size_t stride;
-  size_t cnt;       // counter block offset
-  int cnt_idx;      // which counter holds the item count
-  size_t kin, vin, kout, vout, hist;
-  int shift, bits;
-};
-
-__device__ __forceinline__ uint32_t sort_count(const SortArgs& a, int f) {
-  return ws_ptr<uint32_t>(a.ws, a.stride, f, a.cnt)[a.cnt_idx];
-}
-
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const __grid_constant__ SortArgs a) {
-  const int f = blockIdx.y;
-  const uint32_t count = sort_count(a, f);
-  const uint32_t ntl = (count + kSortTile - 1) / kSortTile;
-  const uint32_t* keys = ws_ptr<uint32_t>(a.ws, a.stride, f, a.kin);
-  uint32_t* hist = ws_ptr<uint32_t>(a.ws, a.stride, f, a.hist);
-  const int radix = 1 << a.bits;
-  const uint32_t mask = radix - 1;
-  __shared__ uint32_t h[256];
-  for (uint32_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
-    for (int d = threadIdx.x; d < radix; d += kSortThreads) h[d] = 0;
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < kSortItems; ++it) {
-      const uint32_t idx = tile * kSortTile + it * kSortThreads + threadIdx.x;
-      if (idx < count) atomicAdd(&h[(keys[idx] >> a.shift) & mask], 1u);
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < radix; d += kSortThreads) hist[(size_t)d * ntl + tile] = h[d];
-    __syncthreads();
-  }
-}
-
-// Block-wide exclusive scan of one value per thread (1024 threads); returns the block total.
+// ------------------------------------------------------------------------------ tile scan (a7)
+// Block-wide exclusive scan of one value per thread; returns the block total.
 template <int NT>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& excl, uint32_t* sw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -262,208 +305,252 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& e
   return total;
 }
 
-__global__ void __launch_bounds__(1024) radix_scan_kernel(const __grid_constant__ SortArgs a) {
+__global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.x;
-  const uint32_t count = sort_count(a, f);
-  const uint32_t ntl = (count + kSortTile - 1) / kSortTile;
-  uint32_t* hist = ws_ptr<uint32_t>(a.ws, a.stride, f, a.hist);
-  const uint32_t total = (uint32_t)(1 << a.bits) * ntl;
-  const uint32_t chunk = (total + 1023) / 1024;
-  const uint32_t beg = min(total, threadIdx.x * chunk), end = min(total, beg + chunk);
-  uint32_t s = 0;
-  for (uint32_t k = beg; k < end; ++k) s += hist[k];
-  __shared__ uint32_t sw[32];
-  uint32_t excl;
-  block_exclusive_scan<1024>(s, excl, sw);
-  for (uint32_t k = beg; k < end; ++k) {
-    const uint32_t v = hist[k];
-    hist[k] = excl;
-    excl += v;
-  }
-}
-
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(const __grid_constant__ SortArgs a) {
-  const int f = blockIdx.y;
-  const uint32_t count = sort_count(a, f);
-  const uint32_t ntl = (count + kSortTile - 1) / kSortTile;
-  const uint32_t* kin = ws_ptr<uint32_t>(a.ws, a.stride, f, a.kin);
-  const uint32_t* vin = ws_ptr<uint32_t>(a.ws, a.stride, f, a.vin);
-  uint32_t* kout = ws_ptr<uint32_t>(a.ws, a.stride, f, a.kout);
-  uint32_t* vout = ws_ptr<uint32_t>(a.ws, a.stride, f, a.vout);
-  const uint32_t* hist = ws_ptr<uint32_t>(a.ws, a.stride, f, a.hist);
-  const int radix = 1 << a.bits;
-  const uint32_t mask = radix - 1;
-  constexpr int NW = kSortThreads / 32;
-  __shared__ uint32_t wc[NW][256];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
-  for (uint32_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
-    for (int d = threadIdx.x; d < NW * 256; d += kSortThreads) (&wc[0][0])[d] = 0;
-    __syncthreads();
-    uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
-    // Warp `warp` owns the contiguous chunk [warp*256, warp*256+256) of the tile, in rounds of 32,
-    // so ranks are stable (input order) within the warp; warps are combined in order below.
-#pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-      const uint32_t idx = tile * kSortTile + warp * (32 * kSortItems) + r * 32 + lane;
-      const bool valid = idx < count;
-      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-      uint32_t d = 0, peers = 0;
-      if (valid) {
-        k[r] = kin[idx];
-        v[r] = vin[idx];
-        d = (k[r] >> a.shift) & mask;
-        peers = __match_any_sync(vm, d);
-        rank[r] = wc[warp][d] + __popc(peers & lt);
-      }
-      __syncwarp();
-      if (valid && (__ffs(peers) - 1) == lane) wc[warp][d] += __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < radix; d += kSortThreads) {
-      uint32_t run = hist[(size_t)d * ntl + tile];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t c = wc[w][d];
-        wc[w][d] = run;
-        run += c;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kSortItems; ++r) {
-      const uint32_t idx = tile * kSortTile + warp * (32 * kSortItems) + r * 32 + lane;
-      if (idx < count) {
-        const uint32_t pos = wc[warp][(k[r] >> a.shift) & mask] + rank[r];
-        kout[pos] = k[r];
-        vout[pos] = v[r];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------------------ instance offsets
-// Exclusive scan over depth order of tiles_touched[vals[p]] (3 phases).
-__global__ void __launch_bounds__(kScanThreads) offsets_reduce_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const int64_t n = b.n;
-  const int64_t nt = (n + kScanTile - 1) / kScanTile;
-  const uint32_t* vals = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.vals0);
-  const uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tt);
-  uint32_t* part = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.partial);
-  __shared__ uint32_t sw[32];
-  for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-      const int64_t p = tile * kScanTile + it * kScanThreads + threadIdx.x;
-      if (p < n) s += tt[vals[p]];
-    }
-    uint32_t excl;
-    const uint32_t tot = block_exclusive_scan<kScanThreads>(s, excl, sw);
-    if (threadIdx.x == 0) part[tile] = tot;
-  }
-}
-
-__global__ void __launch_bounds__(1024) offsets_partials_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.x;
-  const int64_t nt = (b.n + kScanTile - 1) / kScanTile;
-  uint32_t* part = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.partial);
+  const uint32_t* tc = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tile_count);
+  uint32_t* cursor = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.cursor);
+  uint2* ranges = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges);
   uint32_t* cnt = cnt_ptr(b, f);
-  const uint32_t chunk = (uint32_t)((nt + 1023) / 1024);
-  const uint32_t beg = (uint32_t)min((int64_t)threadIdx.x * chunk, nt);
-  const uint32_t end = (uint32_t)min((int64_t)beg + chunk, nt);
-  unsigned long long s = 0;
-  for (uint32_t k = beg; k < end; ++k) s += part[k];
+  const int nt = b.ntiles;
+  const int chunk = (nt + kScanThreads - 1) / kScanThreads;
+  const int beg = min(nt, (int)threadIdx.x * chunk), end = min(nt, beg + chunk);
+  uint64_t s = 0;
+  for (int t = beg; t < end; ++t) s += tc[t];
   __shared__ uint32_t sw[32];
   uint32_t excl;
-  const uint32_t total = block_exclusive_scan<1024>((uint32_t)s, excl, sw);
-  for (uint32_t k = beg; k < end; ++k) {
-    const uint32_t v = part[k];
-    part[k] = excl;
-    excl += v;
+  // the total can exceed 2^32 only far past any capacity; saturate (overflow flag below)
+  const uint32_t total = block_exclusive_scan<kScanThreads>((uint32_t)(s < 0xFFFFFFFFull ? s : 0xFFFFFFFFull), excl, sw);
+  const uint64_t cap = (uint64_t)b.L.cap;
+  uint64_t run = excl;
+  for (int t = beg; t < end; ++t) {
+    const uint64_t e = run + tc[t];
+    cursor[t] = (uint32_t)(run < 0xFFFFFFFFull ? run : 0xFFFFFFFFull);
+    ranges[t] = make_uint2((uint32_t)(run < cap ? run : cap), (uint32_t)(e < cap ? e : cap));
+    run = e;
   }
   if (threadIdx.x == 0) {
-    const uint64_t cap = (uint64_t)b.L.cap;
     cnt[3] = total;
-    cnt[1] = (uint32_t)min((uint64_t)total, cap);
+    cnt[1] = (uint32_t)((uint64_t)total < cap ? (uint64_t)total : cap);
     cnt[2] = (uint64_t)total > cap ? 1u : 0u;
   }
 }
 
-__global__ void __launch_bounds__(kScanThreads) offsets_downsweep_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const int64_t n = b.n;
-  const int64_t nt = (n + kScanTile - 1) / kScanTile;
-  const uint32_t* vals = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.vals0);
-  const uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tt);
-  const uint32_t* part = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.partial);
-  uint32_t* offs = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.offs);
-  __shared__ uint32_t sw[32];
-  for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
-    // thread owns kScanItems consecutive items
-    uint32_t v[kScanItems];
-    uint32_t s = 0;
-#pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-      const int64_t p = tile * kScanTile + (int64_t)threadIdx.x * kScanItems + it;
-      v[it] = p < n ? tt[vals[p]] : 0u;
-      s += v[it];
-    }
-    uint32_t excl;
-    block_exclusive_scan<kScanThreads>(s, excl, sw);
-    excl += part[tile];
-#pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-      const int64_t p = tile * kScanTile + (int64_t)threadIdx.x * kScanItems + it;
-      if (p < n) offs[p] = excl;
-      excl += v[it];
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------ duplicate
+// ------------------------------------------------------------------------------ duplicate (a5)
 __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= b.n) return;
-  const uint32_t* vals = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.vals0);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < b.n;
   const uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tt);
-  const uint2* rect = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.rect);
-  const uint32_t* offs = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.offs);
-  uint32_t* ikey = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.ikey0);
-  uint32_t* ival = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.ival0);
-  const uint32_t gid = vals[p];
-  if (tt[gid] == 0) return;
-  const uint2 r = rect[gid];
-  const uint32_t x0 = r.x & 0xFFFF, y0 = r.x >> 16, x1 = r.y & 0xFFFF, y1 = r.y >> 16;
+  const bool keep = valid && tt[i] != 0;
+  uint32_t key = 0;
+  uint2 r = make_uint2(0, 0);
+  if (keep) {
+    key = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.keys)[i];
+    r = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.rect)[i];
+  }
+  uint32_t* cursor = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.cursor);
+  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst);
+  const int x0 = r.x & 0xFFFF, y0 = r.x >> 16, x1 = r.y & 0xFFFF, y1 = r.y >> 16;
   const uint64_t cap = (uint64_t)b.L.cap;
-  uint64_t o = offs[p];
-  for (uint32_t ty = y0; ty < y1; ++ty)
-    for (uint32_t tx = x0; tx < x1; ++tx, ++o)
-      if (o < cap) { ikey[o] = ty * (uint32_t)b.gx + tx; ival[o] = gid; }
-}
-
-// ------------------------------------------------------------------------------ tile ranges
-__global__ void ranges_clear_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < b.ntiles) ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[t] = make_uint2(0, 0);
-}
-
-__global__ void ranges_kernel(const __grid_constant__ RenderBatch b, size_t keys_off) {
-  const int f = blockIdx.y;
-  const uint32_t M = cnt_ptr(b, f)[1];
-  const uint32_t* keys = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, keys_off);
-  uint2* ranges = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x) {
-    const uint32_t t = keys[i];
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
-    if (i == M - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+  const unsigned long long v = ((unsigned long long)key << 32) | (uint32_t)i;
+  __shared__ int sbox[4];
+  __shared__ uint32_t sbase[kAggTiles];
+  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
+  if (agg_fits(box)) {
+    // one global cursor claim per touched tile for the whole CTA, slots handed out in smem
+    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    for (int q = threadIdx.x; q < area; q += blockDim.x) sbase[q] = 0;
+    __syncthreads();
+    if (keep)
+      for (int ty = y0; ty < y1; ++ty)
+        for (int tx = x0; tx < x1; ++tx) atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
+    __syncthreads();
+    for (int q = threadIdx.x; q < area; q += blockDim.x)
+      if (sbase[q]) sbase[q] = atomicAdd(cursor + (box.y0 + q / bw) * b.gx + box.x0 + q % bw, sbase[q]);
+    __syncthreads();
+    if (keep)
+      for (int ty = y0; ty < y1; ++ty)
+        for (int tx = x0; tx < x1; ++tx) {
+          const uint32_t pos = atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
+          if (pos < cap) inst[pos] = v;
+        }
+  } else if (keep) {
+    for (int ty = y0; ty < y1; ++ty)
+      for (int tx = x0; tx < x1; ++tx) {
+        const uint32_t pos = atomicAdd(cursor + ty * b.gx + tx, 1u);
+        if (pos < cap) inst[pos] = v;
+      }
   }
 }
+
+// ------------------------------------------------------------------------------ tile sort (a6)
+// Bitonic sort of n2 (power of two) 64-bit keys in shared memory by NT threads.
+template <int NT>
+__device__ __forceinline__ void bitonic_sort_smem(unsigned long long* sk, int n2) {
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int p = threadIdx.x; p < (n2 >> 1); p += NT) {
+        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));   // bit j of i is 0; partner i | j
+        const unsigned long long a = sk[i], c = sk[i | j];
+        const bool up = (i & k) == 0;
+        if ((a > c) == up) { sk[i] = c; sk[i | j] = a; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int pow2_at_least(int v) {
+  int p = 2;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// Lists of 2..sort_cap instances: one warp per tile sorts the list in registers — bitonic network over
+// N2 = 32 R keys in the striped layout (key e = 32 r + lane in register r of lane `lane`), so that
+// partners at distance j < 32 are exchanged with shuffles and those at j >= 32 sit in the same lane —
+// and writes it back in place.  Longer lists are queued for long_sort_kernel.
+template <int R>
+__device__ __forceinline__ void sort_reg_stage(unsigned long long (&v)[R], int jr, int k) {
+  // partners 32 jr apart: registers r and r | jr of the same lane; k >= 64 so the direction
+  // depends on r only
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if ((r & jr) == 0 && (r | jr) < R) {
+      const bool up = ((32 * r) & k) == 0;
+      const unsigned long long a = v[r], c = v[r | jr];
+      const bool sw = (a > c) == up;
+      v[r] = sw ? c : a;
+      v[r | jr] = sw ? a : c;
+    }
+  }
+}
+
+template <int R>
+__device__ __noinline__ void warp_sort_tile(unsigned long long* inst, int L, int lane) {
+  constexpr int N2 = 32 * R;
+  unsigned long long v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = 32 * r + lane;
+    v[r] = e < L ? inst[e] : ~0ull;
+  }
+#pragma unroll 1
+  for (int k = 2; k <= N2; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j >= 32; j >>= 1) {
+      // jr is a runtime value: dispatch to a fully unrolled stage so v stays in registers
+      switch (j >> 5) {
+        case 1: sort_reg_stage<R>(v, 1, k); break;
+        case 2: sort_reg_stage<R>(v, 2, k); break;
+        case 4: sort_reg_stage<R>(v, 4, k); break;
+        case 8: sort_reg_stage<R>(v, 8, k); break;
+        default: sort_reg_stage<R>(v, 16, k); break;
+      }
+    }
+#pragma unroll 1
+    for (int j = min(k >> 1, 16); j > 0; j >>= 1) {
+      const bool lower = (lane & j) == 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+        const bool up = (((32 * r) | lane) & k) == 0;
+        const bool keep_min = lower == up;
+        const bool lt = v[r] < o;
+        v[r] = (lt == keep_min) ? v[r] : o;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = 32 * r + lane;
+    if (e < L) inst[e] = v[r];
+  }
+}
+
+constexpr int kTileSortWarps = 4;
+__global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __grid_constant__ RenderBatch b) {
+  const int f = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kTileSortWarps + warp;
+  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
+  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
+  const int L = (int)(rg.y - rg.x);
+  if (L <= 1) return;
+  if (L > b.sort_cap) {
+    if (lane == 0) {
+      const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
+      ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list)[w] = (uint32_t)tile;
+    }
+    return;
+  }
+  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
+  if (L <= 32) warp_sort_tile<1>(inst, L, lane);
+  else if (L <= 64) warp_sort_tile<2>(inst, L, lane);
+  else if (L <= 128) warp_sort_tile<4>(inst, L, lane);
+  else if (L <= 256) warp_sort_tile<8>(inst, L, lane);
+  else if (L <= 512) warp_sort_tile<16>(inst, L, lane);
+  else warp_sort_tile<32>(inst, L, lane);
+}
+
+// Lists longer than b.sort_cap: sorted in place in global memory by one CTA per tile — bitonic runs
+// of kLargeSortChunk in shared memory, then merge-path merges ping-ponging through inst2.
+__device__ __forceinline__ void long_sort_one(const RenderBatch& b, int f, int tile) {
+  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
+  const int L = (int)(rg.y - rg.x);
+  unsigned long long* A = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
+  unsigned long long* B = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst2) + rg.x;
+  __shared__ unsigned long long sk[kLargeSortChunk];
+  for (int c0 = 0; c0 < L; c0 += kLargeSortChunk) {
+    const int len = min(kLargeSortChunk, L - c0);
+    const int n2 = pow2_at_least(len);
+    for (int q = threadIdx.x; q < n2; q += kLargeSortThreads) sk[q] = q < len ? A[c0 + q] : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem<kLargeSortThreads>(sk, n2);
+    for (int q = threadIdx.x; q < len; q += kLargeSortThreads) A[c0 + q] = sk[q];
+    __syncthreads();
+  }
+  unsigned long long* src = A;
+  unsigned long long* dst = B;
+  for (int w = kLargeSortChunk; w < L; w <<= 1) {
+    for (int s = 0; s < L; s += 2 * w) {
+      const int na = min(w, L - s), nb = max(0, min(w, L - s - w));
+      const unsigned long long* a = src + s;
+      const unsigned long long* bq = src + s + na;
+      const int total = na + nb;
+      const int per = (total + kLargeSortThreads - 1) / kLargeSortThreads;
+      const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
+      if (d0 < d1) {
+        // merge path: i = number of a-elements among the first d0 outputs (keys are unique)
+        int lo = max(0, d0 - nb), hi = min(d0, na);
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (a[m] < bq[d0 - 1 - m]) lo = m + 1; else hi = m;
+        }
+        int ia = lo, ib = d0 - lo;
+        for (int d = d0; d < d1; ++d) {
+          const bool take_a = ib >= nb || (ia < na && a[ia] < bq[ib]);
+          dst[s + d] = take_a ? a[ia++] : bq[ib++];
+        }
+      }
+    }
+    __syncthreads();
+    unsigned long long* t = src; src = dst; dst = t;
+  }
+  if (src != A)
+    for (int q = threadIdx.x; q < L; q += kLargeSortThreads) A[q] = src[q];
+}
+
+__global__ void __launch_bounds__(kLargeSortThreads) long_sort_kernel(const __grid_constant__ RenderBatch b) {
+  const int f = blockIdx.y;
+  const uint32_t n_long = cnt_ptr(b, f)[4];
+  const uint32_t* work = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list);
+  for (uint32_t w = blockIdx.x; w < n_long; w += gridDim.x) {
+    long_sort_one(b, f, (int)work[w]);
+    __syncthreads();
+  }
+}
+
 
 // ------------------------------------------------------------------------------ blend (Eq. 4)
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -472,37 +559,65 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Eq. 4 for one pixel and one Gaussian, branch-free (the warp stays converged).
-// p2 = power * log2(e); the Gaussian is skipped if p2 > 0 or alpha < 1/255 (R9); the pixel stops
-// (without adding the Gaussian) when T (1 - alpha) < 1e-4 (R9).
 struct PixelState {
   float T, c0, c1, c2;
   bool done;
   uint32_t ncon, nev;
 };
 
-__device__ __forceinline__ void blend_step(PixelState& s, float p2, float lo, float r, float g, float bch,
+// Eq. 4 for one pixel and one Gaussian; e = p2 + log2(o) with p2 = power * log2(e) (R9: skip if
+// power > 0 or alpha < 1/255; stop, without adding it, when T (1 - alpha) < 1e-4).
+template <bool DBG>
+__device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, float r, float g, float bch,
                                            uint32_t pos) {
-  const float alpha = fminf(kAlphaMax, ex2_approx(p2 + lo));
-  const bool ok = !s.done && !(p2 > 0.f) && !(alpha < kAlphaMin);
-  const float test_T = s.T * (1.f - alpha);
+  const float alpha = fminf(kAlphaMax, ex2_approx(e));
+  const bool ok = !s.done && !(e > lo) && alpha >= kAlphaMin;
+  const float test_T = fmaf(-alpha, s.T, s.T);
   const bool stop = ok && test_T < kTMin;
-  const bool add = ok && !stop;
-  if (stop) { s.done = true; s.nev = pos; }
-  const float w = add ? alpha * s.T : 0.f;
-  s.c0 = fmaf(r, w, s.c0);
-  s.c1 = fmaf(g, w, s.c1);
-  s.c2 = fmaf(bch, w, s.c2);
-  s.T = add ? test_T : s.T;
-  s.ncon += add ? 1u : 0u;
+  if (ok && !stop) {
+    const float w = alpha * s.T;
+    s.c0 = fmaf(r, w, s.c0);
+    s.c1 = fmaf(g, w, s.c1);
+    s.c2 = fmaf(bch, w, s.c2);
+    s.T = test_T;
+    if (DBG) s.ncon += 1u;
+  }
+  if (stop) {
+    s.done = true;
+    if (DBG) s.nev = pos;
+  }
+}
+
+// Conservative ellipse-vs-box cull: true unless q2(d) = qa dx^2 + qb dx dy + qc dy^2 (the negated
+// log2-domain exponent, PSD) exceeds thr over the whole box [xl,xh] x [yl,yh] of offsets
+// d = pixel - mean.  The minimum of a convex quadratic over a box that does not contain its
+// minimiser d = 0 lies on a face whose half-space excludes 0 (KKT), so at most one x-face and one
+// y-face are candidates; on each the 1-D minimiser is clamped to the face.  An inexact minimiser
+// only raises the computed value by qc * delta^2 (quadratic in its error), far inside thr's margin.
+__device__ __forceinline__ bool box_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
+                                              float yl, float yh) {
+  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+  const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
+  float q = 0.f;
+  if (ex != 0.f) {
+    const float yy = fminf(fmaxf(__fdividef(-qb * ex, 2.f * qc), yl), yh);
+    q = fmaf(fmaf(qa, ex, qb * yy), ex, qc * yy * yy);
+  }
+  if (ey != 0.f) {
+    const float xx = fminf(fmaxf(__fdividef(-qb * ey, 2.f * qa), xl), xh);
+    const float q2 = fmaf(fmaf(qc, ey, qb * xx), ey, qa * xx * xx);
+    q = ex != 0.f ? fminf(q, q2) : q2;
+  }
+  return q <= thr;
 }
 
 template <bool DBG>
-__global__ void __launch_bounds__(128) blend_kernel(const __grid_constant__ RenderBatch b, size_t vals_off) {
-  // One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 pixel box ((w&1)*8, (w>>1)*8); each lane
-  // two pixels (x, y) and (x, y+4).  Per batch of 256 Gaussians (smem), each warp tests 32 Gaussians
-  // at a time against a conservative alpha bound over its box (lane-parallel + ballot) and then
-  // evaluates only the survivors for its 64 pixels, in list order.
+__global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_constant__ RenderBatch b) {
+  // One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 pixel box ((w&1)*8, (w>>1)*8); lane l owns
+  // pixel A = (l&7, l>>3) of the box's upper 8x4 half and pixel B = A + (0,4) of the lower half.  The
+  // tile's list (sorted by (depth, gid)) is walked in batches of 256 records staged in smem; per 32
+  // Gaussians each lane tests one against the exact ellipse bound over both half-boxes, and the warp
+  // evaluates, in list order, each Gaussian on the half-boxes it can reach (warp-uniform branches).
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % b.gx, ty = tile / b.gx;
@@ -513,60 +628,78 @@ __global__ void __launch_bounds__(128) blend_kernel(const __grid_constant__ Rend
   const bool inA = pxi < b.width && pyA < b.height;
   const bool inB = pxi < b.width && pyB < b.height;
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
-  const uint32_t* gids = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, vals_off);
+  const int L = (int)(rg.y - rg.x);
+  const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
   __shared__ float4 s0[256], s1[256];
   __shared__ float2 s2[256];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   const float lx = (float)lxi, ly = (float)lyi;
-  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, byh = (float)(by0 + 7);
-  PixelState A{1.f, 0.f, 0.f, 0.f, !inA, 0u, rg.y - rg.x};
-  PixelState B{1.f, 0.f, 0.f, 0.f, !inB, 0u, rg.y - rg.x};
-  for (uint32_t start = rg.x; start < rg.y; start += 256) {
-    if (__syncthreads_count(A.done && B.done) == 128) break;
+  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, bym = (float)(by0 + 3),
+              byn = (float)(by0 + 4), byh = (float)(by0 + 7);
+  uint32_t n_tested = 0, n_evald = 0;    // DBG: per-warp cull statistics (half-box evaluations)
+  PixelState A{1.f, 0.f, 0.f, 0.f, !inA, 0u, (uint32_t)L};
+  PixelState B{1.f, 0.f, 0.f, 0.f, !inB, 0u, (uint32_t)L};
+  for (int start = 0; start < L; start += 256) {
+    if (__syncthreads_count(A.done && B.done) == kBlendThreads) break;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const uint32_t idx = start + threadIdx.x + 128 * k;
-      if (idx < rg.y) {
-        const uint32_t g = gids[idx];
+      const int idx = start + threadIdx.x + kBlendThreads * k;
+      if (idx < L) {
+        const uint32_t g = (uint32_t)inst[idx];
         float4 a = rec[3 * g + 0];
         const float4 c = rec[3 * g + 2];
         a.x = (a.x - tx0) + c.y;      // tile-relative mean: exact hi difference + lo part
         a.y = (a.y - ty0) + c.z;
-        s0[threadIdx.x + 128 * k] = a;
-        s1[threadIdx.x + 128 * k] = rec[3 * g + 1];
-        s2[threadIdx.x + 128 * k] = make_float2(c.x, c.w);
+        s0[threadIdx.x + kBlendThreads * k] = a;
+        s1[threadIdx.x + kBlendThreads * k] = rec[3 * g + 1];
+        s2[threadIdx.x + kBlendThreads * k] = make_float2(c.x, c.w);
       }
     }
     __syncthreads();
-    const int cnt = (int)min(256u, rg.y - start);
+    const int cnt = min(256, L - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (__all_sync(0xffffffffu, A.done && B.done)) break;
+      const bool liveA = __any_sync(0xffffffffu, !A.done), liveB = __any_sync(0xffffffffu, !B.done);
+      if (!liveA && !liveB) break;
       const int jt = c0 + lane;
-      bool need = false;
+      bool needA = false, needB = false;
       if (jt < cnt) {
         const float4 a = s0[jt];
-        const float ddx = fmaxf(fmaxf(bxl - a.x, a.x - bxh), 0.f);
-        const float ddy = fmaxf(fmaxf(byl - a.y, a.y - byh), 0.f);
-        need = ddx * ddx + ddy * ddy <= s2[jt].y;
+        const float qa = -a.z, qb = -a.w, qc = -s1[jt].x, thr = s2[jt].y;
+        const float xl = bxl - a.x, xh = bxh - a.x;
+        needA = liveA && box_may_reach(qa, qb, qc, thr, xl, xh, byl - a.y, bym - a.y);
+        needB = liveB && box_may_reach(qa, qb, qc, thr, xl, xh, byn - a.y, byh - a.y);
       }
-      uint32_t m = __ballot_sync(0xffffffffu, need);
+      const uint32_t mA = __ballot_sync(0xffffffffu, needA), mB = __ballot_sync(0xffffffffu, needB);
+      if (DBG) { n_tested += (uint32_t)min(32, cnt - c0); n_evald += __popc(mA) + __popc(mB); }
+      uint32_t m = mA | mB;
       while (m) {
-        const int j = c0 + __ffs(m) - 1;
+        const int bit = __ffs(m) - 1;
         m &= m - 1;
+        const int j = c0 + bit;
         const float4 a = s0[j], q = s1[j];
         const float bch = s2[j].x;
         const float dx = a.x - lx;
-        const float dyA = a.y - ly, dyB = dyA - 4.f;
-        const float adx = a.z * dx;                         // A' dx, shared by both pixels
-        const float pA = fmaf(dx, fmaf(a.w, dyA, adx), q.x * dyA * dyA);
-        const float pB = fmaf(dx, fmaf(a.w, dyB, adx), q.x * dyB * dyB);
-        const uint32_t pos = start + j - rg.x + 1;
-        blend_step(A, pA, q.y, q.z, q.w, bch, pos);
-        blend_step(B, pB, q.y, q.z, q.w, bch, pos);
+        const float bdx = a.w * dx;                              // b2 dx, shared by both pixels
+        const float base = fmaf(a.z * dx, dx, q.y);              // a2 dx^2 + log2(o)
+        const float dyA = a.y - ly;
+        const uint32_t pos = (uint32_t)(start + j + 1);
+        if ((mA >> bit) & 1u) {
+          const float eA = fmaf(dyA, fmaf(q.x, dyA, bdx), base);
+          blend_step<DBG>(A, eA, q.y, q.z, q.w, bch, pos);
+        }
+        if ((mB >> bit) & 1u) {
+          const float dyB = dyA - 4.f;
+          const float eB = fmaf(dyB, fmaf(q.x, dyB, bdx), base);
+          blend_step<DBG>(B, eB, q.y, q.z, q.w, bch, pos);
+        }
       }
     }
     __syncthreads();
+  }
+  if (DBG && b.blend_work && f == 0 && lane == 0) {
+    atomicAdd(b.blend_work, (unsigned long long)n_evald);
+    atomicAdd(b.blend_work + 1, (unsigned long long)n_tested);
   }
   const size_t hw = (size_t)b.width * b.height;
   float* img = b.image[f];
@@ -588,7 +721,7 @@ __global__ void __launch_bounds__(128) blend_kernel(const __grid_constant__ Rend
   }
 }
 
-int num_sms() {
+int num_sms_cached() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -599,32 +732,6 @@ int num_sms() {
   return sms;
 }
 
-cudaError_t run_sort(SortArgs a, int n_frames, int64_t max_items, int key_bits, bool& swapped,
-                     cudaStream_t s) {
-  // key_bits total bits, split into passes of <= 8 bits; ping-pong kin <-> kout.
-  swapped = false;
-  if (key_bits <= 0) return cudaSuccess;
-  const int passes = (key_bits + 7) / 8;
-  const int base = key_bits / passes, extra = key_bits % passes;
-  const int64_t tiles = (max_items + kSortTile - 1) / kSortTile;
-  int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * 8 / std::max(1, n_frames) + 1));
-  dim3 grid((unsigned)gx, n_frames);
-  int shift = 0;
-  for (int p = 0; p < passes; ++p) {
-    a.shift = shift;
-    a.bits = base + (p < extra ? 1 : 0);
-    shift += a.bits;
-    radix_hist_kernel<<<grid, kSortThreads, 0, s>>>(a);
-    radix_scan_kernel<<<n_frames, 1024, 0, s>>>(a);
-    radix_scatter_kernel<<<grid, kSortThreads, 0, s>>>(a);
-    note_launches(3);
-    std::swap(a.kin, a.kout);
-    std::swap(a.vin, a.vout);
-    swapped = !swapped;
-  }
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
@@ -632,75 +739,57 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   const int64_t n = b.n;
   const unsigned nb = (unsigned)std::max<int64_t>(1, (n + 255) / 256);
   prof_mark(FGS_STAGE_PREPROCESS, true, s);
-  preprocess_kernel<<<dim3(nb, F), 256, 0, s>>>(b);
-  note_launches(1);
+  clear_kernel<<<dim3((unsigned)std::min(64, (b.ntiles + 255) / 256), F), 256, 0, s>>>(b);
+  switch (b.sh_degree) {
+    case 0: preprocess_kernel<0><<<dim3(nb, F), 256, 0, s>>>(b); break;
+    case 1: preprocess_kernel<1><<<dim3(nb, F), 256, 0, s>>>(b); break;
+    case 2: preprocess_kernel<2><<<dim3(nb, F), 256, 0, s>>>(b); break;
+    default: preprocess_kernel<3><<<dim3(nb, F), 256, 0, s>>>(b); break;
+  }
+  note_launches(2);
   prof_mark(FGS_STAGE_PREPROCESS, false, s);
-  // depth sort: 32-bit keys, values = index (stable -> ties by index)
-  SortArgs a{};
-  a.ws = b.ws; a.stride = b.ws_stride; a.cnt = b.L.cnt; a.cnt_idx = 0; a.hist = b.L.hist;
-  a.kin = b.L.keys0; a.vin = b.L.vals0; a.kout = b.L.keys1; a.vout = b.L.vals1;
-  bool sw = false;
-  prof_mark(FGS_STAGE_DEPTH_SORT, true, s);
-  cudaError_t e = run_sort(a, F, n, 32, sw, s);
-  prof_mark(FGS_STAGE_DEPTH_SORT, false, s);
-  if (e != cudaSuccess) return e;
-  // (4 passes -> result back in keys0/vals0)
-  const int64_t nt = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
-  const unsigned sg = (unsigned)std::min<int64_t>(nt, (int64_t)num_sms() * 4 / F + 1);
-  prof_mark(FGS_STAGE_OFFSETS, true, s);
-  offsets_reduce_kernel<<<dim3(sg, F), kScanThreads, 0, s>>>(b);
-  offsets_partials_kernel<<<F, 1024, 0, s>>>(b);
-  offsets_downsweep_kernel<<<dim3(sg, F), kScanThreads, 0, s>>>(b);
-  note_launches(3);
-  prof_mark(FGS_STAGE_OFFSETS, false, s);
+  prof_mark(FGS_STAGE_TILE_SCAN, true, s);
+  tile_scan_kernel<<<F, kScanThreads, 0, s>>>(b);
+  note_launches(1);
+  prof_mark(FGS_STAGE_TILE_SCAN, false, s);
   prof_mark(FGS_STAGE_DUPLICATE, true, s);
   duplicate_kernel<<<dim3(nb, F), 256, 0, s>>>(b);
   note_launches(1);
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
-  // tile sort: ceil(log2(ntiles)) bits
-  int tbits = 0;
-  while ((1 << tbits) < b.ntiles) ++tbits;
-  SortArgs t{};
-  t.ws = b.ws; t.stride = b.ws_stride; t.cnt = b.L.cnt; t.cnt_idx = 1; t.hist = b.L.hist;
-  t.kin = b.L.ikey0; t.vin = b.L.ival0; t.kout = b.L.ikey1; t.vout = b.L.ival1;
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
-  e = run_sort(t, F, b.L.cap, tbits, sw, s);
-  prof_mark(FGS_STAGE_TILE_SORT, false, s);
-  if (e != cudaSuccess) return e;
-  const size_t kfin = sw ? b.L.ikey1 : b.L.ikey0;
-  const size_t vfin = sw ? b.L.ival1 : b.L.ival0;
-  prof_mark(FGS_STAGE_RANGES, true, s);
-  ranges_clear_kernel<<<dim3((b.ntiles + 255) / 256, F), 256, 0, s>>>(b);
-  const unsigned rg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((b.L.cap + 255) / 256, (int64_t)num_sms() * 8 / F + 1));
-  ranges_kernel<<<dim3(rg, F), 256, 0, s>>>(b, kfin);
+  tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
+  // long lists: a few persistent CTAs per frame walk the worklist (usually empty)
+  long_sort_kernel<<<dim3((unsigned)std::max(1, std::min(32, num_sms_cached() / F)), F), kLargeSortThreads, 0, s>>>(b);
   note_launches(2);
-  prof_mark(FGS_STAGE_RANGES, false, s);
+  prof_mark(FGS_STAGE_TILE_SORT, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);
-  const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0];
+  const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;
   if (dbg)
-    blend_kernel<true><<<dim3(b.ntiles, F), 128, 0, s>>>(b, vfin);
+    blend_kernel<true><<<dim3(b.ntiles, F), kBlendThreads, 0, s>>>(b);
   else
-    blend_kernel<false><<<dim3(b.ntiles, F), 128, 0, s>>>(b, vfin);
+    blend_kernel<false><<<dim3(b.ntiles, F), kBlendThreads, 0, s>>>(b);
   note_launches(1);
   prof_mark(FGS_STAGE_BLEND, false, s);
   return cudaGetLastError();
 }
 
-// Debug outputs: copy the per-frame intermediates of frame 0 into caller buffers.
-__global__ void debug_copy_kernel(const __grid_constant__ RenderBatch b, fgs_render_aux aux, size_t kfin,
-                                  size_t vfin) {
+// Debug outputs: copy the per-frame intermediates of frame 0 into caller buffers (after a DBG blend,
+// which writes every tile's sorted list back to the instance array).
+__global__ void debug_copy_kernel(const __grid_constant__ RenderBatch b, fgs_render_aux aux) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t* cnt = cnt_ptr(b, 0);
   const uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, b.L.tt);
   const uint2* rect = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.rect);
   const int32_t* radii = ws_ptr<int32_t>(b.ws, b.ws_stride, 0, b.L.radii);
+  const uint32_t* keys = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, b.L.keys);
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, 0, b.L.rec);
+  const uint2* ranges = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.ranges);
+  const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, 0, b.L.inst);
   if (i < b.n) {
-    // depth keys are permuted by the sort; recompute key from the record of kept Gaussians via
-    // the sorted arrays below instead.  Here: per-Gaussian outputs.
     const bool kept = tt[i] != 0;
     if (aux.radii) aux.radii[i] = radii[i];
     if (aux.tiles_touched) aux.tiles_touched[i] = tt[i];
+    if (aux.depth_key) aux.depth_key[i] = kept ? keys[i] : 0u;
     if (aux.rect) {
       const uint2 r = rect[i];
       aux.rect[4 * i + 0] = (int32_t)(r.x & 0xFFFF);
@@ -714,35 +803,23 @@ __global__ void debug_copy_kernel(const __grid_constant__ RenderBatch b, fgs_ren
       aux.mean2d[2 * i + 1] = kept ? a.y + c.z : 0.f;
     }
   }
-  // depth keys: scatter from the depth-sorted arrays (keys0/vals0 after 4 passes)
-  if (aux.depth_key && i < b.n) {
-    const uint32_t* k = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, b.L.keys0);
-    const uint32_t* v = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, b.L.vals0);
-    const uint32_t key = k[i];
-    aux.depth_key[v[i]] = key == 0xFFFFFFFFu ? 0u : key;
-  }
   const uint32_t M = cnt[1];
-  if (i < (int64_t)M) {
-    if (aux.sorted_tile) aux.sorted_tile[i] = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, kfin)[i];
-    if (aux.sorted_gid) aux.sorted_gid[i] = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, vfin)[i];
-  }
-  if (i < b.ntiles && aux.ranges) {
-    const uint2 r = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.ranges)[i];
-    aux.ranges[2 * i] = r.x;
-    aux.ranges[2 * i + 1] = r.y;
+  if (i < (int64_t)M && aux.sorted_gid) aux.sorted_gid[i] = (uint32_t)inst[i];
+  if (i < b.ntiles) {
+    const uint2 r = ranges[i];
+    if (aux.ranges) {
+      aux.ranges[2 * i] = r.x;
+      aux.ranges[2 * i + 1] = r.y;
+    }
+    if (aux.sorted_tile)
+      for (uint32_t p = r.x; p < r.y; ++p) aux.sorted_tile[p] = (uint32_t)i;
   }
   if (i == 0 && aux.n_instances) aux.n_instances[0] = cnt[3];
 }
 
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s) {
-  int tbits = 0;
-  while ((1 << tbits) < b.ntiles) ++tbits;
-  const int passes = tbits > 0 ? (tbits + 7) / 8 : 0;
-  const bool sw = passes & 1;
-  const size_t kfin = sw ? b.L.ikey1 : b.L.ikey0;
-  const size_t vfin = sw ? b.L.ival1 : b.L.ival0;
   const int64_t m = std::max<int64_t>(std::max<int64_t>(b.n, b.L.cap), b.ntiles);
-  debug_copy_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(b, aux, kfin, vfin);
+  debug_copy_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(b, aux);
   note_launches(1);
   return cudaGetLastError();
 }

@@ -57,15 +57,16 @@ class fgs_camera(ctypes.Structure):
 class fgs_render_aux(ctypes.Structure):
     _fields_ = [(k, c_void_p) for k in ("radii", "rect", "mean2d", "depth_key", "tiles_touched",
                                         "n_instances", "sorted_tile", "sorted_gid", "ranges",
-                                        "final_T", "n_contrib", "n_evaluated")]
+                                        "final_T", "n_contrib", "n_evaluated", "blend_work")]
 
 
 _LIB = None
 EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_batch", "fgs_render_workspace_bytes",
            "fgs_render", "fgs_render_batch", "fgs_render_debug", "fgs_render_status", "fgs_frames",
            "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_profile_enable", "fgs_profile_read",
-           "fgs_launch_count", "fgs_last_error", "fgs_version")
-STAGES = ("deform", "preprocess", "depth_sort", "offsets", "duplicate", "tile_sort", "ranges", "blend")
+           "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version")
+STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend")
+FGS_TUNE_TILE_SORT_CAP = 0
 
 
 def lib():
@@ -99,11 +100,14 @@ def lib():
         L.fgs_profile_enable.argtypes = [c_int]
         L.fgs_profile_read.argtypes = [P(ctypes.c_double), P(c_int64)]
         L.fgs_launch_count.restype = c_int64
+        L.fgs_set_tuning.argtypes = [c_int32, c_int64]
+        L.fgs_get_tuning.argtypes = [c_int32]
+        L.fgs_get_tuning.restype = c_int64
         L.fgs_last_error.restype = c_char_p
         L.fgs_version.restype = c_char_p
         for name in EXPORTS:
             if name not in ("fgs_render_workspace_bytes", "fgs_frames_host_workspace_bytes", "fgs_launch_count",
-                            "fgs_last_error", "fgs_version"):
+                            "fgs_get_tuning", "fgs_last_error", "fgs_version"):
                 getattr(L, name).restype = c_int
         _LIB = L
     return _LIB
@@ -210,6 +214,14 @@ def fgs_profile_read():
 
 def fgs_launch_count():
     return int(lib().fgs_launch_count())
+
+
+def fgs_set_tuning(key, value):
+    return _check(lib().fgs_set_tuning(key, value))
+
+
+def fgs_get_tuning(key):
+    return int(lib().fgs_get_tuning(key))
 
 
 def fgs_last_error():

@@ -237,13 +237,32 @@ def _cameras_times(rng, name, width, height, bg, n_frames=None):
     return cams, _f32(times)
 
 
+def morton_order(means, bmin, bmax, bits: int = 10) -> np.ndarray:
+    """Permutation that sorts points by the Z-order (Morton) code of their position quantised to
+    2^bits cells per axis of the AABB (ties by original index).  A data-layout step of model load
+    (SURVEY §8(d) "Model order"), not arithmetic of the method: every Gaussian keeps its values."""
+    m = np.asarray(means, np.float64)
+    lo, hi = np.asarray(bmin, np.float64), np.asarray(bmax, np.float64)
+    u = np.clip((m - lo) / (hi - lo), 0.0, 1.0)
+    q = np.minimum((u * (1 << bits)).astype(np.int64), (1 << bits) - 1)
+    q = np.where(np.isfinite(m), q, 0)
+    code = np.zeros(m.shape[0], np.int64)
+    for bit in range(bits):
+        for a in range(3):
+            code |= ((q[:, a] >> bit) & 1) << (3 * bit + (2 - a))
+    return np.lexsort((np.arange(m.shape[0]), code))
+
+
 def make_scene(name: str, *, n: Optional[int] = None, width: Optional[int] = None,
                height: Optional[int] = None, n_frames: Optional[int] = None,
-               seed: Optional[int] = None) -> Scene:
+               seed: Optional[int] = None, order: str = "morton") -> Scene:
     """Build a BASELINE.json config (name in CONFIGS or ALIASES).
 
     Overrides (n, width, height, n_frames, seed) produce reduced variants of the
     same distributions for parity tests; the draw order is unchanged.
+    order: "morton" (default) stores the Gaussians in Z-order of their canonical means over the
+    field AABB, the layout a renderer gives a model at load time; "draw" keeps the
+    draw order.  The stored order defines the Gaussian index (the sort tie-break, reading R14).
     """
     name = ALIASES.get(name, name)
     cfg = dict(CONFIGS[name])
@@ -294,6 +313,11 @@ def make_scene(name: str, *, n: Optional[int] = None, width: Optional[int] = Non
               b_s=np.zeros(3, np.float32))
 
     cams, times = _cameras_times(rng, name, W, H, cfg["bg"], n_frames)
+    if order == "morton":
+        perm = morton_order(means, bmin, bmax)
+        means, log_scales, q, opac, sh = means[perm], log_scales[perm], q[perm], opac[perm], sh[perm]
+    elif order != "draw":
+        raise ValueError(f"unknown order {order!r}")
     return Scene(name=name, seed=seed, means=_f32(means), log_scales=_f32(log_scales),
                  quats=_f32(q), opacity_logits=_f32(opac), sh=_f32(sh), sh_degree=deg,
                  field=fld, mlp=mlp, cameras=cams, times=times)

@@ -47,6 +47,7 @@ def gpu_render_debug(ds, cam, dstruct, max_instances=None):
         "final_T": torch.zeros((H, W), dtype=torch.float32, device=dev),
         "n_contrib": torch.zeros((H, W), dtype=torch.int32, device=dev),
         "n_evaluated": torch.zeros((H, W), dtype=torch.int32, device=dev),
+        "blend_work": torch.zeros(2, dtype=torch.int64, device=dev),
     }
     aux = fgs.fgs_render_aux(**{k: v.data_ptr() for k, v in t.items()})
     image = torch.full((3, H, W), float("nan"), dtype=torch.float32, device=dev)

@@ -74,4 +74,23 @@ def test_struct_layouts():
     assert ctypes.sizeof(fgs.fgs_gaussians) == 8 + 8 + 5 * 8
     assert ctypes.sizeof(fgs.fgs_camera) == 4 * (9 + 3 + 4 + 2 + 3)
     assert fgs.fgs_hexplanes.planes.offset == 56
-    assert ctypes.sizeof(fgs.fgs_render_aux) == 12 * 8
+    assert ctypes.sizeof(fgs.fgs_render_aux) == 13 * 8
+
+
+def test_tuning_knob_host_only(L):
+    cap0 = fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_SORT_CAP)
+    assert cap0 == 1024
+    fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 64)
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_SORT_CAP) == 64
+    fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, cap0)
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 0) == fgs.FGS_E_INVALID
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 4096) == fgs.FGS_E_INVALID
+    assert L.fgs_set_tuning(99, 1) == fgs.FGS_E_INVALID
+    assert fgs.fgs_get_tuning(99) == -1
+
+
+def test_stage_names_match_header():
+    src = open(HEADER).read()
+    stages = re.findall(r"FGS_STAGE_(\w+) ?=?", src)
+    stages = [s for i, s in enumerate(stages) if s not in stages[:i]]
+    assert [s.lower() for s in stages] == list(fgs.STAGES)

@@ -3,7 +3,7 @@ and the recipe of SURVEY §8(d) — CPU only."""
 import numpy as np
 import pytest
 
-from paper_2310_08528_b200.inputs import CONFIGS, make_scene
+from paper_2310_08528_b200.inputs import CONFIGS, make_scene, morton_order
 
 
 def test_tiny_recipe():
@@ -37,3 +37,27 @@ def test_other_configs_small(name, fx):
     assert abs(s.cameras[0].fx - fx) < 0.01
     assert s.n_frames == {"hypernerf": 50, "neu3d": 8, "scaling": 64}[name]
     assert s.mlp.width == 128 and s.field.res == CONFIGS[name]["res"]
+
+
+def test_morton_order_is_a_reordering_of_the_draw():
+    a = make_scene("dnerf", n=3000, order="draw")
+    b = make_scene("dnerf", n=3000)
+    perm = morton_order(a.means, a.field.bmin, a.field.bmax)
+    assert sorted(perm.tolist()) == list(range(3000))
+    for k in ("means", "log_scales", "quats", "opacity_logits", "sh"):
+        assert np.array_equal(getattr(b, k), getattr(a, k)[perm]), k
+    # neighbours in index space are close in space (Z-order locality): mean step << random step
+    step_sorted = np.linalg.norm(np.diff(b.means.astype(np.float64), axis=0), axis=1).mean()
+    step_draw = np.linalg.norm(np.diff(a.means.astype(np.float64), axis=0), axis=1).mean()
+    assert step_sorted < 0.25 * step_draw
+
+
+def test_morton_code_order_brute_force():
+    """Z-order of a 2x2x2 grid of cell centres: code bit layout x (msb) y z per level."""
+    pts = np.array([[x, y, z] for x in (0.25, 0.75) for y in (0.25, 0.75) for z in (0.25, 0.75)])
+    rng = np.random.default_rng(0)
+    sh = rng.permutation(8)
+    perm = morton_order(pts[sh], (0, 0, 0), (1, 1, 1), bits=1)
+    got = pts[sh][perm]
+    want = sorted(pts.tolist(), key=lambda p: (p[0] > 0.5) * 4 + (p[1] > 0.5) * 2 + (p[2] > 0.5))
+    assert np.array_equal(got, np.array(want))
