@@ -462,6 +462,43 @@ HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs
 }
 }  // namespace
 
+namespace {
+constexpr int kHostChunkFrames = 4;
+// Side stream + events of fgs_frames_host (one set per process and device 0..7, created on first use).
+struct CopyStreams {
+  bool ok = false;
+  cudaError_t err = cudaSuccess;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t done = nullptr;
+  std::vector<cudaEvent_t> evs;
+  std::mutex mu;
+  std::mutex call_mu;   // one fgs_frames_host enqueue at a time per device (events are shared)
+  cudaEvent_t event(int i) {
+    std::lock_guard<std::mutex> lk(mu);
+    while ((int)evs.size() <= i) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      evs.push_back(e);
+    }
+    return evs[i];
+  }
+};
+CopyStreams& copy_streams() {
+  static CopyStreams cs[8];
+  static std::once_flag once[8];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = std::max(0, std::min(dev, 7));
+  std::call_once(once[dev], [&] {
+    CopyStreams& c = cs[dev];
+    c.err = cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking);
+    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
+    c.ok = c.err == cudaSuccess;
+  });
+  return cs[dev];
+}
+}  // namespace
+
 size_t fgs_frames_host_workspace_bytes(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
                                        int32_t n_frames, int32_t width, int32_t height, int64_t max_instances) {
   if (!g || !field || !mlp || n_frames <= 0 || width <= 0 || height <= 0 || max_instances < 1) return 0;
@@ -528,13 +565,30 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
     defs[f].opacity_logits = gd.opacity_logits; defs[f].sh = gd.sh;
     imgs[f] = (float*)(d + L.images + (size_t)f * L.per_img);
   }
-  rc = fgs_frames(&gd, &hd, &md, ts, cams, F, defs.data(), imgs.data(), d + L.render, L.per_render * (size_t)F,
-                  stream);
+  // Deform all frames in one launch (the spatial-plane work is shared across times), then render in
+  // chunks; the device->host copy of chunk c runs on a side stream while chunk c+1 renders.
+  rc = deform_impl(&gd, &hd, &md, ts, F, 0, gd.n, defs.data(), s);
   if (rc != FGS_OK) return rc;
-  for (int f = 0; f < F; ++f) {
-    e = cudaMemcpyAsync(images_host[f], imgs[f], (size_t)3 * W * H * 4, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+  CopyStreams& cs = copy_streams();
+  if (!cs.ok) return cuda_fail(cs.err, "copy stream setup");
+  std::lock_guard<std::mutex> call_lock(cs.call_mu);
+  const int chunk = std::max(1, std::min(F, kHostChunkFrames));
+  for (int f0 = 0; f0 < F; f0 += chunk) {
+    const int nf = std::min(chunk, F - f0);
+    rc = render_impl(cams + f0, defs.data() + f0, imgs.data() + f0, nf, d + L.render + (size_t)f0 * L.per_render,
+                     L.per_render * (size_t)nf, nullptr, s);
+    if (rc != FGS_OK) return rc;
+    cudaEvent_t ev = cs.event(f0 / chunk);
+    if ((e = cudaEventRecord(ev, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(cs.copy, ev, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    for (int f = f0; f < f0 + nf; ++f) {
+      e = cudaMemcpyAsync(images_host[f], imgs[f], (size_t)3 * W * H * 4, cudaMemcpyDeviceToHost, cs.copy);
+      if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+    }
   }
+  // the caller's stream covers the copies: it waits for the side stream's last copy
+  if ((e = cudaEventRecord(cs.done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
+  if ((e = cudaStreamWaitEvent(s, cs.done, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
   return FGS_OK;
 }
 

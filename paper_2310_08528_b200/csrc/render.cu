@@ -406,22 +406,22 @@ __device__ __forceinline__ int pow2_at_least(int v) {
   return p;
 }
 
-// Lists of 2..sort_cap instances: one warp per tile sorts the list in registers — bitonic network over
-// N2 = 32 R keys in the striped layout (key e = 32 r + lane in register r of lane `lane`), so that
-// partners at distance j < 32 are exchanged with shuffles and those at j >= 32 sit in the same lane —
-// and writes it back in place.  Longer lists are queued for long_sort_kernel.
+// Lists of 2..sort_cap instances: one warp per tile sorts the list in registers — a bitonic network
+// over N2 = 32 R keys in the blocked layout (key e = R lane + r in register r of lane `lane`), so that
+// partners at distance j < R are compare-exchanged inside a thread and those at j >= R are exchanged
+// with shuffles (lane ^ j/R) — and writes it back in place.  Longer lists are queued for
+// long_sort_kernel.
 template <int R>
-__device__ __forceinline__ void sort_reg_stage(unsigned long long (&v)[R], int jr, int k) {
-  // partners 32 jr apart: registers r and r | jr of the same lane; k >= 64 so the direction
-  // depends on r only
+__device__ __forceinline__ void sort_local_stage(unsigned long long (&v)[R], int j, int k, int lane) {
+  // partners j < R apart inside the thread; direction from bit k of e = R lane + r
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if ((r & jr) == 0 && (r | jr) < R) {
-      const bool up = ((32 * r) & k) == 0;
-      const unsigned long long a = v[r], c = v[r | jr];
+    if ((r & j) == 0) {
+      const bool up = ((R * lane + r) & k) == 0;
+      const unsigned long long a = v[r], c = v[r | j];
       const bool sw = (a > c) == up;
       v[r] = sw ? c : a;
-      v[r | jr] = sw ? a : c;
+      v[r | j] = sw ? a : c;
     }
   }
 }
@@ -432,38 +432,37 @@ __device__ __noinline__ void warp_sort_tile(unsigned long long* inst, int L, int
   unsigned long long v[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int e = 32 * r + lane;
+    const int e = R * lane + r;
     v[r] = e < L ? inst[e] : ~0ull;
   }
 #pragma unroll 1
   for (int k = 2; k <= N2; k <<= 1) {
 #pragma unroll 1
-    for (int j = k >> 1; j >= 32; j >>= 1) {
-      // jr is a runtime value: dispatch to a fully unrolled stage so v stays in registers
-      switch (j >> 5) {
-        case 1: sort_reg_stage<R>(v, 1, k); break;
-        case 2: sort_reg_stage<R>(v, 2, k); break;
-        case 4: sort_reg_stage<R>(v, 4, k); break;
-        case 8: sort_reg_stage<R>(v, 8, k); break;
-        default: sort_reg_stage<R>(v, 16, k); break;
-      }
-    }
-#pragma unroll 1
-    for (int j = min(k >> 1, 16); j > 0; j >>= 1) {
-      const bool lower = (lane & j) == 0;
+    for (int j = k >> 1; j >= R; j >>= 1) {
+      const int jl = j / R;                          // partner lane distance
+      const bool lower = (lane & jl) == 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
-        const bool up = (((32 * r) | lane) & k) == 0;
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], jl);
+        const bool up = ((R * lane + r) & k) == 0;
         const bool keep_min = lower == up;
         const bool lt = v[r] < o;
         v[r] = (lt == keep_min) ? v[r] : o;
       }
     }
+    // j < R: the remaining stages of this k are thread-local (j is a compile-time value per case)
+    if constexpr (R >= 2) {
+      const int jmax = min(k >> 1, R >> 1);
+      if constexpr (R >= 32) { if (jmax >= 16) sort_local_stage<R>(v, 16, k, lane); }
+      if constexpr (R >= 16) { if (jmax >= 8) sort_local_stage<R>(v, 8, k, lane); }
+      if constexpr (R >= 8) { if (jmax >= 4) sort_local_stage<R>(v, 4, k, lane); }
+      if constexpr (R >= 4) { if (jmax >= 2) sort_local_stage<R>(v, 2, k, lane); }
+      sort_local_stage<R>(v, 1, k, lane);
+    }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int e = 32 * r + lane;
+    const int e = R * lane + r;
     if (e < L) inst[e] = v[r];
   }
 }
