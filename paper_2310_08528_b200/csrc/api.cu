@@ -99,8 +99,8 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.w_r = m->w_r; p.b_r = m->b_r; p.w_s = m->w_s; p.b_s = m->b_s;
 }
 
-// FGS_DEFORM = simt | tc1 | tc2 forces a deform kernel (A/B comparison).  Default: tc2 (TMEM-resident,
-// frame-outer) when the field fits its line buffer, else tc1.
+// FGS_DEFORM = simt | tc1 | tc2 | tc3 forces a deform kernel (A/B comparison).  Default: tc3
+// (warp-specialised pipeline) when the field fits its line buffer and TMEM plan, else tc2, else tc1.
 int deform_choice() {
   static const int c = [] {
     const char* e = getenv("FGS_DEFORM");
@@ -108,6 +108,7 @@ int deform_choice() {
     if (strcmp(e, "simt") == 0) return 1;
     if (strcmp(e, "tc1") == 0) return 2;
     if (strcmp(e, "tc2") == 0) return 3;
+    if (strcmp(e, "tc3") == 0) return 4;
     return 0;
   }();
   return c;
@@ -117,7 +118,10 @@ cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
   switch (deform_choice()) {
     case 1: return launch_deform(p, s);
     case 2: return launch_deform_tc(p, s);
-    default: return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
+    case 3: return launch_deform_tc2(p, s);
+    default:
+      if (deform_tc3_supported(p)) return launch_deform_tc3(p, s);
+      return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
   }
 }
 

@@ -1,0 +1,503 @@
+// Gaussian deformation field, v3: warp-specialised tcgen05 pipeline (sm_100a).
+// PAPER.md §4.2: Eq. 7 HexPlane query, phi_d, heads and additive update
+// (P:797-802).  Same arithmetic as deform_tc2.cu; what changes is the schedule.
+//
+// One persistent CTA per SM over a contiguous range of 128-Gaussian tiles, processed in groups of G
+// tiles; per group, for every time t of the batch, every tile of the group is one "tile-frame" i.
+// Roles (416 threads):
+//   producers (warps 0-7)  group prologue: the spatial-plane product S = xy . xz . yz of every
+//                          (Gaussian, feature) of the group, parked in TENSOR MEMORY, and the knot
+//                          window each axis of the group touches; per time t: the three temporal planes
+//                          collapsed to 1-D lines at t over those windows only (smem); per tile-frame:
+//                          f_h = S . line_x(u_x) . line_y(u_y) . line_z(u_z), split hi/lo (3xTF32) and
+//                          stored to TMEM as the A operand.
+//   MMA issuer (warp 12)   one thread: 3 x K/8 tcgen05.mma.kind::tf32 (A from TMEM, W_d hi/lo from
+//                          smem) into accumulator D[i % 2]; commits to "A free" and "D[i % 2] full".
+//   epilogue (warps 8-11)  one thread per Gaussian row: D -> bias + ReLU -> the 10 head dot products ->
+//                          additive update -> global stores; releases D[i % 2].
+// Producer work on tile-frame i+1 and the epilogue of i-1 overlap the MMAs of i (mbarrier pipeline).
+// TMEM columns: D0 | D1 | A_hi | A_lo | S[0..G).  Thread (warp w, lane) touches TMEM lane quarter w % 4.
+#include <cuda_runtime.h>
+#include <limits.h>
+
+#include <algorithm>
+
+#include "fgs_internal.cuh"
+#include "tc.cuh"
+
+namespace fgs {
+
+namespace {
+
+constexpr int kM = 128;
+constexpr int kTmemCols = 512;
+constexpr int kMaxG = 16;
+constexpr int kMaxLineFloats = 3 * 192 * 32;   // 72 KB: 3 planes x (64 + 128) knots x h 32
+constexpr int kProdWarps = 8;
+constexpr int kEpiWarps = 4;
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;
+constexpr int kThreads = 32 * (kMmaWarp + 1);    // 416
+constexpr int kProdThreads = 32 * kProdWarps;
+
+__device__ __forceinline__ uint32_t core_off(int row, int k, int rows) {
+  return (uint32_t)((((k >> 2) * (rows >> 3) + (row >> 3)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
+}
+
+template <int FEAT>
+__device__ __forceinline__ float4 bilerp4(const float* __restrict__ P, int na, int nb, float ua, float ub,
+                                          int c4) {
+  const float ga = ua * (float)(na - 1);
+  const float gb = ub * (float)(nb - 1);
+  const int i0 = min((int)floorf(ga), na - 2);
+  const int j0 = min((int)floorf(gb), nb - 2);
+  const float fa = ga - (float)i0;
+  const float fb = gb - (float)j0;
+  const float4* row0 = reinterpret_cast<const float4*>(P + ((size_t)j0 * na + i0) * FEAT) + c4;
+  const float4* row1 = reinterpret_cast<const float4*>(P + ((size_t)(j0 + 1) * na + i0) * FEAT) + c4;
+  const float4 v00 = __ldg(row0), v01 = __ldg(row0 + FEAT / 4);
+  const float4 v10 = __ldg(row1), v11 = __ldg(row1 + FEAT / 4);
+  const float w00 = (1.f - fa) * (1.f - fb), w01 = fa * (1.f - fb);
+  const float w10 = (1.f - fa) * fb, w11 = fa * fb;
+  float4 r;
+  r.x = w00 * v00.x + w01 * v01.x + w10 * v10.x + w11 * v11.x;
+  r.y = w00 * v00.y + w01 * v01.y + w10 * v10.y + w11 * v11.y;
+  r.z = w00 * v00.z + w01 * v01.z + w10 * v10.z + w11 * v11.z;
+  r.w = w00 * v00.w + w01 * v01.w + w10 * v10.w + w11 * v11.w;
+  return r;
+}
+
+// Lines are stored [R][FEAT/4] float4 with the quad index XOR-swizzled by the knot index.
+template <int FEAT>
+__device__ __forceinline__ int swz(int i, int c4) {
+  return c4 ^ (i & (FEAT / 4 - 1));
+}
+
+template <int FEAT>
+__device__ __forceinline__ int knot0(float u, int R) {
+  return min((int)floorf(u * (float)(R - 1)), R - 2);
+}
+
+// linear interpolation of a line [R][FEAT] (smem) at u in [0,1], channel quad c4
+template <int FEAT>
+__device__ __forceinline__ float4 lerp_line(const float* line, int R, float u, int c4) {
+  const float g = u * (float)(R - 1);
+  const int i0 = min((int)floorf(g), R - 2);
+  const float fa = g - (float)i0;
+  const float4 a = reinterpret_cast<const float4*>(line + i0 * FEAT)[swz<FEAT>(i0, c4)];
+  const float4 b = reinterpret_cast<const float4*>(line + (i0 + 1) * FEAT)[swz<FEAT>(i0 + 1, c4)];
+  const float wa = 1.f - fa;
+  return make_float4(wa * a.x + fa * b.x, wa * a.y + fa * b.y, wa * a.z + fa * b.z, wa * a.w + fa * b.w);
+}
+
+template <int WIDTH>
+struct Tc3Smem {
+  static constexpr int B_BYTES = 64 * WIDTH * 4;
+  static constexpr int OFF_BHI = 0;
+  static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
+  static constexpr int OFF_LINE = OFF_BLO + B_BYTES;
+  static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [kMaxG][128][4]
+  static constexpr int OFF_WH = OFF_U + kMaxG * kM * 16;
+  static constexpr int OFF_BD = OFF_WH + 10 * WIDTH * 4;
+  static constexpr int OFF_BH = OFF_BD + WIDTH * 4;
+  static constexpr int OFF_WIN = OFF_BH + 16 * 4;               // int [FGS_MAX_SCALES][3][2]
+  static constexpr int OFF_BAR = OFF_WIN + FGS_MAX_SCALES * 6 * 4;
+  // barriers: 0 a_full, 1 a_free, 2-3 d_full, 4-5 d_free; then the TMEM base address
+  static constexpr int TOTAL = OFF_BAR + 6 * 8 + 16;
+};
+
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const float* v) {
+  if constexpr (N % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 16) tc::tmem_st16(taddr + i, v + i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) tc::tmem_st4(taddr + i, v + i);
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
+  if constexpr (N % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 16) tc::tmem_ld16(taddr + i, v + i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) tc::tmem_ld4(taddr + i, v + i);
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void prod_sync() {   // named barrier over the producer warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
+}
+
+template <int FEAT, int WIDTH>
+__global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_constant__ DeformBatch p) {
+  using SM = Tc3Smem<WIDTH>;
+  constexpr int FT = FEAT / 2;                 // features per (producer thread, scale)
+  constexpr int QT = FT / 4;
+  constexpr int MAXS = 64 / FEAT;              // max scales (IN <= 64)
+  constexpr int DW = WIDTH < 32 ? 32 : WIDTH;  // columns of one accumulator
+  constexpr uint32_t IDESC = tc::idesc_tf32(kM, WIDTH);
+  const int NS = p.n_scales;
+  const int IN = p.in_dim;
+  const int KP = (IN + 7) & ~7;
+  const uint32_t colA_hi = 2 * DW, colA_lo = 2 * DW + KP, colS = 2 * DW + 2 * KP;
+  const int G = min(kMaxG, (kTmemCols - (int)colS) / IN);
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* line = reinterpret_cast<float*>(smem + SM::OFF_LINE);
+  float* U = reinterpret_cast<float*>(smem + SM::OFF_U);
+  float* Wh = reinterpret_cast<float*>(smem + SM::OFF_WH);
+  float* bd = reinterpret_cast<float*>(smem + SM::OFF_BD);
+  float* bh = reinterpret_cast<float*>(smem + SM::OFF_BH);
+  int* win = reinterpret_cast<int*>(smem + SM::OFF_WIN);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
+  uint64_t* a_full = bar + 0;
+  uint64_t* a_free = bar + 1;
+  uint64_t* d_full = bar + 2;
+  uint64_t* d_free = bar + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- setup (all threads) ----
+  for (int i = tid; i < WIDTH * KP; i += kThreads) {
+    const int n = i / KP, k = i - n * KP;
+    const float w = k < IN ? p.w_d[n * IN + k] : 0.f;
+    float hi, lo;
+    tc::tf32_split(w, hi, lo);
+    const uint32_t o = core_off(n, k, WIDTH);
+    *reinterpret_cast<float*>(smem + SM::OFF_BHI + o) = hi;
+    *reinterpret_cast<float*>(smem + SM::OFF_BLO + o) = lo;
+  }
+  for (int i = tid; i < 3 * WIDTH; i += kThreads) Wh[i] = p.w_x[i];
+  for (int i = tid; i < 4 * WIDTH; i += kThreads) Wh[3 * WIDTH + i] = p.w_r[i];
+  for (int i = tid; i < 3 * WIDTH; i += kThreads) Wh[7 * WIDTH + i] = p.w_s[i];
+  for (int i = tid; i < WIDTH; i += kThreads) bd[i] = p.b_d[i];
+  if (tid < 3) bh[tid] = p.b_x[tid];
+  if (tid < 4) bh[3 + tid] = p.b_r[tid];
+  if (tid < 3) bh[7 + tid] = p.b_s[tid];
+  if (tid == 0) {
+    tc::mbar_init(a_full, kProdWarps);
+    tc::mbar_init(a_free, 1);
+    tc::mbar_init(d_full + 0, 1);
+    tc::mbar_init(d_full + 1, 1);
+    tc::mbar_init(d_free + 0, kEpiWarps);
+    tc::mbar_init(d_free + 1, kEpiWarps);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, kTmemCols);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t count = p.end - p.begin;
+  const int64_t tiles = (count + kM - 1) / kM;
+  const int64_t t_beg = tiles * blockIdx.x / gridDim.x, t_end = tiles * (blockIdx.x + 1) / gridDim.x;
+
+  if (warp < kProdWarps) {
+    // =============================================================== producers
+    const int quarter = warp & 3, part = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    int line_off[MAXS];
+    {
+      int o = 0;
+#pragma unroll
+      for (int l = 0; l < MAXS; ++l) {
+        line_off[l] = o;
+        if (l < NS) o += 3 * p.res[l] * FEAT;
+      }
+    }
+    if (part == 0) {   // zero the K padding columns of A once (never written afterwards)
+      for (int k = IN; k < KP; k += 4) {
+        const float z[4] = {0.f, 0.f, 0.f, 0.f};
+        tc::tmem_st4(lane_base + colA_hi + k, z);
+        tc::tmem_st4(lane_base + colA_lo + k, z);
+      }
+      tc::tmem_st_wait();
+    }
+    uint32_t it = 0;   // tile-frame counter
+    for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
+      const int ng = (int)min((int64_t)G, t_end - gstart);
+      // ---- group prologue: grid coordinates (smem), knot windows, spatial products S (TMEM) ----
+      prod_sync();     // previous group's line / U readers are done
+      if (tid < FGS_MAX_SCALES * 3) { win[2 * tid] = INT_MAX; win[2 * tid + 1] = INT_MIN; }
+      prod_sync();
+      for (int gt = 0; gt < ng; ++gt) {
+        const int64_t g = p.begin + (gstart + gt) * kM + row;
+        const bool valid = g < p.end;
+        float u[3] = {0.f, 0.f, 0.f};
+        if (valid) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float m = __ldg(p.means + g * 3 + a);
+            u[a] = fminf(fmaxf((m - p.bmin[a]) / p.ext[a], 0.f), 1.f);
+          }
+        }
+        if (part == 0) {
+          float* Ur = U + (gt * kM + row) * 4;
+          Ur[0] = u[0]; Ur[1] = u[1]; Ur[2] = u[2];
+          if (valid) {
+#pragma unroll
+            for (int l = 0; l < MAXS; ++l) {
+              if (l >= NS) break;
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                const int i0 = knot0<FEAT>(u[a], p.res[l]);
+                atomicMin(win + (l * 3 + a) * 2, i0);
+                atomicMax(win + (l * 3 + a) * 2 + 1, i0 + 1);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int l = 0; l < MAXS; ++l) {
+          if (l >= NS) break;
+          const int R = p.res[l];
+          float sv[FT];
+#pragma unroll
+          for (int qq = 0; qq < QT; ++qq) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) {
+              const int c4 = part * QT + qq;
+              v = bilerp4<FEAT>(p.planes[l][0], R, R, u[0], u[1], c4);
+              const float4 b = bilerp4<FEAT>(p.planes[l][1], R, R, u[0], u[2], c4);
+              const float4 c = bilerp4<FEAT>(p.planes[l][2], R, R, u[1], u[2], c4);
+              v = make_float4(v.x * b.x * c.x, v.y * b.y * c.y, v.z * b.z * c.z, v.w * b.w * c.w);
+            }
+            sv[4 * qq + 0] = v.x; sv[4 * qq + 1] = v.y; sv[4 * qq + 2] = v.z; sv[4 * qq + 3] = v.w;
+          }
+          tmem_st_n<FT>(lane_base + colS + gt * IN + l * FEAT + part * FT, sv);
+        }
+      }
+      tc::tmem_st_wait();
+      for (int f = 0; f < p.n_t; ++f) {
+        const float t = p.t[f];
+        // ---- stage the temporal lines at t over the group's knot windows (time lerp of 2 rows) ----
+        prod_sync();   // U/win visible; previous frame's line readers done
+        {
+          const int Tn = p.t_res;
+          const float gt_ = t * (float)(Tn - 1);
+          const int j0 = min((int)floorf(gt_), Tn - 2);
+          const float ft = gt_ - (float)j0, wt = 1.f - ft;
+#pragma unroll
+          for (int l = 0; l < MAXS; ++l) {
+            if (l >= NS) break;
+            const int R = p.res[l];
+            const int per_plane = R * (FEAT / 4);
+            float4* dst = reinterpret_cast<float4*>(line + line_off[l]);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+              const int lo = win[(l * 3 + pl) * 2], hi = win[(l * 3 + pl) * 2 + 1];
+              if (lo > hi) continue;
+              const float4* P0 = reinterpret_cast<const float4*>(p.planes[l][3 + pl]) + (size_t)j0 * per_plane;
+              const float4* P1 = P0 + per_plane;
+              const int n_items = (hi - lo + 1) * (FEAT / 4);
+              for (int q = tid; q < n_items; q += kProdThreads) {
+                const int rem = lo * (FEAT / 4) + q;
+                const float4 a = __ldg(P0 + rem);
+                const float4 b = __ldg(P1 + rem);
+                const int i = rem / (FEAT / 4), c4 = rem - i * (FEAT / 4);
+                dst[pl * per_plane + i * (FEAT / 4) + swz<FEAT>(i, c4)] =
+                    make_float4(wt * a.x + ft * b.x, wt * a.y + ft * b.y, wt * a.z + ft * b.z, wt * a.w + ft * b.w);
+              }
+            }
+          }
+        }
+        prod_sync();
+        for (int gt = 0; gt < ng; ++gt, ++it) {
+          const float* Ur = U + (gt * kM + row) * 4;
+          const float ux = Ur[0], uy = Ur[1], uz = Ur[2];
+          float hi[MAXS][FT], lo[MAXS][FT];
+#pragma unroll
+          for (int l = 0; l < MAXS; ++l) {
+            if (l >= NS) break;
+            const int R = p.res[l];
+            float sv[FT];
+            tmem_ld_n<FT>(lane_base + colS + gt * IN + l * FEAT + part * FT, sv);
+            const float* lx = line + line_off[l];
+            const float* ly = lx + R * FEAT;
+            const float* lz = ly + R * FEAT;
+#pragma unroll
+            for (int qq = 0; qq < QT; ++qq) {
+              const int c4 = part * QT + qq;
+              const float4 a = lerp_line<FEAT>(lx, R, ux, c4);
+              const float4 b = lerp_line<FEAT>(ly, R, uy, c4);
+              const float4 c = lerp_line<FEAT>(lz, R, uz, c4);
+              const float fh[4] = {sv[4 * qq + 0] * (a.x * b.x * c.x), sv[4 * qq + 1] * (a.y * b.y * c.y),
+                                   sv[4 * qq + 2] * (a.z * b.z * c.z), sv[4 * qq + 3] * (a.w * b.w * c.w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) tc::tf32_split(fh[e], hi[l][4 * qq + e], lo[l][4 * qq + e]);
+            }
+          }
+          // A is single-buffered: wait until the MMAs of tile-frame it-1 have read it
+          if (it > 0) tc::mbar_wait(a_free, (it - 1) & 1u);
+          tc::fence_after_sync();
+#pragma unroll
+          for (int l = 0; l < MAXS; ++l) {
+            if (l >= NS) break;
+            tmem_st_n<FT>(lane_base + colA_hi + l * FEAT + part * FT, hi[l]);
+            tmem_st_n<FT>(lane_base + colA_lo + l * FEAT + part * FT, lo[l]);
+          }
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // =============================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t b_hi = tc::smem_u32(smem + SM::OFF_BHI), b_lo = tc::smem_u32(smem + SM::OFF_BLO);
+      uint32_t it = 0;
+      for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
+        const int ng = (int)min((int64_t)G, t_end - gstart);
+        for (int f = 0; f < p.n_t; ++f) {
+          for (int gt = 0; gt < ng; ++gt, ++it) {
+            const uint32_t buf = it & 1u;
+            tc::mbar_wait(a_full, it & 1u);
+            if (it >= 2) tc::mbar_wait(d_free + buf, ((it >> 1) - 1) & 1u);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + buf * DW;
+            for (int s = 0; s < KP / 8; ++s) {
+              const uint32_t bo = (uint32_t)s * (2 * (WIDTH / 8) * 128);
+              const uint64_t dbh = tc::smem_desc(b_hi + bo, (WIDTH / 8) * 128, 128);
+              const uint64_t dbl = tc::smem_desc(b_lo + bo, (WIDTH / 8) * 128, 128);
+              tc::mma_tf32_ts(d, tmem + colA_lo + 8 * s, dbh, IDESC, s > 0 ? 1u : 0u);
+              tc::mma_tf32_ts(d, tmem + colA_hi + 8 * s, dbl, IDESC, 1u);
+              tc::mma_tf32_ts(d, tmem + colA_hi + 8 * s, dbh, IDESC, 1u);
+            }
+            tc::mma_commit(a_free);
+            tc::mma_commit(d_full + buf);
+          }
+        }
+      }
+    }
+  } else {
+    // =============================================================== epilogue
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    uint32_t it = 0;
+    for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
+      const int ng = (int)min((int64_t)G, t_end - gstart);
+      for (int f = 0; f < p.n_t; ++f) {
+        for (int gt = 0; gt < ng; ++gt, ++it) {
+          const int64_t g = p.begin + (gstart + gt) * kM + row;
+          const bool valid = g < p.end;
+          float cx[10];
+          if (valid) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cx[c] = __ldg(p.means + g * 3 + c);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cx[3 + c] = __ldg(p.quats + g * 4 + c);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cx[7 + c] = __ldg(p.log_scales + g * 3 + c);
+          }
+          const uint32_t buf = it & 1u;
+          tc::mbar_wait(d_full + buf, (it >> 1) & 1u);
+          tc::fence_after_sync();
+          float ho[10];
+#pragma unroll
+          for (int o = 0; o < 10; ++o) ho[o] = 0.f;
+#pragma unroll
+          for (int c0 = 0; c0 < WIDTH; c0 += 16) {
+            float v[16];
+            if constexpr (WIDTH % 16 == 0) {
+              tc::tmem_ld16(lane_base + buf * DW + (uint32_t)c0, v);
+            } else {
+              tmem_ld_n<WIDTH>(lane_base + buf * DW, v);
+            }
+            if (c0 + 16 >= WIDTH) {   // all of D read: hand the buffer back to the MMA issuer
+              tc::fence_before_sync();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(d_free + buf);
+            }
+#pragma unroll
+            for (int i = 0; i < 16 && c0 + i < WIDTH; ++i) {
+              const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
+#pragma unroll
+              for (int o = 0; o < 10; ++o) ho[o] = fmaf(fd, Wh[o * WIDTH + c0 + i], ho[o]);
+            }
+          }
+          if (valid) {
+#pragma unroll
+            for (int o = 0; o < 10; ++o) ho[o] = cx[o] + (ho[o] + bh[o]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p.out_means[f][g * 3 + c] = ho[c];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) p.out_quats[f][g * 4 + c] = ho[3 + c];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p.out_log_scales[f][g * 3 + c] = ho[7 + c];
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+template <int FEAT, int WIDTH>
+cudaError_t launch_tc3_t(const DeformBatch& p, cudaStream_t s) {
+  using SM = Tc3Smem<WIDTH>;
+  auto kern = deform_tc3_kernel<FEAT, WIDTH>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (p.end - p.begin + kM - 1) / kM;
+  int64_t grid = std::min<int64_t>(sms, tiles);   // 1 CTA/SM: it owns all 512 TMEM columns
+  if (grid < 1) return cudaSuccess;
+  prof_mark(FGS_STAGE_DEFORM, true, s);
+  kern<<<(unsigned)grid, kThreads, SM::TOTAL, s>>>(p);
+  note_launches(1);
+  prof_mark(FGS_STAGE_DEFORM, false, s);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// True if the v3 schedule supports this field (lines of all scales fit the smem line buffer, the
+// accumulators and A leave room for at least one tile of S in TMEM).
+bool deform_tc3_supported(const DeformBatch& p) {
+  if (!(p.feat == 8 || p.feat == 16 || p.feat == 32)) return false;
+  if (p.in_dim > 64) return false;
+  long lines = 0;
+  for (int l = 0; l < p.n_scales; ++l) lines += 3L * p.res[l] * p.feat;
+  if (lines > kMaxLineFloats) return false;
+  const int DW = p.width < 32 ? 32 : p.width, KP = (p.in_dim + 7) & ~7;
+  return kTmemCols - (2 * DW + 2 * KP) >= p.in_dim;
+}
+
+cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s) {
+  if (p.end <= p.begin || p.n_t <= 0) return cudaSuccess;
+#define FGS_DISPATCH_W(FEAT)                          \
+  switch (p.width) {                                  \
+    case 32: return launch_tc3_t<FEAT, 32>(p, s);     \
+    case 64: return launch_tc3_t<FEAT, 64>(p, s);     \
+    case 128: return launch_tc3_t<FEAT, 128>(p, s);   \
+    default: return cudaErrorInvalidValue;            \
+  }
+  switch (p.feat) {
+    case 8: FGS_DISPATCH_W(8)
+    case 16: FGS_DISPATCH_W(16)
+    case 32: FGS_DISPATCH_W(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FGS_DISPATCH_W
+}
+
+}  // namespace fgs

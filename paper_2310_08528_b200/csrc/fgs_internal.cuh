@@ -91,6 +91,8 @@ cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);      // SIMT FP
 cudaError_t launch_deform_tc(const DeformBatch& p, cudaStream_t s);   // tcgen05 3xTF32 (deform_tc.cu)
 cudaError_t launch_deform_tc2(const DeformBatch& p, cudaStream_t s);  // TMEM-resident v2 (deform_tc2.cu)
 bool deform_tc2_supported(const DeformBatch& p);
+cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s);  // warp-specialised v3 (deform_tc3.cu)
+bool deform_tc3_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
 
