@@ -33,11 +33,17 @@ constexpr int kM = 128;
 constexpr int kTmemCols = 512;
 constexpr int kMaxG = 16;
 constexpr int kMaxLineFloats = 3 * 192 * 32;   // 72 KB: 3 planes x (64 + 128) knots x h 32
-constexpr int kProdWarps = 8;
 constexpr int kEpiWarps = 4;
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;
-constexpr int kThreads = 32 * (kMmaWarp + 1);    // 416
-constexpr int kProdThreads = 32 * kProdWarps;
+// Producer warps per TMEM lane quarter (each takes FEAT / NP features of every scale).
+template <int FEAT>
+struct Roles {
+  static constexpr int NP = FEAT >= 16 ? 4 : 2;
+  static constexpr int PROD_WARPS = 4 * NP;
+  static constexpr int PROD_THREADS = 32 * PROD_WARPS;
+  static constexpr int EPI0 = PROD_WARPS;                 // first epilogue warp
+  static constexpr int MMA_WARP = PROD_WARPS + kEpiWarps;
+  static constexpr int THREADS = 32 * (MMA_WARP + 1);     // 672 (FEAT >= 16) or 416
+};
 
 __device__ __forceinline__ uint32_t core_off(int row, int k, int rows) {
   return (uint32_t)((((k >> 2) * (rows >> 3) + (row >> 3)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
@@ -129,14 +135,18 @@ __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
+template <int NTHREADS>
 __device__ __forceinline__ void prod_sync() {   // named barrier over the producer warps only
-  asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
 }
 
 template <int FEAT, int WIDTH>
-__global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_constant__ DeformBatch p) {
+__global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(const __grid_constant__ DeformBatch p) {
   using SM = Tc3Smem<WIDTH>;
-  constexpr int FT = FEAT / 2;                 // features per (producer thread, scale)
+  using RL = Roles<FEAT>;
+  constexpr int kThreads = RL::THREADS, kProdWarps = RL::PROD_WARPS, kProdThreads = RL::PROD_THREADS;
+  constexpr int kMmaWarp = RL::MMA_WARP;
+  constexpr int FT = FEAT / RL::NP;            // features per (producer thread, scale)
   constexpr int QT = FT / 4;
   constexpr int MAXS = 64 / FEAT;              // max scales (IN <= 64)
   constexpr int DW = WIDTH < 32 ? 32 : WIDTH;  // columns of one accumulator
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_co
 
   if (warp < kProdWarps) {
     // =============================================================== producers
-    const int quarter = warp & 3, part = warp >> 2;
+    const int quarter = warp & 3, part = warp >> 2;   // part: which FT-feature slice of each scale
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     int line_off[MAXS];
@@ -226,9 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_co
     for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
       const int ng = (int)min((int64_t)G, t_end - gstart);
       // ---- group prologue: grid coordinates (smem), knot windows, spatial products S (TMEM) ----
-      prod_sync();     // previous group's line / U readers are done
+      prod_sync<kProdThreads>();     // previous group's line / U readers are done
       if (tid < FGS_MAX_SCALES * 3) { win[2 * tid] = INT_MAX; win[2 * tid + 1] = INT_MIN; }
-      prod_sync();
+      prod_sync<kProdThreads>();
       for (int gt = 0; gt < ng; ++gt) {
         const int64_t g = p.begin + (gstart + gt) * kM + row;
         const bool valid = g < p.end;
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_co
       for (int f = 0; f < p.n_t; ++f) {
         const float t = p.t[f];
         // ---- stage the temporal lines at t over the group's knot windows (time lerp of 2 rows) ----
-        prod_sync();   // U/win visible; previous frame's line readers done
+        prod_sync<kProdThreads>();   // U/win visible; previous frame's line readers done
         {
           const int Tn = p.t_res;
           const float gt_ = t * (float)(Tn - 1);
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) deform_tc3_kernel(const __grid_co
             }
           }
         }
-        prod_sync();
+        prod_sync<kProdThreads>();
         for (int gt = 0; gt < ng; ++gt, ++it) {
           const float* Ur = U + (gt * kM + row) * 4;
           const float ux = Ur[0], uy = Ur[1], uz = Ur[2];
@@ -462,7 +472,7 @@ cudaError_t launch_tc3_t(const DeformBatch& p, cudaStream_t s) {
   int64_t grid = std::min<int64_t>(sms, tiles);   // 1 CTA/SM: it owns all 512 TMEM columns
   if (grid < 1) return cudaSuccess;
   prof_mark(FGS_STAGE_DEFORM, true, s);
-  kern<<<(unsigned)grid, kThreads, SM::TOTAL, s>>>(p);
+  kern<<<(unsigned)grid, Roles<FEAT>::THREADS, SM::TOTAL, s>>>(p);
   note_launches(1);
   prof_mark(FGS_STAGE_DEFORM, false, s);
   return cudaGetLastError();

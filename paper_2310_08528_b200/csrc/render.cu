@@ -427,13 +427,14 @@ __device__ __forceinline__ void sort_local_stage(unsigned long long (&v)[R], int
 }
 
 template <int R>
-__device__ __noinline__ void warp_sort_tile(unsigned long long* inst, int L, int lane) {
+__device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsigned long long* dst, int L,
+                                            int lane) {
   constexpr int N2 = 32 * R;
   unsigned long long v[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = R * lane + r;
-    v[r] = e < L ? inst[e] : ~0ull;
+    v[r] = e < L ? src[e] : ~0ull;
   }
 #pragma unroll 1
   for (int k = 2; k <= N2; k <<= 1) {
@@ -463,19 +464,67 @@ __device__ __noinline__ void warp_sort_tile(unsigned long long* inst, int L, int
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = R * lane + r;
-    if (e < L) inst[e] = v[r];
+    if (e < L) dst[e] = v[r];
   }
 }
 
+// Sorts L <= 256 keys src[0..L) -> dst[0..L) with the smallest register network that holds them.
+__device__ __forceinline__ void warp_sort_upto256(const unsigned long long* src, unsigned long long* dst, int L,
+                                                  int lane) {
+  if (L <= 32) warp_sort_tile<1>(src, dst, L, lane);
+  else if (L <= 64) warp_sort_tile<2>(src, dst, L, lane);
+  else if (L <= 128) warp_sort_tile<4>(src, dst, L, lane);
+  else warp_sort_tile<8>(src, dst, L, lane);
+}
+
+// Warp-cooperative merge of sorted runs a[0..na) and b[0..nb) (shared memory) into out[0..na+nb):
+// lane l produces a contiguous slice of the output, found by a merge-path binary search (keys are
+// unique, so the split is exact).
+__device__ __forceinline__ void warp_merge(const unsigned long long* a, int na, const unsigned long long* bq,
+                                           int nb, unsigned long long* out, int lane) {
+  const int n = na + nb;
+  const int per = (n + 31) >> 5;
+  const int d0 = min(n, lane * per), d1 = min(n, d0 + per);
+  int lo = max(0, d0 - nb), hi = min(d0, na);
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] < bq[d0 - 1 - m]) lo = m + 1; else hi = m;
+  }
+  int ia = lo, ib = d0 - lo;
+  unsigned long long va = ia < na ? a[ia] : ~0ull, vb = ib < nb ? bq[ib] : ~0ull;
+  for (int d = d0; d < d1; ++d) {
+    const bool ta = va < vb;
+    out[d] = ta ? va : vb;
+    if (ta) { ++ia; va = ia < na ? a[ia] : ~0ull; }
+    else { ++ib; vb = ib < nb ? bq[ib] : ~0ull; }
+  }
+}
+
+// Two launches split by list length so each gets its own register budget: lists of up to 256 keys
+// are sorted by one register network per warp; longer ones (up to sort_cap) as runs of 256 sorted in
+// registers, then merged pairwise by the warp (merge path) through shared memory.
 constexpr int kTileSortWarps = 4;
-__global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __grid_constant__ RenderBatch b) {
+constexpr int kMergeWarps = 2;
+__global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_small_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kTileSortWarps + warp;
   if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
-  if (L <= 1) return;
+  if (L <= 1 || L > 256 || L > b.sort_cap) return;
+  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
+  warp_sort_upto256(inst, inst, L, lane);
+}
+
+__global__ void __launch_bounds__(32 * kMergeWarps) tile_sort_merge_kernel(const __grid_constant__ RenderBatch b) {
+  const int f = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kMergeWarps + warp;
+  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
+  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
+  const int L = (int)(rg.y - rg.x);
+  if (L <= 256 && L <= b.sort_cap) return;
   if (L > b.sort_cap) {
     if (lane == 0) {
       const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
@@ -484,12 +533,21 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
     return;
   }
   unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
-  if (L <= 32) warp_sort_tile<1>(inst, L, lane);
-  else if (L <= 64) warp_sort_tile<2>(inst, L, lane);
-  else if (L <= 128) warp_sort_tile<4>(inst, L, lane);
-  else if (L <= 256) warp_sort_tile<8>(inst, L, lane);
-  else if (L <= 512) warp_sort_tile<16>(inst, L, lane);
-  else warp_sort_tile<32>(inst, L, lane);
+  __shared__ unsigned long long buf[kMergeWarps][2][kBlendSortMax];
+  unsigned long long* A = buf[warp][0];
+  unsigned long long* B = buf[warp][1];
+  for (int c0 = 0; c0 < L; c0 += 256) warp_sort_upto256(inst + c0, A + c0, min(256, L - c0), lane);
+  __syncwarp();
+  for (int w = 256; w < L; w <<= 1) {
+    const bool last = 2 * w >= L;
+    unsigned long long* out = last ? inst : B;
+    for (int s0 = 0; s0 < L; s0 += 2 * w) {
+      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
+      warp_merge(A + s0, na, A + s0 + na, nb, out + s0, lane);
+    }
+    __syncwarp();
+    unsigned long long* t = A; A = B; B = t;
+  }
 }
 
 // Lists longer than b.sort_cap: sorted in place in global memory by one CTA per tile — bitonic runs
@@ -756,10 +814,12 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   note_launches(1);
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
-  tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
+  const dim3 tsg((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F);
+  tile_sort_small_kernel<<<tsg, 32 * kTileSortWarps, 0, s>>>(b);
+  tile_sort_merge_kernel<<<dim3((b.ntiles + kMergeWarps - 1) / kMergeWarps, F), 32 * kMergeWarps, 0, s>>>(b);
   // long lists: a few persistent CTAs per frame walk the worklist (usually empty)
   long_sort_kernel<<<dim3((unsigned)std::max(1, std::min(32, num_sms_cached() / F)), F), kLargeSortThreads, 0, s>>>(b);
-  note_launches(2);
+  note_launches(3);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);
   const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;

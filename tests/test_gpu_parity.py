@@ -203,7 +203,7 @@ def test_nan_and_degenerate_gaussians_are_culled():
     assert np.all(out["radii"][:20] == 0) and np.all(out["tiles_touched"][:20] == 0)
 
 
-@pytest.mark.parametrize("cap", [1, 16, 100])
+@pytest.mark.parametrize("cap", [1, 16, 100, 300, 700])
 def test_long_list_sort_path_matches(cap):
     """Tile lists longer than the shared-memory sort cap go through long_sort_kernel (global-memory
     runs + merge-path merges): same lists, same image, bit for bit, as the in-smem bitonic path."""
