@@ -250,6 +250,17 @@ def bin_ref(pre, cam):
     return tiles, gids, ranges
 
 
+def tile_list_ref(pre, cam, tile):
+    """Step 13 for ONE tile: the kept Gaussians whose rect contains `tile`, sorted by (depth key,
+    index) — the slice bin_ref gives that tile, without building all instances (large configs)."""
+    gx, _ = tile_grid(cam.width, cam.height)
+    ty, tx = divmod(int(tile), gx)
+    r = pre["rect"]
+    hit = pre["kept"] & (r[:, 0] <= tx) & (tx < r[:, 2]) & (r[:, 1] <= ty) & (ty < r[:, 3])
+    idx = np.nonzero(hit)[0]
+    return idx[np.lexsort((idx, pre["depth_key"][idx].astype(np.int64)))]
+
+
 # ---------------------------------------------------------------- step 14
 def composite(pre, order, px, py, bg, flags=None):
     """Front-to-back alpha blending (Eq. 4) of Gaussians `order` at pixels (px, py).
@@ -302,7 +313,7 @@ def _tile_pixels(tile, gx, W, H):
     return px.ravel(), py.ravel()
 
 
-def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, pre=None):
+def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, pre=None, full_bins=True):
     """I = S(M, G'): preprocess, bin/sort, per-tile blend (tiled oracle).
 
     deformed: dict with means, log_scales, quats (raw, as written by deform).
@@ -310,23 +321,37 @@ def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, 
     Returns dict: image [3,H,W], final_T [H,W], n_contrib [H,W], flagged [H,W]
     (decision within relative 1e-4 of a threshold, or tile touched by a
     boundary Gaussian), plus the preprocess dict and (tiles, gids, ranges).
+    full_bins=False (with tiles_subset): per-tile lists from tile_list_ref only, for configs where
+    building every instance is too slow; (tiles, gids, ranges) are then None.
     """
     W, H = cam.width, cam.height
     gx, gy = tile_grid(W, H)
     if pre is None:
         pre = preprocess_ref(deformed["means"], deformed["log_scales"], deformed["quats"],
                              opacity_logits, sh, sh_degree, cam)
-    tiles, gids, ranges = bin_ref(pre, cam)
+    if full_bins or tiles_subset is None:
+        tiles, gids, ranges = bin_ref(pre, cam)
+    else:
+        tiles = gids = ranges = None
     img = np.full((3, H, W), np.nan)
     fT = np.full((H, W), np.nan)
     ncon = np.full((H, W), -1, np.int64)
     flag = np.zeros((H, W), bool)
-    bnd_tiles = set(tiles[pre["boundary"][gids]].tolist()) if gids.size else set()
+    if gids is not None:
+        bnd_tiles = set(tiles[pre["boundary"][gids]].tolist()) if gids.size else set()
     todo = range(gx * gy) if tiles_subset is None else tiles_subset
     for tile in todo:
         px, py = _tile_pixels(tile, gx, W, H)
-        s, e = ranges[tile]
-        rgb, T, nc, fl = composite(pre, gids[s:e], px.astype(np.float64), py.astype(np.float64), cam.bg)
+        if gids is not None:
+            s, e = ranges[tile]
+            lst = gids[s:e]
+        else:
+            lst = tile_list_ref(pre, cam, tile)
+            if pre["boundary"][lst].any():
+                bnd_tiles = {tile}
+            else:
+                bnd_tiles = set()
+        rgb, T, nc, fl = composite(pre, lst, px.astype(np.float64), py.astype(np.float64), cam.bg)
         img[:, py, px] = rgb.T
         fT[py, px] = T
         ncon[py, px] = nc

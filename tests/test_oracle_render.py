@@ -311,3 +311,23 @@ def test_binning_lists_are_valid(tiny_scene):
         keys = pre["depth_key"][lst].astype(np.int64)
         pairs = list(zip(keys.tolist(), lst.tolist()))
         assert pairs == sorted(pairs)
+
+
+def test_tile_list_ref_equals_bin_ref_slices(tiny_scene):
+    """The single-tile list builder (used for sampled tiles at large configs) gives exactly the
+    slice of the full instance sort, and the subset render equals the full render on those tiles."""
+    s = make_scene("tiny", width=70, height=50)
+    d = oracle.deform_ref(s, s.times[0])
+    cam = s.cameras[0]
+    pre = R.preprocess_ref(d["means"], d["log_scales"], d["quats"], s.opacity_logits, s.sh, 0, cam)
+    tiles, gids, ranges = R.bin_ref(pre, cam)
+    gx, gy = R.tile_grid(cam.width, cam.height)
+    for tile in range(gx * gy):
+        st, en = ranges[tile]
+        assert np.array_equal(R.tile_list_ref(pre, cam, tile), gids[st:en])
+    sub = [0, 5, gx * gy - 1]
+    a = R.render_ref(d, s.opacity_logits, s.sh, 0, cam, tiles_subset=sub, pre=pre)
+    b = R.render_ref(d, s.opacity_logits, s.sh, 0, cam, tiles_subset=sub, pre=pre, full_bins=False)
+    m = np.isfinite(a["image"][0])
+    assert m.sum() > 0 and np.array_equal(a["image"][:, m], b["image"][:, m])
+    assert np.array_equal(a["flagged"], b["flagged"])
