@@ -411,19 +411,12 @@ __device__ __forceinline__ int pow2_at_least(int v) {
 // partners at distance j < R are compare-exchanged inside a thread and those at j >= R are exchanged
 // with shuffles (lane ^ j/R) — and writes it back in place.  Longer lists are queued for
 // long_sort_kernel.
-template <int R>
-__device__ __forceinline__ void sort_local_stage(unsigned long long (&v)[R], int j, int k, int lane) {
-  // partners j < R apart inside the thread; direction from bit k of e = R lane + r
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if ((r & j) == 0) {
-      const bool up = ((R * lane + r) & k) == 0;
-      const unsigned long long a = v[r], c = v[r | j];
-      const bool sw = (a > c) == up;
-      v[r] = sw ? c : a;
-      v[r | j] = sw ? a : c;
-    }
-  }
+// Compare-exchange of two 64-bit keys: (a, c) <- (min, max) if up else (max, min).
+__device__ __forceinline__ void cmp_swap(unsigned long long& a, unsigned long long& c, bool up) {
+  const bool sw = (a > c) == up;
+  const unsigned long long lo = sw ? c : a, hi = sw ? a : c;
+  a = lo;
+  c = hi;
 }
 
 template <int R>
@@ -436,29 +429,40 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
     const int e = R * lane + r;
     v[r] = e < L ? src[e] : ~0ull;
   }
+  // k < R: every stage is thread-local and every direction a compile-time function of r
+#pragma unroll
+  for (int k = 2; k < R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & j) == 0) cmp_swap(v[r], v[r | j], (r & k) == 0);
+    }
+  }
+  // k >= R: bit k of e = R lane + r comes from the lane, so the direction is one value per lane
 #pragma unroll 1
-  for (int k = 2; k <= N2; k <<= 1) {
+  for (int k = R; k <= N2; k <<= 1) {
+    if (k < 2) continue;
+    const bool up = ((R * lane) & k) == 0;
 #pragma unroll 1
     for (int j = k >> 1; j >= R; j >>= 1) {
       const int jl = j / R;                          // partner lane distance
-      const bool lower = (lane & jl) == 0;
+      const bool keep_min = ((lane & jl) == 0) == up;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], jl);
-        const bool up = ((R * lane + r) & k) == 0;
-        const bool keep_min = lower == up;
         const bool lt = v[r] < o;
         v[r] = (lt == keep_min) ? v[r] : o;
       }
     }
-    // j < R: the remaining stages of this k are thread-local (j is a compile-time value per case)
-    if constexpr (R >= 2) {
-      const int jmax = min(k >> 1, R >> 1);
-      if constexpr (R >= 32) { if (jmax >= 16) sort_local_stage<R>(v, 16, k, lane); }
-      if constexpr (R >= 16) { if (jmax >= 8) sort_local_stage<R>(v, 8, k, lane); }
-      if constexpr (R >= 8) { if (jmax >= 4) sort_local_stage<R>(v, 4, k, lane); }
-      if constexpr (R >= 4) { if (jmax >= 2) sort_local_stage<R>(v, 2, k, lane); }
-      sort_local_stage<R>(v, 1, k, lane);
+    // j < R: the remaining stages of this k are thread-local (compile-time j)
+#pragma unroll
+    for (int j = R >> 1; j > 0; j >>= 1) {
+      if (j < k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if ((r & j) == 0) cmp_swap(v[r], v[r | j], up);
+      }
     }
   }
 #pragma unroll
@@ -512,19 +516,7 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_small_kernel(co
   if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
-  if (L <= 1 || L > 256 || L > b.sort_cap) return;
-  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
-  warp_sort_upto256(inst, inst, L, lane);
-}
-
-__global__ void __launch_bounds__(32 * kMergeWarps) tile_sort_merge_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kMergeWarps + warp;
-  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
-  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
-  const int L = (int)(rg.y - rg.x);
-  if (L <= 256 && L <= b.sort_cap) return;
+  if (L <= 1 || L > 256) return;
   if (L > b.sort_cap) {
     if (lane == 0) {
       const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
@@ -533,9 +525,35 @@ __global__ void __launch_bounds__(32 * kMergeWarps) tile_sort_merge_kernel(const
     return;
   }
   unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
-  __shared__ unsigned long long buf[kMergeWarps][2][kBlendSortMax];
+  warp_sort_upto256(inst, inst, L, lane);
+}
+
+// MAXL = 512: lists of 257..512 keys, two runs merged straight from one shared buffer to global memory;
+// MAXL = 1024: lists of 513..sort_cap keys (up to four runs, two merge levels, ping-pong buffers).
+template <int MAXL>
+__global__ void __launch_bounds__(32 * (MAXL == 512 ? 4 : kMergeWarps))
+tile_sort_merge_kernel(const __grid_constant__ RenderBatch b) {
+  constexpr int NW = MAXL == 512 ? 4 : kMergeWarps;
+  constexpr int NBUF = MAXL == 512 ? 1 : 2;
+  const int f = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * NW + warp;
+  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
+  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
+  const int L = (int)(rg.y - rg.x);
+  if (L <= MAXL / 2 || (MAXL == 512 && L > 512)) return;
+  if (L > b.sort_cap) {
+    // each over-cap length is queued by exactly one launch (small: <= 256, 512: 257..512, 1024: > 512)
+    if (lane == 0) {
+      const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
+      ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list)[w] = (uint32_t)tile;
+    }
+    return;
+  }
+  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
+  __shared__ unsigned long long buf[NW][NBUF][MAXL];
   unsigned long long* A = buf[warp][0];
-  unsigned long long* B = buf[warp][1];
+  unsigned long long* B = buf[warp][NBUF - 1];
   for (int c0 = 0; c0 < L; c0 += 256) warp_sort_upto256(inst + c0, A + c0, min(256, L - c0), lane);
   __syncwarp();
   for (int w = 256; w < L; w <<= 1) {
@@ -816,10 +834,11 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
   const dim3 tsg((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F);
   tile_sort_small_kernel<<<tsg, 32 * kTileSortWarps, 0, s>>>(b);
-  tile_sort_merge_kernel<<<dim3((b.ntiles + kMergeWarps - 1) / kMergeWarps, F), 32 * kMergeWarps, 0, s>>>(b);
+  tile_sort_merge_kernel<512><<<dim3((b.ntiles + 3) / 4, F), 128, 0, s>>>(b);
+  tile_sort_merge_kernel<1024><<<dim3((b.ntiles + kMergeWarps - 1) / kMergeWarps, F), 32 * kMergeWarps, 0, s>>>(b);
   // long lists: a few persistent CTAs per frame walk the worklist (usually empty)
   long_sort_kernel<<<dim3((unsigned)std::max(1, std::min(32, num_sms_cached() / F)), F), kLargeSortThreads, 0, s>>>(b);
-  note_launches(3);
+  note_launches(4);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);
   const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;
