@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   const double s0 = exp((double)ls[0]), s1 = exp((double)ls[1]), s2 = exp((double)ls[2]);
   const float4 qv = *reinterpret_cast<const float4*>(b.quats[f] + 4 * i);
   double qw = qv.x, qx = qv.y, qy = qv.z, qz = qv.w;
-  const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-  qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+  const double qinv = 1.0 / sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  qw *= qinv; qx *= qinv; qy *= qinv; qz *= qinv;
   const double r00 = 1 - 2 * (qy * qy + qz * qz), r01 = 2 * (qx * qy - qw * qz), r02 = 2 * (qx * qz + qw * qy);
   const double r10 = 2 * (qx * qy + qw * qz), r11 = 1 - 2 * (qx * qx + qz * qz), r12 = 2 * (qy * qz - qw * qx);
   const double r20 = 2 * (qx * qz - qw * qy), r21 = 2 * (qy * qz + qw * qx), r22 = 1 - 2 * (qx * qx + qy * qy);
@@ -174,13 +174,15 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   const double S12 = m10 * m20 + m11 * m21 + m12 * m22;
   const double S22 = m20 * m20 + m21 * m21 + m22 * m22;
   // ---- steps 4-6: J (x/z, y/z clamped, R4), Sigma2 = J W Sigma W^T J^T + 0.3 I (Eq. 3) ----
+  // (one fp64 reciprocal of z; a reordering at the 1e-16 level, far inside the 1e-5 px decision band)
   const double fx = c.fx, fy = c.fy;
+  const double iz = 1.0 / pz;
   const double limx = kFovClamp * ((double)b.width / (2.0 * fx));
   const double limy = kFovClamp * ((double)b.height / (2.0 * fy));
-  const double xt = fmin(limx, fmax(-limx, px / pz)) * pz;
-  const double yt = fmin(limy, fmax(-limy, py / pz)) * pz;
-  const double j00 = fx / pz, j02 = -fx * xt / (pz * pz);
-  const double j11 = fy / pz, j12 = -fy * yt / (pz * pz);
+  const double xt = fmin(limx, fmax(-limx, px * iz)) * pz;
+  const double yt = fmin(limy, fmax(-limy, py * iz)) * pz;
+  const double j00 = fx * iz, j02 = -fx * xt * (iz * iz);
+  const double j11 = fy * iz, j12 = -fy * yt * (iz * iz);
   const double W00 = c.R[0], W01 = c.R[1], W02 = c.R[2];
   const double W10 = c.R[3], W11 = c.R[4], W12 = c.R[5];
   const double W20 = c.R[6], W21 = c.R[7], W22 = c.R[8];
@@ -204,8 +206,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   const double lam1 = mid + disc;
   const double rad = ceil(3.0 * sqrt(lam1));
   // ---- step 9: mean2d ----
-  const double mx = fx * px / pz + (double)c.cx;
-  const double my = fy * py / pz + (double)c.cy;
+  const double mx = fx * px * iz + (double)c.cx;
+  const double my = fy * py * iz + (double)c.cy;
   // ---- step 10: tile rect ([3dgs] truncating rule, R8) ----
   int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
   if (keep) {
@@ -249,30 +251,30 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
   rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
   radii[i] = (int32_t)rad;
   // ---- step 12: SH colour at d = normalize(X - campos), campos = -R^T t (R10, R11) ----
-  const double cxw = -((double)c.R[0] * c.t[0] + (double)c.R[3] * c.t[1] + (double)c.R[6] * c.t[2]);
-  const double cyw = -((double)c.R[1] * c.t[0] + (double)c.R[4] * c.t[1] + (double)c.R[7] * c.t[2]);
-  const double czw = -((double)c.R[2] * c.t[0] + (double)c.R[5] * c.t[1] + (double)c.R[8] * c.t[2]);
-  const double dx = x - cxw, dy = y - cyw, dz = z - czw;
-  const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+  // (colour is not a decision: fp32 direction)
+  const float cxw = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
+  const float cyw = -(c.R[1] * c.t[0] + c.R[4] * c.t[1] + c.R[7] * c.t[2]);
+  const float czw = -(c.R[2] * c.t[0] + c.R[5] * c.t[1] + c.R[8] * c.t[2]);
+  const float dx = (float)x - cxw, dy = (float)y - cyw, dz = (float)z - czw;
+  const float dn = rsqrtf(dx * dx + dy * dy + dz * dz);
   float col[3];
-  sh_colour<DEG>(b.sh[f] + (size_t)i * (DEG + 1) * (DEG + 1) * 3, (float)(dx / dn), (float)(dy / dn),
-                 (float)(dz / dn), col);
+  sh_colour<DEG>(b.sh[f] + (size_t)i * (DEG + 1) * (DEG + 1) * 3, dx * dn, dy * dn, dz * dn, col);
   // ---- blend record: mean2d as hi/lo fp32 pairs, conic pre-scaled to the log2 domain ----
   //   p2 = a2 dx^2 + b2 dx dy + c2 dy^2 = power * log2(e);  alpha = min(0.99, 2^(p2 + log2 o))
   const float mxh = (float)mx, myh = (float)my;
   const float mxl = (float)(mx - (double)mxh), myl = (float)(my - (double)myh);
-  const double opac = 1.0 / (1.0 + exp(-(double)b.opacity[f][i]));
+  const float opac = 1.f / (1.f + __expf(-b.opacity[f][i]));
+  const double idet = kLog2e / det;
   // Ellipse cull threshold (blend): q2 = -p2 >= 0; alpha >= 1/255 needs q2 <= log2(255 o).  The
   // margin covers the fp32 evaluation of q2 in the blend and in the cull test, whose relative
   // error grows with the conic's condition number kappa = lambda_max / lambda_min of Sigma2.
-  const double lam_min = fmax(mid - sqrt(fmax(0.0, mid * mid - det)), 1e-30);
-  const double lam_max = mid + sqrt(fmax(0.0, mid * mid - det));
-  const double thr2 = log2(255.0 * opac);
-  const double thr_keep = thr2 + (fabs(thr2) + 1.0) * (2e-3 + 4e-6 * (lam_max / lam_min));
-  rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * kLog2e * cc / det), (float)(kLog2e * bb / det));
-  rec[3 * i + 1] = make_float4((float)(-0.5 * kLog2e * a / det), (float)log2(opac), fmaxf(col[0], 0.f),
-                               fmaxf(col[1], 0.f));
-  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, (float)thr_keep);
+  const float root = (float)sqrt(fmax(0.0, mid * mid - det));
+  const float lam_max = (float)mid + root, lam_min = fmaxf((float)mid - root, 1e-30f);
+  const float thr2 = __log2f(255.f * opac);
+  const float thr_keep = thr2 + (fabsf(thr2) + 1.f) * (2e-3f + 4e-6f * (lam_max / lam_min));
+  rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * cc * idet), (float)(bb * idet));
+  rec[3 * i + 1] = make_float4((float)(-0.5 * a * idet), __log2f(opac), fmaxf(col[0], 0.f), fmaxf(col[1], 0.f));
+  rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, thr_keep);
 }
 
 // ------------------------------------------------------------------------------ tile scan (a7)
