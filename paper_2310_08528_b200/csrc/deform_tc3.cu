@@ -103,7 +103,7 @@ struct Tc3Smem {
   static constexpr int OFF_LINE = OFF_BLO + B_BYTES;
   static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [kMaxG][128][4]
   static constexpr int OFF_WH = OFF_U + kMaxG * kM * 16;
-  static constexpr int OFF_BD = OFF_WH + 10 * WIDTH * 4;
+  static constexpr int OFF_BD = OFF_WH + 12 * WIDTH * 4;   // head weights transposed [W][12]
   static constexpr int OFF_BH = OFF_BD + WIDTH * 4;
   static constexpr int OFF_WIN = OFF_BH + 16 * 4;               // int [FGS_MAX_SCALES][3][2]
   static constexpr int OFF_BAR = OFF_WIN + FGS_MAX_SCALES * 6 * 4;
@@ -130,6 +130,17 @@ __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < N; i += 4) tc::tmem_ld4(taddr + i, v + i);
   }
+}
+
+// Packed fp32x2 FMA (sm_100: FFMA2, two lanes of fp32 per instruction).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -183,9 +194,11 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     *reinterpret_cast<float*>(smem + SM::OFF_BHI + o) = hi;
     *reinterpret_cast<float*>(smem + SM::OFF_BLO + o) = lo;
   }
-  for (int i = tid; i < 3 * WIDTH; i += kThreads) Wh[i] = p.w_x[i];
-  for (int i = tid; i < 4 * WIDTH; i += kThreads) Wh[3 * WIDTH + i] = p.w_r[i];
-  for (int i = tid; i < 3 * WIDTH; i += kThreads) Wh[7 * WIDTH + i] = p.w_s[i];
+  for (int i = tid; i < 12 * WIDTH; i += kThreads) {
+    const int c = i / 12, o = i - 12 * c;          // WhT[c][o] = head output o, hidden column c
+    Wh[i] = o < 3 ? p.w_x[o * WIDTH + c] : o < 7 ? p.w_r[(o - 3) * WIDTH + c]
+          : o < 10 ? p.w_s[(o - 7) * WIDTH + c] : 0.f;
+  }
   for (int i = tid; i < WIDTH; i += kThreads) bd[i] = p.b_d[i];
   if (tid < 3) bh[tid] = p.b_x[tid];
   if (tid < 4) bh[3 + tid] = p.b_r[tid];
@@ -414,29 +427,34 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           const uint32_t buf = it & 1u;
           tc::mbar_wait(d_full + buf, (it >> 1) & 1u);
           tc::fence_after_sync();
-          float ho[10];
+          float2 acc[5];
 #pragma unroll
-          for (int o = 0; o < 10; ++o) ho[o] = 0.f;
+          for (int o = 0; o < 5; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
           for (int c0 = 0; c0 < WIDTH; c0 += 16) {
             float v[16];
-            if constexpr (WIDTH % 16 == 0) {
-              tc::tmem_ld16(lane_base + buf * DW + (uint32_t)c0, v);
-            } else {
-              tmem_ld_n<WIDTH>(lane_base + buf * DW, v);
-            }
+            tc::tmem_ld16(lane_base + buf * DW + (uint32_t)c0, v);
             if (c0 + 16 >= WIDTH) {   // all of D read: hand the buffer back to the MMA issuer
               tc::fence_before_sync();
               __syncwarp();
               if (lane == 0) mbar_arrive(d_free + buf);
             }
 #pragma unroll
-            for (int i = 0; i < 16 && c0 + i < WIDTH; ++i) {
+            for (int i = 0; i < 16; ++i) {
               const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
-#pragma unroll
-              for (int o = 0; o < 10; ++o) ho[o] = fmaf(fd, Wh[o * WIDTH + c0 + i], ho[o]);
+              const float4* w4 = reinterpret_cast<const float4*>(Wh + (c0 + i) * 12);
+              const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+              const float2 fd2 = make_float2(fd, fd);
+              acc[0] = ffma2(fd2, make_float2(wa.x, wa.y), acc[0]);
+              acc[1] = ffma2(fd2, make_float2(wa.z, wa.w), acc[1]);
+              acc[2] = ffma2(fd2, make_float2(wb.x, wb.y), acc[2]);
+              acc[3] = ffma2(fd2, make_float2(wb.z, wb.w), acc[3]);
+              acc[4] = ffma2(fd2, make_float2(wc.x, wc.y), acc[4]);
             }
           }
+          float ho[10];
+#pragma unroll
+          for (int o = 0; o < 5; ++o) { ho[2 * o] = acc[o].x; ho[2 * o + 1] = acc[o].y; }
           if (valid) {
 #pragma unroll
             for (int o = 0; o < 10; ++o) ho[o] = cx[o] + (ho[o] + bh[o]);
