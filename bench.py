@@ -184,6 +184,27 @@ def run_reference(args, scene, rank):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+STAGE_KERNELS = {"deform": ["deform_tc3_kernel", "deform_tc2_kernel", "deform_tc_kernel"],
+                 "preprocess": ["preprocess_kernel"], "blend": ["blend_kernel"],
+                 "binning": ["tile_scan_kernel", "duplicate_kernel", "tile_sort_kernel",
+                             "long_sort_kernel"]}
+
+
+def ncu_traffic(scene, stage):
+    """DRAM bytes per launch of a stage's kernel(s) from the committed ncu capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), if it was taken on this workload."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    if d.get("config") != scene.name or d.get("frames_per_launch") != scene.n_frames:
+        return None
+    ks = [d["kernels"][k]["dram_bytes_per_launch"] for k in STAGE_KERNELS.get(stage, []) if k in d["kernels"]]
+    if not ks:
+        return None
+    return sum(ks) if stage == "binning" else ks[0]
+
+
 def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
     """Algorithmic work per launch / measured launch time for each stage."""
     F = scene.n_frames
@@ -233,6 +254,11 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
         out["binning"] = {"bound": "hbm", "achieved": by / (t_sort / 1e3 / steps) / 1e9, "peak": hbm,
                           "unit": "GB/s", "frac": by / (t_sort / 1e3 / steps) / 1e9 / hbm, "traffic": None,
                           "algorithmic": "16 B per instance + 16 B per Gaussian (lower bound)"}
+    for k, v in out.items():
+        tr = ncu_traffic(scene, k)
+        if tr is not None:
+            v["traffic"] = tr
+            v["traffic_unit"] = "DRAM bytes per launch (ncu --set full, profiles/ncu_traffic.json)"
     return out
 
 

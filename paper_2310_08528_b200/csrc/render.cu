@@ -506,19 +506,20 @@ __device__ __forceinline__ void warp_merge(const unsigned long long* a, int na, 
   }
 }
 
-// Two launches split by list length so each gets its own register budget: lists of up to 256 keys
-// are sorted by one register network per warp; longer ones (up to sort_cap) as runs of 256 sorted in
-// registers, then merged pairwise by the warp (merge path) through shared memory.
+// One warp per tile.  Lists of up to 256 keys are sorted by one register network; longer ones (up to
+// sort_cap <= 1024) as runs of 256 sorted in registers into the warp's shared buffer and merged
+// pairwise by merge path — 2 runs: straight to the list in global memory; 3-4 runs: the first level
+// writes the two 512-runs to the list itself, which is copied back (coalesced) for the last level.
+// Longer lists are queued for long_sort_kernel.
 constexpr int kTileSortWarps = 4;
-constexpr int kMergeWarps = 2;
-__global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_small_kernel(const __grid_constant__ RenderBatch b) {
+__global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kTileSortWarps + warp;
   if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
-  if (L <= 1 || L > 256) return;
+  if (L <= 1) return;
   if (L > b.sort_cap) {
     if (lane == 0) {
       const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
@@ -527,46 +528,25 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_small_kernel(co
     return;
   }
   unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
-  warp_sort_upto256(inst, inst, L, lane);
-}
-
-// MAXL = 512: lists of 257..512 keys, two runs merged straight from one shared buffer to global memory;
-// MAXL = 1024: lists of 513..sort_cap keys (up to four runs, two merge levels, ping-pong buffers).
-template <int MAXL>
-__global__ void __launch_bounds__(32 * (MAXL == 512 ? 4 : kMergeWarps))
-tile_sort_merge_kernel(const __grid_constant__ RenderBatch b) {
-  constexpr int NW = MAXL == 512 ? 4 : kMergeWarps;
-  constexpr int NBUF = MAXL == 512 ? 1 : 2;
-  const int f = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * NW + warp;
-  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
-  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
-  const int L = (int)(rg.y - rg.x);
-  if (L <= MAXL / 2 || (MAXL == 512 && L > 512)) return;
-  if (L > b.sort_cap) {
-    // each over-cap length is queued by exactly one launch (small: <= 256, 512: 257..512, 1024: > 512)
-    if (lane == 0) {
-      const uint32_t w = atomicAdd(cnt_ptr(b, f) + 4, 1u);
-      ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list)[w] = (uint32_t)tile;
-    }
+  if (L <= 256) {
+    warp_sort_upto256(inst, inst, L, lane);
     return;
   }
-  unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
-  __shared__ unsigned long long buf[NW][NBUF][MAXL];
-  unsigned long long* A = buf[warp][0];
-  unsigned long long* B = buf[warp][NBUF - 1];
+  __shared__ unsigned long long buf[kTileSortWarps][kBlendSortMax];
+  unsigned long long* A = buf[warp];
   for (int c0 = 0; c0 < L; c0 += 256) warp_sort_upto256(inst + c0, A + c0, min(256, L - c0), lane);
   __syncwarp();
-  for (int w = 256; w < L; w <<= 1) {
-    const bool last = 2 * w >= L;
-    unsigned long long* out = last ? inst : B;
-    for (int s0 = 0; s0 < L; s0 += 2 * w) {
-      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
-      warp_merge(A + s0, na, A + s0 + na, nb, out + s0, lane);
-    }
+  if (L > 512) {
+    // level 1: runs (0,1) and (2,3) -> two sorted 512-runs in the list's own storage
+    warp_merge(A, 256, A + 256, 256, inst, lane);
+    warp_merge(A + 512, min(256, L - 512), A + 768, max(0, L - 768), inst + 512, lane);
     __syncwarp();
-    unsigned long long* t = A; A = B; B = t;
+    __threadfence_block();
+    for (int q = lane; q < L; q += 32) A[q] = inst[q];
+    __syncwarp();
+    warp_merge(A, 512, A + 512, L - 512, inst, lane);
+  } else {
+    warp_merge(A, 256, A + 256, L - 256, inst, lane);
   }
 }
 
@@ -834,13 +814,10 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   note_launches(1);
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
-  const dim3 tsg((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F);
-  tile_sort_small_kernel<<<tsg, 32 * kTileSortWarps, 0, s>>>(b);
-  tile_sort_merge_kernel<512><<<dim3((b.ntiles + 3) / 4, F), 128, 0, s>>>(b);
-  tile_sort_merge_kernel<1024><<<dim3((b.ntiles + kMergeWarps - 1) / kMergeWarps, F), 32 * kMergeWarps, 0, s>>>(b);
+  tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
   // long lists: a few persistent CTAs per frame walk the worklist (usually empty)
   long_sort_kernel<<<dim3((unsigned)std::max(1, std::min(32, num_sms_cached() / F)), F), kLargeSortThreads, 0, s>>>(b);
-  note_launches(4);
+  note_launches(2);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);
   const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;
