@@ -427,6 +427,90 @@ def run_fgs(args, scene, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_shard(args, scene, rank, world, local_rank):
+    """(e2) SURVEY §8(e2): the batch is (time k, view v) frames; views are split across ranks, every rank
+    deforms 1/world of the Gaussians at each distinct time and all-gathers X', r', s' (NCCL), overlapped
+    with the render of the previous time.  value = all frames of the batch / max-over-ranks time
+    ("scaling": "strong": the batch is fixed as N grows)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_08528_b200 import build, fgs
+    from paper_2310_08528_b200.sharding import ShardedDeform, sharded_frames
+
+    build.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ds = fgs.DeviceScene(scene, dev)
+    ts_all = [float(t) for t in scene.times]
+    uniq = sorted(set(ts_all), key=ts_all.index)
+    frames_of = {t: [f for f in range(scene.n_frames) if ts_all[f] == t] for t in uniq}
+    # views split across ranks: rank r renders the frames whose index within their time is in its slice
+    from paper_2310_08528_b200.sharding import frame_split
+    views = []
+    mine = []
+    for t in uniq:
+        fs = frames_of[t]
+        sel = [fs[i] for i in frame_split(len(fs), rank, world)]
+        views.append([(ds.cams[f], j) for j, f in enumerate(sel, start=len(mine))])
+        mine.extend(sel)
+    W, H = scene.cameras[0].width, scene.cameras[0].height
+    images = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in mine]
+    per_t = max(len(v) for v in views)
+    ws = ds.alloc_workspace(max(per_t, 1), 16 * scene.n)
+    sd = ShardedDeform(scene.n, world, rank, dev, n_slots=2)
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        sharded_frames(ds, sd, uniq, views, images, ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = fgs.fgs_launch_count()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    launches = fgs.fgs_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    if rank != 0:
+        return
+    F = scene.n_frames
+    line = {
+        "metric": METRIC, "value": F * args.steps / (t_max / 1e3), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_desc(scene), "frames_per_step": F, "distinct_times": len(uniq),
+                   "parallelism": f"views split x{world}; deformation sharded by Gaussian + all_gather (e2)",
+                   "l2": "flushed between steps (512 MiB write outside the events)"},
+        "gaussians_deformed_per_s": scene.n * len(uniq) * args.steps / (t_max / 1e3),
+        "gpu_launches": launches, "clocks": clk, "mode": "shard",
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -437,6 +521,9 @@ def main():
     ap.add_argument("--frames", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="frames", choices=["frames", "shard"],
+                    help="frames: every rank renders its own frame batch (e1); shard: multi-view batch, views "
+                         "split across ranks, deformation sharded by Gaussian + NCCL all-gather (e2)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "fgs":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
@@ -457,7 +544,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_fgs(args, scene, rank, world, local_rank)
+        if args.mode == "shard":
+            run_shard(args, scene, rank, world, local_rank)
+        else:
+            run_fgs(args, scene, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -158,7 +158,9 @@ int fgs_render_status(const void* ws, size_t ws_bytes, int32_t n_frames, fgs_str
 
 /* ---- whole frames (deform + render), the step bench.py times --------------------------------
  * Frame f deforms G at ts[f] into defs_scratch[f] (device buffers owned by the caller) and renders
- * it with cams[f] into images[f].  Device pointers everywhere except the host arrays. */
+ * it with cams[f] into images[f].  Device pointers everywhere except the host arrays.  Frames whose
+ * ts are bitwise equal (several views of one instant) share one deformation: only the first such
+ * frame's defs_scratch is written and all of them render from it. */
 int fgs_frames(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
                const float* ts, const fgs_camera* cams, int32_t n_frames, fgs_deformed* defs_scratch,
                float* const* images, void* ws, size_t ws_bytes, fgs_stream_t stream);

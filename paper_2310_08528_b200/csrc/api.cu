@@ -375,13 +375,42 @@ int fgs_render_status(const void* ws, size_t ws_bytes, int32_t n_frames, fgs_str
   return FGS_OK;
 }
 
+namespace fgs {
+namespace {
+// Deform the distinct times of a frame batch once each (frames sharing a time — several views of one
+// instant — share its G'); fills `render_defs` with the deformed set each frame renders.
+int frames_deform(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int F,
+                  fgs_deformed* defs, cudaStream_t s, std::vector<fgs_deformed>& render_defs) {
+  FGS_CHECK(ts && defs && F >= 0, "null times/outputs");
+  int rc;
+  for (int f = 0; f < F; ++f)
+    if ((rc = check_deformed(&defs[f], g->n, g->sh_degree, true)) != FGS_OK) return rc;
+  std::vector<float> ut;
+  std::vector<fgs_deformed> uo;
+  std::vector<int> map(F);
+  for (int f = 0; f < F; ++f) {
+    int j = 0;
+    while (j < (int)ut.size() && memcmp(&ut[j], &ts[f], sizeof(float)) != 0) ++j;
+    if (j == (int)ut.size()) { ut.push_back(ts[f]); uo.push_back(defs[f]); }
+    map[f] = j;
+  }
+  rc = deform_impl(g, h, m, ut.data(), (int)ut.size(), 0, g->n, uo.data(), s);
+  if (rc != FGS_OK) return rc;
+  render_defs.resize(F);
+  for (int f = 0; f < F; ++f) render_defs[f] = uo[map[f]];
+  return FGS_OK;
+}
+}  // namespace
+}  // namespace fgs
+
 int fgs_frames(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, const float* ts,
                const fgs_camera* cams, int32_t n_frames, fgs_deformed* defs_scratch, float* const* images,
                void* ws, size_t ws_bytes, fgs_stream_t stream) {
   if (!g) return fail(FGS_E_INVALID, "gaussians is NULL");
-  int rc = deform_impl(g, field, mlp, ts, n_frames, 0, g->n, defs_scratch, (cudaStream_t)stream);
+  std::vector<fgs_deformed> rd;
+  int rc = frames_deform(g, field, mlp, ts, n_frames, defs_scratch, (cudaStream_t)stream, rd);
   if (rc != FGS_OK) return rc;
-  return render_impl(cams, defs_scratch, images, n_frames, ws, ws_bytes, nullptr, (cudaStream_t)stream);
+  return render_impl(cams, rd.data(), images, n_frames, ws, ws_bytes, nullptr, (cudaStream_t)stream);
 }
 
 int fgs_profile_enable(int enable) {
@@ -571,7 +600,8 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   }
   // Deform all frames in one launch (the spatial-plane work is shared across times), then render in
   // chunks; the device->host copy of chunk c runs on a side stream while chunk c+1 renders.
-  rc = deform_impl(&gd, &hd, &md, ts, F, 0, gd.n, defs.data(), s);
+  std::vector<fgs_deformed> rdefs;
+  rc = frames_deform(&gd, &hd, &md, ts, F, defs.data(), s, rdefs);
   if (rc != FGS_OK) return rc;
   CopyStreams& cs = copy_streams();
   if (!cs.ok) return cuda_fail(cs.err, "copy stream setup");
@@ -579,7 +609,7 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   const int chunk = std::max(1, std::min(F, kHostChunkFrames));
   for (int f0 = 0; f0 < F; f0 += chunk) {
     const int nf = std::min(chunk, F - f0);
-    rc = render_impl(cams + f0, defs.data() + f0, imgs.data() + f0, nf, d + L.render + (size_t)f0 * L.per_render,
+    rc = render_impl(cams + f0, rdefs.data() + f0, imgs.data() + f0, nf, d + L.render + (size_t)f0 * L.per_render,
                      L.per_render * (size_t)nf, nullptr, s);
     if (rc != FGS_OK) return rc;
     cudaEvent_t ev = cs.event(f0 / chunk);

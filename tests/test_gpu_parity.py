@@ -258,3 +258,22 @@ def test_sharded_frames_single_rank_equals_fgs_frames():
     torch.cuda.synchronize()
     for a, b in zip(imgs, ref):
         assert torch.equal(a, b)
+
+
+def test_frames_sharing_a_time_share_the_deformation():
+    """fgs_frames deforms each distinct t once; frames at the same t (views of one instant) render
+    from it — images equal the per-frame deform + render path bit for bit."""
+    import torch
+    s = make_scene("dnerf", n=20_000, width=160, height=120, n_frames=3)
+    ds = _ds(s)
+    ts = [float(s.times[1]), float(s.times[1]), float(s.times[2])]
+    scratch, _ = ds.alloc_deformed(3)
+    imgs = [torch.empty((3, 120, 160), device="cuda") for _ in range(3)]
+    ws = ds.alloc_workspace(3)
+    fgs.fgs_frames(ds.g, ds.field, ds.mlp, ts, ds.cams, scratch, imgs, ws)
+    for f in range(3):
+        d, _, _ = gpu_deform(ds, ts[f])
+        ws1 = ds.alloc_workspace(1)
+        im = torch.empty((3, 120, 160), device="cuda")
+        fgs.fgs_render(ds.cams[f], d, im, ws1)
+        assert torch.equal(im, imgs[f]), f
