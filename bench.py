@@ -519,6 +519,8 @@ def main():
     ap.add_argument("--impl", default="fgs", choices=["fgs", "reference"])
     ap.add_argument("--config", default="dnerf")
     ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None,
+                    help="override the number of Gaussians (SURVEY 8(f) N-sweep: same distributions)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="frames", choices=["frames", "shard"],
@@ -533,7 +535,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     from paper_2310_08528_b200.inputs import make_scene
-    scene = make_scene(args.config, n_frames=args.frames)
+    scene = make_scene(args.config, n_frames=args.frames, n=args.n)
 
     if args.impl == "reference":
         run_reference(args, scene, rank)

@@ -9,7 +9,9 @@
  *
  * Conventions (all entry points):
  *  - Every array pointer inside the structs and every image/workspace pointer is a DEVICE pointer
- *    (cudaMalloc / torch CUDA tensor), fp32 unless stated, C-contiguous, 16-byte aligned.  Struct
+ *    (cudaMalloc / torch CUDA tensor), fp32 unless stated, C-contiguous, 16-byte aligned — except
+ *    means, log_scales and opacity_logits, which need only 4-byte alignment, so that a struct may
+ *    view a row range of a larger array (composition of several models into one G').  Struct
  *    and struct-array arguments themselves (and `ts`) live in HOST memory and are read before the
  *    call returns.  `stream` is a cudaStream_t (0 = legacy default stream).
  *  - Ownership: the caller owns every buffer; the library never allocates device memory on these

@@ -29,6 +29,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+bool aligned4(const void* p) { return ((uintptr_t)p & 3u) == 0; }
 
 #define FGS_CHECK(cond, msg) \
   do {                       \
@@ -41,9 +42,9 @@ int check_gaussians(const fgs_gaussians* g) {
   FGS_CHECK(g->sh_degree >= 0 && g->sh_degree <= 3, "sh_degree must be in [0,3]");
   if (g->n == 0) return FGS_OK;
   FGS_CHECK(g->means && g->log_scales && g->quats && g->opacity_logits && g->sh, "null Gaussian array");
-  FGS_CHECK(aligned16(g->means) && aligned16(g->log_scales) && aligned16(g->quats) &&
-                aligned16(g->opacity_logits) && aligned16(g->sh),
-            "Gaussian arrays must be 16-byte aligned");
+  FGS_CHECK(aligned4(g->means) && aligned4(g->log_scales) && aligned16(g->quats) &&
+                aligned4(g->opacity_logits) && aligned16(g->sh),
+            "Gaussian arrays misaligned (quats, sh: 16 B; means, log_scales, opacity: 4 B)");
   return FGS_OK;
 }
 
@@ -73,8 +74,12 @@ int check_deformed(const fgs_deformed* d, int64_t n, int sh_degree, bool writabl
   FGS_CHECK(d->sh_degree == sh_degree, "deformed.sh_degree mismatch");
   if (n == 0) return FGS_OK;
   FGS_CHECK(d->means && d->log_scales && d->quats, "null deformed output array");
-  FGS_CHECK(aligned16(d->means) && aligned16(d->log_scales) && aligned16(d->quats), "deformed arrays misaligned");
-  if (!writable) FGS_CHECK(d->opacity_logits && d->sh, "null deformed opacity/sh");
+  FGS_CHECK(aligned4(d->means) && aligned4(d->log_scales) && aligned16(d->quats),
+            "deformed arrays misaligned (quats: 16 B; means, log_scales: 4 B)");
+  if (!writable) {
+    FGS_CHECK(d->opacity_logits && d->sh, "null deformed opacity/sh");
+    FGS_CHECK(aligned4(d->opacity_logits) && aligned16(d->sh), "deformed opacity/sh misaligned");
+  }
   return FGS_OK;
 }
 

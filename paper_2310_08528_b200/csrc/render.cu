@@ -386,22 +386,6 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ tile sort (a6)
-// Bitonic sort of n2 (power of two) 64-bit keys in shared memory by NT threads.
-template <int NT>
-__device__ __forceinline__ void bitonic_sort_smem(unsigned long long* sk, int n2) {
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int p = threadIdx.x; p < (n2 >> 1); p += NT) {
-        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));   // bit j of i is 0; partner i | j
-        const unsigned long long a = sk[i], c = sk[i | j];
-        const bool up = (i & k) == 0;
-        if ((a > c) == up) { sk[i] = c; sk[i | j] = a; }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 __device__ __forceinline__ int pow2_at_least(int v) {
   int p = 2;
   while (p < v) p <<= 1;
@@ -550,64 +534,92 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
   }
 }
 
-// Lists longer than b.sort_cap: sorted in place in global memory by one CTA per tile — bitonic runs
-// of kLargeSortChunk in shared memory, then merge-path merges ping-ponging through inst2.
-__device__ __forceinline__ void long_sort_one(const RenderBatch& b, int f, int tile) {
+// Lists longer than b.sort_cap: one CTA (8 warps) per list, persistent over the frame's worklist.
+// Up to kCtaSortMax keys: runs of 256 sorted in registers by the warps, then merge-path levels over
+// all 256 threads, ping-ponging between two shared buffers.  Longer lists: segments of kCtaSortMax
+// sorted that way in place, then merge-path levels in global memory through the inst2 scratch.
+constexpr int kCtaSortMax = 4096;
+constexpr size_t kLongSortSmem = 2 * kCtaSortMax * sizeof(unsigned long long);   // 64 KB dynamic
+
+__device__ __forceinline__ void block_merge(const unsigned long long* a, int na, const unsigned long long* bq,
+                                            int nb, unsigned long long* out, int t, int nt) {
+  const int n = na + nb;
+  const int per = (n + nt - 1) / nt;
+  const int d0 = min(n, t * per), d1 = min(n, d0 + per);
+  if (d0 >= d1) return;
+  int lo = max(0, d0 - nb), hi = min(d0, na);
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] < bq[d0 - 1 - m]) lo = m + 1; else hi = m;
+  }
+  int ia = lo, ib = d0 - lo;
+  unsigned long long va = ia < na ? a[ia] : ~0ull, vb = ib < nb ? bq[ib] : ~0ull;
+  for (int d = d0; d < d1; ++d) {
+    const bool ta = va < vb;
+    out[d] = ta ? va : vb;
+    if (ta) { ++ia; va = ia < na ? a[ia] : ~0ull; }
+    else { ++ib; vb = ib < nb ? bq[ib] : ~0ull; }
+  }
+}
+
+// Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA.
+__device__ void cta_sort(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sA,
+                         unsigned long long* sB) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kLargeSortThreads / 32;
+  for (int r0 = warp * 256; r0 < L; r0 += NW * 256)
+    warp_sort_upto256(src + r0, sA + r0, min(256, L - r0), lane);
+  __syncthreads();
+  unsigned long long* A = sA;
+  unsigned long long* B = sB;
+  for (int w = 256; w < L; w <<= 1) {
+    const bool last = 2 * w >= L;
+    unsigned long long* out = last ? dst : B;
+    for (int s0 = 0; s0 < L; s0 += 2 * w) {
+      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
+      block_merge(A + s0, na, A + s0 + na, nb, out + s0, threadIdx.x, kLargeSortThreads);
+    }
+    __syncthreads();
+    unsigned long long* t = A; A = B; B = t;
+  }
+  if (L <= 256) {   // a single run: copy it out
+    for (int q = threadIdx.x; q < L; q += kLargeSortThreads) dst[q] = sA[q];
+    __syncthreads();
+  }
+}
+
+__device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned long long* sm) {
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
   unsigned long long* A = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
   unsigned long long* B = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst2) + rg.x;
-  __shared__ unsigned long long sk[kLargeSortChunk];
-  for (int c0 = 0; c0 < L; c0 += kLargeSortChunk) {
-    const int len = min(kLargeSortChunk, L - c0);
-    const int n2 = pow2_at_least(len);
-    for (int q = threadIdx.x; q < n2; q += kLargeSortThreads) sk[q] = q < len ? A[c0 + q] : ~0ull;
-    __syncthreads();
-    bitonic_sort_smem<kLargeSortThreads>(sk, n2);
-    for (int q = threadIdx.x; q < len; q += kLargeSortThreads) A[c0 + q] = sk[q];
-    __syncthreads();
-  }
+  for (int c0 = 0; c0 < L; c0 += kCtaSortMax) cta_sort(A + c0, A + c0, min(kCtaSortMax, L - c0), sm, sm + kCtaSortMax);
   unsigned long long* src = A;
   unsigned long long* dst = B;
-  for (int w = kLargeSortChunk; w < L; w <<= 1) {
-    for (int s = 0; s < L; s += 2 * w) {
-      const int na = min(w, L - s), nb = max(0, min(w, L - s - w));
-      const unsigned long long* a = src + s;
-      const unsigned long long* bq = src + s + na;
-      const int total = na + nb;
-      const int per = (total + kLargeSortThreads - 1) / kLargeSortThreads;
-      const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
-      if (d0 < d1) {
-        // merge path: i = number of a-elements among the first d0 outputs (keys are unique)
-        int lo = max(0, d0 - nb), hi = min(d0, na);
-        while (lo < hi) {
-          const int m = (lo + hi) >> 1;
-          if (a[m] < bq[d0 - 1 - m]) lo = m + 1; else hi = m;
-        }
-        int ia = lo, ib = d0 - lo;
-        for (int d = d0; d < d1; ++d) {
-          const bool take_a = ib >= nb || (ia < na && a[ia] < bq[ib]);
-          dst[s + d] = take_a ? a[ia++] : bq[ib++];
-        }
-      }
+  for (int w = kCtaSortMax; w < L; w <<= 1) {
+    for (int s0 = 0; s0 < L; s0 += 2 * w) {
+      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
+      block_merge(src + s0, na, src + s0 + na, nb, dst + s0, threadIdx.x, kLargeSortThreads);
     }
     __syncthreads();
     unsigned long long* t = src; src = dst; dst = t;
   }
-  if (src != A)
+  if (src != A) {
     for (int q = threadIdx.x; q < L; q += kLargeSortThreads) A[q] = src[q];
-}
-
-__global__ void __launch_bounds__(kLargeSortThreads) long_sort_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const uint32_t n_long = cnt_ptr(b, f)[4];
-  const uint32_t* work = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list);
-  for (uint32_t w = blockIdx.x; w < n_long; w += gridDim.x) {
-    long_sort_one(b, f, (int)work[w]);
     __syncthreads();
   }
 }
 
+__global__ void __launch_bounds__(kLargeSortThreads) long_sort_kernel(const __grid_constant__ RenderBatch b) {
+  extern __shared__ unsigned long long long_sm[];
+  const int f = blockIdx.y;
+  const uint32_t n_long = cnt_ptr(b, f)[4];
+  const uint32_t* work = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list);
+  for (uint32_t w = blockIdx.x; w < n_long; w += gridDim.x) {
+    long_sort_one(b, f, (int)work[w], long_sm);
+    __syncthreads();
+  }
+}
 
 // ------------------------------------------------------------------------------ blend (Eq. 4)
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -815,8 +827,12 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
   tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
-  // long lists: a few persistent CTAs per frame walk the worklist (usually empty)
-  long_sort_kernel<<<dim3((unsigned)std::max(1, std::min(32, num_sms_cached() / F)), F), kLargeSortThreads, 0, s>>>(b);
+  // long lists: persistent CTAs (3 per SM over the batch) walk each frame's worklist (usually empty)
+  static const cudaError_t attr = cudaFuncSetAttribute(long_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)kLongSortSmem);
+  if (attr != cudaSuccess) return attr;
+  long_sort_kernel<<<dim3((unsigned)std::max(1, (3 * num_sms_cached() + F - 1) / F), F), kLargeSortThreads,
+                     kLongSortSmem, s>>>(b);
   note_launches(2);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
   prof_mark(FGS_STAGE_BLEND, true, s);

@@ -244,6 +244,16 @@ def make_camera(cam) -> fgs_camera:
     return c
 
 
+def deformed_rows(d: fgs_deformed, row0: int, n: int, opacity_logits=None, sh=None) -> fgs_deformed:
+    """View of rows [row0, row0 + n) of a deformed set's means / log_scales / quats as an fgs_deformed
+    of n Gaussians (composition: deform model k into its own row range of one G', then render the
+    union).  opacity/sh default to the same row range of d's arrays."""
+    K3 = (d.sh_degree + 1) ** 2 * 3
+    return fgs_deformed(n, d.sh_degree, d.means + 12 * row0, d.log_scales + 12 * row0, d.quats + 16 * row0,
+                        (d.opacity_logits + 4 * row0) if opacity_logits is None else opacity_logits,
+                        (d.sh + 4 * K3 * row0) if sh is None else sh)
+
+
 class HostScene:
     """A Scene's arrays in pinned host memory + C structs whose pointers are HOST pointers
     (the inputs of fgs_frames_host, i.e. the end-to-end path)."""

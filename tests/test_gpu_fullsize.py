@@ -29,7 +29,8 @@ PSNR_MIN = 60.0
 
 # (config, frames in the batch): the bench batches of D (20) and N3 (8); H and S with fewer frames of
 # the same per-frame size (their full batches only repeat the same kernels with other t / cameras).
-CASES = [("dnerf", None), ("neu3d", None), ("hypernerf", 6), ("scaling", 3)]
+CASES = [("dnerf", None, None), ("neu3d", None, None), ("hypernerf", 6, None), ("scaling", 3, None),
+         ("dnerf", 4, 1_000_000), ("dnerf", 4, 10_000)]     # ends of the N sweep
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -53,11 +54,12 @@ def _run_frames(s):
     return ds, outs, tens, imgs
 
 
-@pytest.mark.parametrize("name,frames", CASES)
-def test_fullsize_batch_parity(name, frames):
-    s = make_scene(name, n_frames=frames)
+@pytest.mark.parametrize("name,frames,n", CASES)
+def test_fullsize_batch_parity(name, frames, n):
+    s = make_scene(name, n_frames=frames, n=n)
     ds, outs, tens, imgs = _run_frames(s)
-    n, F = s.n, s.n_frames
+    F = s.n_frames
+    n = s.n
     rng = np.random.default_rng(123)
     W, H = s.cameras[0].width, s.cameras[0].height
     gx, gy = OR.tile_grid(W, H)

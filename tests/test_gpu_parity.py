@@ -277,3 +277,38 @@ def test_frames_sharing_a_time_share_the_deformation():
         im = torch.empty((3, 120, 160), device="cuda")
         fgs.fgs_render(ds.cams[f], d, im, ws1)
         assert torch.equal(im, imgs[f]), f
+
+
+def test_composition_of_two_models():
+    """two 4D-GS models with their own fields and MLPs are deformed into
+    row ranges of ONE G' (fgs_deformed row views) and rendered together; equals the oracle render of
+    the merged set (deform per model by the oracle, then one render)."""
+    import torch
+    a = make_scene("tiny", n=1203, seed=10, width=72, height=56)
+    b = make_scene("tiny", n=801, seed=11, width=72, height=56)
+    b.means[:] = (b.means * 0.5 + np.float32(0.3)).astype(np.float32)   # a second object, inside A's box
+    dA, dB = _ds(a), _ds(b)
+    N = a.n + b.n
+    X = torch.empty((N, 3), device="cuda"); S = torch.empty((N, 3), device="cuda")
+    Q = torch.empty((N, 4), device="cuda")
+    op = torch.cat([dA.opacity_logits, dB.opacity_logits]).contiguous()
+    sh = torch.cat([dA.sh, dB.sh]).contiguous()
+    whole = fgs.fgs_deformed(N, 0, X.data_ptr(), S.data_ptr(), Q.data_ptr(), op.data_ptr(), sh.data_ptr())
+    t = 0.61
+    fgs.fgs_deform(dA.g, dA.field, dA.mlp, t, fgs.deformed_rows(whole, 0, a.n, op.data_ptr(), sh.data_ptr()))
+    fgs.fgs_deform(dB.g, dB.field, dB.mlp, t, fgs.deformed_rows(whole, a.n, b.n, op.data_ptr(), sh.data_ptr()))
+    torch.cuda.synchronize()
+    g = {"means": X.cpu().numpy(), "log_scales": S.cpu().numpy(), "quats": Q.cpu().numpy()}
+    ra, rb = oracle.deform_ref(a, t), oracle.deform_ref(b, t)
+    for k in g:
+        ref = np.concatenate([ra[k], rb[k]])
+        assert np.abs(g[k].astype(np.float64) - ref).max() <= DEFORM_TOL, k
+    cam = a.cameras[0]
+    ws = dA.alloc_workspace(1, 16 * N)
+    img = torch.empty((3, 56, 72), device="cuda")
+    fgs.fgs_render(fgs.make_camera(cam), whole, img, ws)
+    fgs.fgs_render_status(ws)
+    opn = np.concatenate([a.opacity_logits, b.opacity_logits]); shn = np.concatenate([a.sh, b.sh])
+    ref = OR.render_ref(g, opn, shn, 0, cam)
+    pix = compare_pixels(img.cpu().numpy(), ref["image"], ref["flagged"])
+    assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, pix
