@@ -657,27 +657,37 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
   }
 }
 
-// Conservative ellipse-vs-box cull: true unless q2(d) = qa dx^2 + qb dx dy + qc dy^2 (the negated
-// log2-domain exponent, PSD) exceeds thr over the whole box [xl,xh] x [yl,yh] of offsets
-// d = pixel - mean.  The minimum of a convex quadratic over a box that does not contain its
-// minimiser d = 0 lies on a face whose half-space excludes 0 (KKT), so at most one x-face and one
-// y-face are candidates; on each the 1-D minimiser is clamped to the face.  An inexact minimiser
-// only raises the computed value by qc * delta^2 (quadratic in its error), far inside thr's margin.
-__device__ __forceinline__ bool box_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
-                                              float yl, float yh) {
-  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+// Conservative ellipse-vs-box cull: a half-box is skipped only if q2(d) = qa dx^2 + qb dx dy + qc dy^2
+// (the negated log2-domain exponent, PSD) exceeds thr over the whole box of offsets d = pixel - mean.
+// The minimum of a convex quadratic over a box that does not contain its minimiser d = 0 lies on a
+// face whose half-space excludes 0 (KKT), so at most one x-face and one y-face are candidates; on
+// each the 1-D minimiser is clamped to the face.  An inexact minimiser only raises the computed value
+// by qc delta^2 (quadratic in its error), far inside thr's margin.
+// Both half-boxes of a warp at once: they share the x-range, so the x-face and the two minimiser
+// ratios (x* = kx ey on a y-face, y* = ky ex on an x-face) are computed once.
+__device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx, float ky, float ex, float xl,
+                                          float xh, float yl, float yh) {
   const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
   float q = 0.f;
   if (ex != 0.f) {
-    const float yy = fminf(fmaxf(__fdividef(-qb * ex, 2.f * qc), yl), yh);
+    const float yy = fminf(fmaxf(ky * ex, yl), yh);
     q = fmaf(fmaf(qa, ex, qb * yy), ex, qc * yy * yy);
   }
   if (ey != 0.f) {
-    const float xx = fminf(fmaxf(__fdividef(-qb * ey, 2.f * qa), xl), xh);
+    const float xx = fminf(fmaxf(kx * ey, xl), xh);
     const float q2 = fmaf(fmaf(qc, ey, qb * xx), ey, qa * xx * xx);
     q = ex != 0.f ? fminf(q, q2) : q2;
   }
-  return q <= thr;
+  return q;
+}
+
+__device__ __forceinline__ void halfboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
+                                                    float ylA, float yhA, float ylB, float yhB, bool& nA,
+                                                    bool& nB) {
+  const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
+  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+  nA = face_min(qa, qb, qc, kx, ky, ex, xl, xh, ylA, yhA) <= thr;
+  nB = face_min(qa, qb, qc, kx, ky, ex, xl, xh, ylB, yhB) <= thr;
 }
 
 template <bool DBG>
@@ -736,8 +746,9 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
         const float4 a = s0[jt];
         const float qa = -a.z, qb = -a.w, qc = -s1[jt].x, thr = s2[jt].y;
         const float xl = bxl - a.x, xh = bxh - a.x;
-        needA = liveA && box_may_reach(qa, qb, qc, thr, xl, xh, byl - a.y, bym - a.y);
-        needB = liveB && box_may_reach(qa, qb, qc, thr, xl, xh, byn - a.y, byh - a.y);
+        halfboxes_may_reach(qa, qb, qc, thr, xl, xh, byl - a.y, bym - a.y, byn - a.y, byh - a.y, needA, needB);
+        needA = needA && liveA;
+        needB = needB && liveB;
       }
       const uint32_t mA = __ballot_sync(0xffffffffu, needA), mB = __ballot_sync(0xffffffffu, needB);
       if (DBG) { n_tested += (uint32_t)min(32, cnt - c0); n_evald += __popc(mA) + __popc(mB); }
