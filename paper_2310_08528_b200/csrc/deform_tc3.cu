@@ -100,9 +100,11 @@ struct Tc3Smem {
   static constexpr int B_BYTES = 64 * WIDTH * 4;
   static constexpr int OFF_BHI = 0;
   static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
+  // tiles per group the TMEM plan allows for phi_d width WIDTH at in_dim 64 (more for smaller in_dim)
+  static constexpr int GMAX = WIDTH >= 128 ? 2 : (WIDTH >= 64 ? 4 : kMaxG);
   static constexpr int OFF_LINE = OFF_BLO + B_BYTES;
-  static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [kMaxG][128][4]
-  static constexpr int OFF_WH = OFF_U + kMaxG * kM * 16;
+  static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [GMAX][128][4]
+  static constexpr int OFF_WH = OFF_U + GMAX * kM * 16;
   static constexpr int OFF_BD = OFF_WH + 12 * WIDTH * 4;   // head weights transposed [W][12]
   static constexpr int OFF_BH = OFF_BD + WIDTH * 4;
   static constexpr int OFF_WIN = OFF_BH + 16 * 4;               // int [FGS_MAX_SCALES][3][2]
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   const int IN = p.in_dim;
   const int KP = (IN + 7) & ~7;
   const uint32_t colA_hi = 2 * DW, colA_lo = 2 * DW + KP, colS = 2 * DW + 2 * KP;
-  const int G = min(kMaxG, (kTmemCols - (int)colS) / IN);
+  const int G = min(SM::GMAX, (kTmemCols - (int)colS) / IN);
 
   extern __shared__ __align__(128) unsigned char smem[];
   float* line = reinterpret_cast<float*>(smem + SM::OFF_LINE);
