@@ -223,14 +223,17 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
         n = max(stage_launches.get(stage, 0), 1)
         return stage_ms.get(stage, 0.0) / 1e3 / n
 
-    # deform: FP32 lane instructions per Gaussian-frame (sampling FMA + phi_d + heads), HBM 80 B
-    inst_def = (3 * L * f.feat * 5) + (3 * L * f.feat * 5) / F + scene.mlp.in_dim * W + 10 * W
+    # deform: bound by the on-chip gathers of the time lines: per Gaussian-frame
+    # 3 temporal planes x L scales x 2 knots x h fp32 read from shared memory (the spatial product is
+    # sampled once per batch and the MLP runs on the tensor core); peak = 128 B/clk/SM shared memory
     t = avg_launch_s("deform")
     if t > 0:
-        work = inst_def * N * F / 1e12
-        out["deform"] = {"bound": "alu", "achieved": work / t, "peak": fp32_peak, "unit": "Tinst/s",
-                         "frac": work / t / fp32_peak, "traffic": None,
-                         "algorithmic": f"{inst_def:.0f} FP32 inst per Gaussian-frame x {N}x{F}"}
+        by_def = 3 * L * 2 * f.feat * 4
+        work = by_def * N * F / 1e9
+        smem_peak = sms * 128 * clk / 1e9
+        out["deform"] = {"bound": "smem", "achieved": work / t, "peak": smem_peak, "unit": "GB/s",
+                         "frac": work / t / smem_peak, "traffic": None,
+                         "algorithmic": f"{by_def} B of time-line reads per Gaussian-frame x {N}x{F}"}
     # preprocess: HBM bytes per Gaussian (read G' 40 + opacity 4 + SH 12K; write 72 B)
     by_pre = N * (44 + 12 * K + 72) * F
     t = avg_launch_s("preprocess")
