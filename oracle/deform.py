@@ -11,7 +11,10 @@ Steps:
  4. f_d = phi_d(f_h) = ReLU(W_d f_h + b_d) (P:791, reading D5);
  5. dX = phi_x(f_d), dr = phi_r(f_d), ds = phi_s(f_d) (P:797, reading D6);
  6. (X', r', s') = (X + dX, r + dr, s + ds) (raw space, reading D7).
-Opacity and SH are not deformed (G' = {X', s', r', sigma, C}).
+Opacity and SH are not deformed (G' = {X', s', r', sigma, C}) — unless the model carries the
+colour and opacity decoders of P:1232 ("Color and Opacity's Deformation", the variant of Table 5):
+ 7. dC = phi_C(f_d), dalpha = phi_alpha(f_d); C' = C + dC over all (D+1)^2 x 3 SH coefficients
+    and logit' = logit + dalpha (raw space, reading C1 — the same convention as D7).
 """
 from __future__ import annotations
 
@@ -69,17 +72,34 @@ def hexplane_features(means, t, field):
     return np.concatenate(feats, axis=1)
 
 
+def phi_d(f_h, mlp):
+    """f_d = ReLU(W_d f_h + b_d) (reading D5).  Returns [N, W] float64."""
+    W_d = np.asarray(mlp.w_d, np.float64)
+    return np.maximum(0.0, f_h @ W_d.T + np.asarray(mlp.b_d, np.float64))
+
+
 def decoder(f_h, mlp):
     """phi_d then the heads phi_x, phi_r, phi_s (readings D5, D6).
 
     Returns (dX [N,3], dr [N,4], ds [N,3]) float64.
     """
-    W_d = np.asarray(mlp.w_d, np.float64)
-    f_d = np.maximum(0.0, f_h @ W_d.T + np.asarray(mlp.b_d, np.float64))
+    f_d = phi_d(f_h, mlp)
     dX = f_d @ np.asarray(mlp.w_x, np.float64).T + np.asarray(mlp.b_x, np.float64)
     dr = f_d @ np.asarray(mlp.w_r, np.float64).T + np.asarray(mlp.b_r, np.float64)
     ds = f_d @ np.asarray(mlp.w_s, np.float64).T + np.asarray(mlp.b_s, np.float64)
     return dX, dr, ds
+
+
+def colour_opacity_heads(f_h, mlp):
+    """dC = phi_C(f_d) [N, 3K] (k-major, channel-minor: the SH layout) and dalpha = phi_alpha(f_d) [N]
+    (reading C1: one Linear each).  Either is None when the model has no such head."""
+    f_d = phi_d(f_h, mlp)
+    dC = dA = None
+    if getattr(mlp, "w_c", None) is not None:
+        dC = f_d @ np.asarray(mlp.w_c, np.float64).T + np.asarray(mlp.b_c, np.float64)
+    if getattr(mlp, "w_a", None) is not None:
+        dA = f_d @ np.asarray(mlp.w_a, np.float64).T[:, 0] + np.asarray(mlp.b_a, np.float64)[0]
+    return dC, dA
 
 
 def deform_ref(scene, t, means=None, log_scales=None, quats=None, begin=0, end=None):
@@ -96,4 +116,11 @@ def deform_ref(scene, t, means=None, log_scales=None, quats=None, begin=0, end=N
     X, r, s = X[begin:end], r[begin:end], s[begin:end]
     f_h = hexplane_features(X, t, scene.field)
     dX, dr, ds = decoder(f_h, scene.mlp)
-    return {"means": X + dX, "quats": r + dr, "log_scales": s + ds}
+    out = {"means": X + dX, "quats": r + dr, "log_scales": s + ds}
+    dC, dA = colour_opacity_heads(f_h, scene.mlp)
+    if dC is not None:
+        C = np.asarray(scene.sh, np.float64)[begin:end]
+        out["sh"] = C + dC.reshape(C.shape)
+    if dA is not None:
+        out["opacity_logits"] = np.asarray(scene.opacity_logits, np.float64)[begin:end] + dA
+    return out

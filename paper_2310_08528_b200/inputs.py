@@ -75,6 +75,11 @@ class MLP:
     b_r: np.ndarray
     w_s: np.ndarray
     b_s: np.ndarray
+    # optional colour / opacity decoders phi_C, phi_alpha: [3K][W], [3K]; [1][W], [1]
+    w_c: Optional[np.ndarray] = None
+    b_c: Optional[np.ndarray] = None
+    w_a: Optional[np.ndarray] = None
+    b_a: Optional[np.ndarray] = None
 
     @property
     def width(self) -> int:
@@ -344,6 +349,26 @@ def with_heads(scene: Scene, sigma: float, seed: int = 1234, bias_sigma: float =
     mlp = replace(m, w_x=draw((3, W)), w_r=draw((4, W)), w_s=draw((3, W)),
                   b_x=drawb(3), b_r=drawb(4), b_s=drawb(3))
     return replace(scene, mlp=mlp)
+
+
+def with_colour_heads(scene: Scene, sigma_c: float, sigma_a: float, seed: int = 4321, colour: bool = True,
+                      opacity: bool = True) -> Scene:
+    """Add the colour / opacity decoders phi_C, phi_alpha of P:1232 (Table 5 variant): weights
+    N(0, sigma), biases N(0, sigma / 2) (sigma = 0 -> exact zero heads)."""
+    rng = np.random.default_rng(seed)
+    m = scene.mlp
+    W = m.width
+    K3 = (scene.sh_degree + 1) ** 2 * 3
+
+    def draw(shape, sg):
+        return _f32(rng.normal(0.0, sg, shape)) if sg > 0 else np.zeros(shape, np.float32)
+
+    kw = {}
+    if colour:
+        kw.update(w_c=draw((K3, W), sigma_c), b_c=draw(K3, sigma_c / 2))
+    if opacity:
+        kw.update(w_a=draw((1, W), sigma_a), b_a=draw(1, sigma_a / 2))
+    return replace(scene, mlp=replace(m, **kw))
 
 
 def with_max_opacity(scene: Scene, max_opacity: float) -> Scene:

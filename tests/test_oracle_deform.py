@@ -185,3 +185,43 @@ def test_grid_clamp_outside_aabb(tiny_scene):
     u = grid_coords(X, s.field.bmin, s.field.bmax, 0.25)
     assert np.array_equal(u[0], [1.0, 0.0, 0.5, 0.25])
     assert np.array_equal(u[1], [1.0, 1.0, 1.0, 0.25])
+
+
+# ---------------------------------------------------------------- colour / opacity decoders
+def test_colour_opacity_heads_match_scalar_loop():
+    """dC = phi_C(f_d), dalpha = phi_alpha(f_d), one Linear each (reading C1) — scalar-loop brute force,
+    and the SH layout of dC (k-major, channel-minor)."""
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = with_colour_heads(make_scene("dnerf", n=40), 0.3, 0.5, seed=9)
+    t = 0.42
+    fh = hexplane_features(s.means[:6], t, s.field)
+    d = oracle.deform_ref(s, t, begin=0, end=6)
+    m = s.mlp
+    K = (s.sh_degree + 1) ** 2
+    for n in range(6):
+        hid = []
+        for o in range(m.width):
+            acc = float(m.b_d[o]) + sum(float(m.w_d[o, k]) * fh[n, k] for k in range(m.in_dim))
+            hid.append(max(0.0, acc))
+        for kk in range(K):
+            for ch in range(3):
+                o = 3 * kk + ch
+                acc = float(m.b_c[o]) + sum(float(m.w_c[o, j]) * hid[j] for j in range(m.width))
+                assert abs(float(s.sh[n, kk, ch]) + acc - d["sh"][n, kk, ch]) < 1e-12
+        acc = float(m.b_a[0]) + sum(float(m.w_a[0, j]) * hid[j] for j in range(m.width))
+        assert abs(float(s.opacity_logits[n]) + acc - d["opacity_logits"][n]) < 1e-12
+
+
+def test_zero_colour_heads_identity_and_constant_shift():
+    """Zero phi_C, phi_alpha leave SH and opacity unchanged (exact); a bias-only phi_alpha shifts every
+    logit by that bias; models without the heads return no SH / opacity (P:802 G' aliases them)."""
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    base = make_scene("tiny", n=300)
+    assert "sh" not in oracle.deform_ref(base, 0.3) and "opacity_logits" not in oracle.deform_ref(base, 0.3)
+    s = with_colour_heads(base, 0.0, 0.0)
+    d = oracle.deform_ref(s, 0.3)
+    assert np.array_equal(d["sh"], s.sh.astype(np.float64))
+    assert np.array_equal(d["opacity_logits"], s.opacity_logits.astype(np.float64))
+    s2 = replace(s, mlp=replace(s.mlp, b_a=np.array([0.25], np.float32)))
+    d2 = oracle.deform_ref(s2, 0.3)
+    assert np.array_equal(d2["opacity_logits"] - s.opacity_logits.astype(np.float64), np.full(s.n, 0.25))
