@@ -52,9 +52,10 @@ def load_peaks():
 
 def workload_desc(scene):
     f = scene.field
+    heads = " + phi_C/phi_alpha decoders (P:1232)" if getattr(scene.mlp, "w_c", None) is not None else ""
     return (f"{scene.name}: {scene.n} Gaussians, {scene.cameras[0].width}x{scene.cameras[0].height}, "
             f"SH{scene.sh_degree}, HexPlane {'/'.join(map(str, f.res))} x t{f.t_res} h{f.feat}, "
-            f"phi_d {scene.mlp.width}, {scene.n_frames} (t, view) frames per step")
+            f"phi_d {scene.mlp.width}{heads}, {scene.n_frames} (t, view) frames per step")
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -522,6 +523,8 @@ def main():
     ap.add_argument("--impl", default="fgs", choices=["fgs", "reference"])
     ap.add_argument("--config", default="dnerf")
     ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--colour-heads", action="store_true",
+                    help="P:1232 variant: add the colour / opacity decoders phi_C, phi_alpha (SURVEY 8(f) rank 2)")
     ap.add_argument("--n", type=int, default=None,
                     help="override the number of Gaussians (SURVEY 8(f) N-sweep: same distributions)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -539,6 +542,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     from paper_2310_08528_b200.inputs import make_scene
     scene = make_scene(args.config, n_frames=args.frames, n=args.n)
+    if args.colour_heads:
+        from paper_2310_08528_b200.inputs import with_colour_heads
+        scene = with_colour_heads(scene, 0.05, 0.05)
 
     if args.impl == "reference":
         run_reference(args, scene, rank)

@@ -74,7 +74,12 @@ typedef struct {
 } fgs_hexplanes;
 
 /* phi_d (one Linear + ReLU) and the heads phi_x, phi_r, phi_s (one Linear each).
- * Row-major [out][in] (PyTorch Linear layout). */
+ * Row-major [out][in] (PyTorch Linear layout).  Optional: the colour and opacity decoders phi_C,
+ * phi_alpha of P:1232 ("Color and Opacity's Deformation"): dC = phi_C(f_d) over all K x 3 SH
+ * coefficients (output o = 3k + channel, the SH layout), dalpha = phi_alpha(f_d) on the opacity logit;
+ * NULL weights = no such head.  With either head, fgs_deform writes the deformed SH / opacity into the
+ * fgs_deformed arrays (which must then be caller buffers, not the canonical arrays); the field must fit
+ * the warp-specialised deform kernel (else FGS_E_NOTIMPL). */
 typedef struct {
   int32_t in_dim;               /* = feat * n_scales (<= 64)                                      */
   int32_t width;                /* hidden width W of phi_d: 32, 64 or 128                         */
@@ -82,18 +87,21 @@ typedef struct {
   const float *w_x, *b_x;       /* [3][W], [3]                                                    */
   const float *w_r, *b_r;       /* [4][W], [4]                                                    */
   const float *w_s, *b_s;       /* [3][W], [3]                                                    */
+  const float *w_c, *b_c;       /* optional phi_C: [3K][W], [3K]  (K = (sh_degree+1)^2)           */
+  const float *w_a, *b_a;       /* optional phi_alpha: [1][W], [1]                                 */
 } fgs_mlp;
 
 /* Deformed Gaussians G' = {X', s', r', sigma, C}.  fgs_deform writes means, log_scales and
- * quats (raw: X + dX, log s + ds, r + dr); opacity and SH alias the canonical arrays. */
+ * quats (raw: X + dX, log s + ds, r + dr); opacity and SH alias the canonical arrays, unless the
+ * MLP has phi_alpha / phi_C, in which case fgs_deform writes logit + dalpha / C + dC there. */
 typedef struct {
   int64_t n;
   int32_t sh_degree;
   float* means;                 /* [n][3] */
   float* log_scales;            /* [n][3] */
   float* quats;                 /* [n][4] */
-  const float* opacity_logits;  /* [n]       (alias of the canonical array)                       */
-  const float* sh;              /* [n][K][3] (alias of the canonical array)                       */
+  float* opacity_logits;        /* [n]       canonical alias, or written (phi_alpha)               */
+  float* sh;                    /* [n][K][3] canonical alias, or written (phi_C)                   */
 } fgs_deformed;
 
 /* View matrix M = [R, T] + pinhole intrinsics.  World->camera, row-major, OpenCV axes

@@ -64,6 +64,8 @@ int check_field(const fgs_hexplanes* h, const fgs_mlp* m) {
   FGS_CHECK(m->in_dim <= 64, "in_dim must be <= 64");
   FGS_CHECK(m->width == 32 || m->width == 64 || m->width == 128, "mlp.width must be 32, 64 or 128");
   FGS_CHECK(m->w_d && m->b_d && m->w_x && m->b_x && m->w_r && m->b_r && m->w_s && m->b_s, "null MLP array");
+  FGS_CHECK((m->w_c == nullptr) == (m->b_c == nullptr), "phi_C needs both w_c and b_c");
+  FGS_CHECK((m->w_a == nullptr) == (m->b_a == nullptr), "phi_alpha needs both w_a and b_a");
   FGS_CHECK(aligned16(m->w_d), "w_d must be 16-byte aligned");
   return FGS_OK;
 }
@@ -102,6 +104,9 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.in_dim = m->in_dim; p.width = m->width;
   p.w_d = m->w_d; p.b_d = m->b_d; p.w_x = m->w_x; p.b_x = m->b_x;
   p.w_r = m->w_r; p.b_r = m->b_r; p.w_s = m->w_s; p.b_s = m->b_s;
+  p.w_c = m->w_c; p.b_c = m->b_c; p.w_a = m->w_a; p.b_a = m->b_a;
+  p.n_c = m->w_c ? 3 * (g->sh_degree + 1) * (g->sh_degree + 1) : 0;
+  p.sh_in = g->sh; p.opac_in = g->opacity_logits;
 }
 
 // FGS_DEFORM = simt | tc1 | tc2 | tc3 forces a deform kernel (A/B comparison).  Default: tc3
@@ -120,10 +125,12 @@ int deform_choice() {
 }
 
 cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
+  if (p.w_c || p.w_a) return launch_deform_tc3(p, s);   // the only kernel with the P:1232 decoders
   switch (deform_choice()) {
     case 1: return launch_deform(p, s);
     case 2: return launch_deform_tc(p, s);
     case 3: return launch_deform_tc2(p, s);
+    case 4: return launch_deform_tc3(p, s);
     default:
       if (deform_tc3_supported(p)) return launch_deform_tc3(p, s);
       return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
@@ -137,14 +144,23 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
   if ((rc = check_field(h, m)) != FGS_OK) return rc;
   FGS_CHECK(ts && outs && n_t >= 0, "null times/outputs");
   FGS_CHECK(begin >= 0 && begin <= end && end <= g->n, "begin/end out of range");
+  const bool heads_c = m->w_c != nullptr, heads_a = m->w_a != nullptr;
   for (int f = 0; f < n_t; ++f) {
     FGS_CHECK(isfinite(ts[f]) && ts[f] >= 0.f && ts[f] <= 1.f, "t must be finite and in [0,1]");
     if ((rc = check_deformed(&outs[f], g->n, g->sh_degree, true)) != FGS_OK) return rc;
+    if (g->n > 0 && heads_c)
+      FGS_CHECK(outs[f].sh && aligned16(outs[f].sh) && outs[f].sh != g->sh,
+                "phi_C: deformed.sh must be a caller buffer (16-byte aligned), not the canonical SH");
+    if (g->n > 0 && heads_a)
+      FGS_CHECK(outs[f].opacity_logits && aligned4(outs[f].opacity_logits) && outs[f].opacity_logits != g->opacity_logits,
+                "phi_alpha: deformed.opacity_logits must be a caller buffer, not the canonical array");
   }
   if (end == begin || n_t == 0) return FGS_OK;
   DeformBatch p;
   fill_deform(p, g, h, m);
   p.begin = begin; p.end = end;
+  if ((heads_c || heads_a) && !deform_tc3_supported(p))
+    return fail(FGS_E_NOTIMPL, "colour/opacity decoders need the warp-specialised deform (field too large)");
   for (int f0 = 0; f0 < n_t; f0 += kMaxFrames) {
     p.n_t = std::min(kMaxFrames, n_t - f0);
     for (int f = 0; f < p.n_t; ++f) {
@@ -152,6 +168,8 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
       p.out_means[f] = outs[f0 + f].means;
       p.out_log_scales[f] = outs[f0 + f].log_scales;
       p.out_quats[f] = outs[f0 + f].quats;
+      p.out_sh[f] = outs[f0 + f].sh;
+      p.out_opacity[f] = outs[f0 + f].opacity_logits;
     }
     cudaError_t e = launch_deform_any(p, s);
     if (e != cudaSuccess) return cuda_fail(e, "deform launch");
@@ -468,9 +486,9 @@ int64_t fgs_get_tuning(int32_t key) {
 // ---- end to end with host buffers -------------------------------------------------------------
 namespace {
 struct HostLayout {
-  size_t means, log_scales, quats, opac, sh, planes[FGS_MAX_SCALES][FGS_PLANES], mlp[8], defs, images, render;
-  size_t plane_bytes[FGS_MAX_SCALES][FGS_PLANES], mlp_bytes[8];
-  size_t per_def, per_img, per_render, total;
+  size_t means, log_scales, quats, opac, sh, planes[FGS_MAX_SCALES][FGS_PLANES], mlp[12], defs, images, render;
+  size_t plane_bytes[FGS_MAX_SCALES][FGS_PLANES], mlp_bytes[12];
+  size_t per_def, def_sh, def_opac, per_img, per_render, total;
 };
 HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, int F, int W, int H,
                        int64_t cap) {
@@ -487,9 +505,14 @@ HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs
       L.planes[l][p] = take(L.plane_bytes[l][p]);
     }
   const size_t Wd = (size_t)m->width, In = (size_t)m->in_dim;
-  const size_t mb[8] = {Wd * In * 4, Wd * 4, 3 * Wd * 4, 12, 4 * Wd * 4, 16, 3 * Wd * 4, 12};
-  for (int i = 0; i < 8; ++i) { L.mlp_bytes[i] = mb[i]; L.mlp[i] = take(mb[i]); }
-  L.per_def = align256(12 * n) * 2 + align256(16 * n);
+  const size_t hc = m->w_c ? 3 * K : 0, ha = m->w_a ? 1 : 0;
+  const size_t mb[12] = {Wd * In * 4, Wd * 4, 3 * Wd * 4, 12, 4 * Wd * 4, 16, 3 * Wd * 4, 12,
+                         hc * Wd * 4, hc * 4, ha * Wd * 4, ha * 4};
+  for (int i = 0; i < 12; ++i) { L.mlp_bytes[i] = mb[i]; L.mlp[i] = take(mb[i]); }
+  // per frame: X', s', r' and, with the P:1232 decoders, the deformed SH / opacity
+  L.def_sh = align256(12 * n) * 2 + align256(16 * n);
+  L.def_opac = L.def_sh + (hc ? align256(4 * hc * n) : 0);
+  L.per_def = L.def_opac + (ha ? align256(4 * n) : 0);
   L.defs = take(L.per_def * (size_t)F);
   L.per_img = align256((size_t)3 * W * H * 4);
   L.images = take(L.per_img * (size_t)F);
@@ -581,9 +604,12 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
       hd.planes[l][p] = (const float*)(d + L.planes[l][p]);
     }
   fgs_mlp md = *mh;
-  const float* srcs[8] = {mh->w_d, mh->b_d, mh->w_x, mh->b_x, mh->w_r, mh->b_r, mh->w_s, mh->b_s};
-  const float** dsts[8] = {&md.w_d, &md.b_d, &md.w_x, &md.b_x, &md.w_r, &md.b_r, &md.w_s, &md.b_s};
-  for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
+  const float* srcs[12] = {mh->w_d, mh->b_d, mh->w_x, mh->b_x, mh->w_r, mh->b_r, mh->w_s, mh->b_s,
+                           mh->w_c, mh->b_c, mh->w_a, mh->b_a};
+  const float** dsts[12] = {&md.w_d, &md.b_d, &md.w_x, &md.b_x, &md.w_r, &md.b_r, &md.w_s, &md.b_s,
+                            &md.w_c, &md.b_c, &md.w_a, &md.b_a};
+  for (int i = 0; i < 12 && e == cudaSuccess; ++i) {
+    if (!srcs[i]) { *dsts[i] = nullptr; continue; }
     e = h2d(L.mlp[i], srcs[i], L.mlp_bytes[i]);
     *dsts[i] = (const float*)(d + L.mlp[i]);
   }
@@ -600,7 +626,8 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
     defs[f].means = (float*)base;
     defs[f].log_scales = (float*)(base + align256(12 * n));
     defs[f].quats = (float*)(base + 2 * align256(12 * n));
-    defs[f].opacity_logits = gd.opacity_logits; defs[f].sh = gd.sh;
+    defs[f].opacity_logits = mh->w_a ? (float*)(base + L.def_opac) : const_cast<float*>(gd.opacity_logits);
+    defs[f].sh = mh->w_c ? (float*)(base + L.def_sh) : const_cast<float*>(gd.sh);
     imgs[f] = (float*)(d + L.images + (size_t)f * L.per_img);
   }
   // Deform all frames in one launch (the spatial-plane work is shared across times), then render in

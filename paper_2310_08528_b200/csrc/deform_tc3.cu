@@ -95,8 +95,13 @@ __device__ __forceinline__ float4 lerp_line(const float* line, int R, float u, i
   return make_float4(wa * a.x + fa * b.x, wa * a.y + fa * b.y, wa * a.z + fa * b.z, wa * a.w + fa * b.w);
 }
 
-template <int WIDTH>
+// Head outputs (transposed weights [W][NOUTP], 12 per pass of the epilogue): 10 geometry outputs
+// (dX 3, dr 4, ds 3), then with the P:1232 decoders 3K colour outputs and 1 opacity output.
+constexpr int kNoutColor = 60;   // 10 + 48 + 1 = 59 at SH degree 3, padded to a multiple of 12
+
+template <int WIDTH, bool COLOR = false>
 struct Tc3Smem {
+  static constexpr int NOUTP = COLOR ? kNoutColor : 12;
   static constexpr int B_BYTES = 64 * WIDTH * 4;
   static constexpr int OFF_BHI = 0;
   static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
@@ -105,9 +110,9 @@ struct Tc3Smem {
   static constexpr int OFF_LINE = OFF_BLO + B_BYTES;
   static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [GMAX][128][4]
   static constexpr int OFF_WH = OFF_U + GMAX * kM * 16;
-  static constexpr int OFF_BD = OFF_WH + 12 * WIDTH * 4;   // head weights transposed [W][12]
+  static constexpr int OFF_BD = OFF_WH + NOUTP * WIDTH * 4;   // head weights transposed [W][NOUTP]
   static constexpr int OFF_BH = OFF_BD + WIDTH * 4;
-  static constexpr int OFF_WIN = OFF_BH + 16 * 4;               // int [FGS_MAX_SCALES][3][2]
+  static constexpr int OFF_WIN = OFF_BH + NOUTP * 4;            // int [FGS_MAX_SCALES][3][2]
   static constexpr int OFF_BAR = OFF_WIN + FGS_MAX_SCALES * 6 * 4;
   // barriers: 0 a_full, 1 a_free, 2-3 d_full, 4-5 d_free; then the TMEM base address
   static constexpr int TOTAL = OFF_BAR + 6 * 8 + 16;
@@ -153,9 +158,10 @@ __device__ __forceinline__ void prod_sync() {   // named barrier over the produc
   asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
 }
 
-template <int FEAT, int WIDTH>
+template <int FEAT, int WIDTH, bool COLOR>
 __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(const __grid_constant__ DeformBatch p) {
-  using SM = Tc3Smem<WIDTH>;
+  using SM = Tc3Smem<WIDTH, COLOR>;
+  constexpr int NOUTP = SM::NOUTP;
   using RL = Roles<FEAT>;
   constexpr int kThreads = RL::THREADS, kProdWarps = RL::PROD_WARPS, kProdThreads = RL::PROD_THREADS;
   constexpr int kMmaWarp = RL::MMA_WARP;
@@ -196,15 +202,28 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     *reinterpret_cast<float*>(smem + SM::OFF_BHI + o) = hi;
     *reinterpret_cast<float*>(smem + SM::OFF_BLO + o) = lo;
   }
-  for (int i = tid; i < 12 * WIDTH; i += kThreads) {
-    const int c = i / 12, o = i - 12 * c;          // WhT[c][o] = head output o, hidden column c
-    Wh[i] = o < 3 ? p.w_x[o * WIDTH + c] : o < 7 ? p.w_r[(o - 3) * WIDTH + c]
-          : o < 10 ? p.w_s[(o - 7) * WIDTH + c] : 0.f;
+  const int n_c = COLOR ? p.n_c : 0;                 // colour outputs (0 without phi_C)
+  const int n_out = 10 + n_c + ((COLOR && p.w_a) ? 1 : 0);
+  for (int i = tid; i < NOUTP * WIDTH; i += kThreads) {
+    const int c = i / NOUTP, o = i - NOUTP * c;    // WhT[c][o] = head output o, hidden column c
+    float w = 0.f;
+    if (o < 3) w = p.w_x[o * WIDTH + c];
+    else if (o < 7) w = p.w_r[(o - 3) * WIDTH + c];
+    else if (o < 10) w = p.w_s[(o - 7) * WIDTH + c];
+    else if (o < 10 + n_c) w = p.w_c[(o - 10) * WIDTH + c];
+    else if (o < n_out) w = p.w_a[c];
+    Wh[i] = w;
+  }
+  for (int o = tid; o < NOUTP; o += kThreads) {
+    float bb = 0.f;
+    if (o < 3) bb = p.b_x[o];
+    else if (o < 7) bb = p.b_r[o - 3];
+    else if (o < 10) bb = p.b_s[o - 7];
+    else if (o < 10 + n_c) bb = p.b_c[o - 10];
+    else if (o < n_out) bb = p.b_a[0];
+    bh[o] = bb;
   }
   for (int i = tid; i < WIDTH; i += kThreads) bd[i] = p.b_d[i];
-  if (tid < 3) bh[tid] = p.b_x[tid];
-  if (tid < 4) bh[3 + tid] = p.b_r[tid];
-  if (tid < 3) bh[7 + tid] = p.b_s[tid];
   if (tid == 0) {
     tc::mbar_init(a_full, kProdWarps);
     tc::mbar_init(a_free, 1);
@@ -429,34 +448,53 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           const uint32_t buf = it & 1u;
           tc::mbar_wait(d_full + buf, (it >> 1) & 1u);
           tc::fence_after_sync();
-          float2 acc[5];
+          // head outputs in passes of 12 over the hidden columns (one pass without the P:1232
+          // decoders); the geometry outputs (pass 0) are kept, the colour / opacity ones stored
+          float ho[12];
+          const int npass = COLOR ? (n_out + 11) / 12 : 1;
+          for (int pass = 0; pass < npass; ++pass) {
+            float2 acc[6];
 #pragma unroll
-          for (int o = 0; o < 5; ++o) acc[o] = make_float2(0.f, 0.f);
+            for (int o = 0; o < 6; ++o) acc[o] = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int c0 = 0; c0 < WIDTH; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(lane_base + buf * DW + (uint32_t)c0, v);
-            if (c0 + 16 >= WIDTH) {   // all of D read: hand the buffer back to the MMA issuer
-              tc::fence_before_sync();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(d_free + buf);
+            for (int c0 = 0; c0 < WIDTH; c0 += 16) {
+              float v[16];
+              tc::tmem_ld16(lane_base + buf * DW + (uint32_t)c0, v);
+              if (pass == npass - 1 && c0 + 16 >= WIDTH) {   // all of D read: hand the buffer back
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(d_free + buf);
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
+                const float4* w4 = reinterpret_cast<const float4*>(Wh + (c0 + i) * NOUTP + 12 * pass);
+                const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+                const float2 fd2 = make_float2(fd, fd);
+                acc[0] = ffma2(fd2, make_float2(wa.x, wa.y), acc[0]);
+                acc[1] = ffma2(fd2, make_float2(wa.z, wa.w), acc[1]);
+                acc[2] = ffma2(fd2, make_float2(wb.x, wb.y), acc[2]);
+                acc[3] = ffma2(fd2, make_float2(wb.z, wb.w), acc[3]);
+                acc[4] = ffma2(fd2, make_float2(wc.x, wc.y), acc[4]);
+                if (COLOR) acc[5] = ffma2(fd2, make_float2(wc.z, wc.w), acc[5]);
+              }
             }
+            if (pass == 0) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
-              const float4* w4 = reinterpret_cast<const float4*>(Wh + (c0 + i) * 12);
-              const float4 wa = w4[0], wb = w4[1], wc = w4[2];
-              const float2 fd2 = make_float2(fd, fd);
-              acc[0] = ffma2(fd2, make_float2(wa.x, wa.y), acc[0]);
-              acc[1] = ffma2(fd2, make_float2(wa.z, wa.w), acc[1]);
-              acc[2] = ffma2(fd2, make_float2(wb.x, wb.y), acc[2]);
-              acc[3] = ffma2(fd2, make_float2(wb.z, wb.w), acc[3]);
-              acc[4] = ffma2(fd2, make_float2(wc.x, wc.y), acc[4]);
+              for (int o = 0; o < 6; ++o) { ho[2 * o] = acc[o].x; ho[2 * o + 1] = acc[o].y; }
+            }
+            if (COLOR && valid) {
+#pragma unroll
+              for (int j = 0; j < 12; ++j) {
+                const int o = 12 * pass + j;
+                const float a = (j & 1) ? acc[j >> 1].y : acc[j >> 1].x;
+                if (o >= 10 && o < 10 + n_c)
+                  p.out_sh[f][g * n_c + (o - 10)] = p.sh_in[g * n_c + (o - 10)] + (a + bh[o]);
+                else if (o == 10 + n_c && o < n_out)
+                  p.out_opacity[f][g] = p.opac_in[g] + (a + bh[o]);
+              }
             }
           }
-          float ho[10];
-#pragma unroll
-          for (int o = 0; o < 5; ++o) { ho[2 * o] = acc[o].x; ho[2 * o + 1] = acc[o].y; }
           if (valid) {
 #pragma unroll
             for (int o = 0; o < 10; ++o) ho[o] = cx[o] + (ho[o] + bh[o]);
@@ -479,10 +517,10 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   }
 }
 
-template <int FEAT, int WIDTH>
+template <int FEAT, int WIDTH, bool COLOR>
 cudaError_t launch_tc3_t(const DeformBatch& p, cudaStream_t s) {
-  using SM = Tc3Smem<WIDTH>;
-  auto kern = deform_tc3_kernel<FEAT, WIDTH>;
+  using SM = Tc3Smem<WIDTH, COLOR>;
+  auto kern = deform_tc3_kernel<FEAT, WIDTH, COLOR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -514,12 +552,14 @@ bool deform_tc3_supported(const DeformBatch& p) {
 
 cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s) {
   if (p.end <= p.begin || p.n_t <= 0) return cudaSuccess;
-#define FGS_DISPATCH_W(FEAT)                          \
-  switch (p.width) {                                  \
-    case 32: return launch_tc3_t<FEAT, 32>(p, s);     \
-    case 64: return launch_tc3_t<FEAT, 64>(p, s);     \
-    case 128: return launch_tc3_t<FEAT, 128>(p, s);   \
-    default: return cudaErrorInvalidValue;            \
+  const bool color = p.w_c || p.w_a;
+  if (p.n_c + 11 > kNoutColor) return cudaErrorInvalidValue;
+#define FGS_DISPATCH_W(FEAT)                                                                        \
+  switch (p.width) {                                                                                \
+    case 32: return color ? launch_tc3_t<FEAT, 32, true>(p, s) : launch_tc3_t<FEAT, 32, false>(p, s);    \
+    case 64: return color ? launch_tc3_t<FEAT, 64, true>(p, s) : launch_tc3_t<FEAT, 64, false>(p, s);    \
+    case 128: return color ? launch_tc3_t<FEAT, 128, true>(p, s) : launch_tc3_t<FEAT, 128, false>(p, s); \
+    default: return cudaErrorInvalidValue;                                                          \
   }
   switch (p.feat) {
     case 8: FGS_DISPATCH_W(8)

@@ -79,10 +79,16 @@ struct DeformBatch {
   const float* planes[FGS_MAX_SCALES][FGS_PLANES];
   int in_dim, width;
   const float *w_d, *b_d, *w_x, *b_x, *w_r, *b_r, *w_s, *b_s;
+  const float *w_c, *b_c, *w_a, *b_a;   // optional colour / opacity decoders
+  int n_c;                              // 3K when phi_C is present, else 0
+  const float* sh_in;                   // canonical SH [n][K][3] and opacity logits [n]
+  const float* opac_in;
   float t[kMaxFrames];
   float* out_means[kMaxFrames];
   float* out_log_scales[kMaxFrames];
   float* out_quats[kMaxFrames];
+  float* out_sh[kMaxFrames];            // written when phi_C is present
+  float* out_opacity[kMaxFrames];       // written when phi_alpha is present
 };
 
 // Kernel launchers (return cudaError_t of the launch).

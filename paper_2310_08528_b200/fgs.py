@@ -38,9 +38,11 @@ class fgs_hexplanes(ctypes.Structure):
                 ("planes", (c_void_p * PLANES) * MAX_SCALES)]
 
 
+MLP_ARRAYS = ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s", "w_c", "b_c", "w_a", "b_a")
+
+
 class fgs_mlp(ctypes.Structure):
-    _fields_ = [("in_dim", c_int32), ("width", c_int32)] + [
-        (k, c_void_p) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")]
+    _fields_ = [("in_dim", c_int32), ("width", c_int32)] + [(k, c_void_p) for k in MLP_ARRAYS]
 
 
 class fgs_deformed(ctypes.Structure):
@@ -282,7 +284,7 @@ class HostScene:
         hp.bmax[:] = [float(v) for v in f.bmax]
         self.field = hp
         m = scene.mlp
-        self.mlp_t = {k: T(getattr(m, k)) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")}
+        self.mlp_t = {k: T(getattr(m, k)) for k in MLP_ARRAYS if getattr(m, k, None) is not None}
         mm = fgs_mlp()
         mm.in_dim, mm.width = m.in_dim, m.width
         for k, v in self.mlp_t.items():
@@ -316,7 +318,9 @@ class DeviceScene:
         f = scene.field
         self.planes = [[T(P) for P in ps] for ps in f.planes]
         m = scene.mlp
-        self.mlp_t = {k: T(getattr(m, k)) for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s")}
+        self.mlp_t = {k: T(getattr(m, k)) for k in MLP_ARRAYS if getattr(m, k, None) is not None}
+        self.has_c = "w_c" in self.mlp_t
+        self.has_a = "w_a" in self.mlp_t
         self.g = fgs_gaussians(self.n, self.sh_degree, self.means.data_ptr(), self.log_scales.data_ptr(),
                                self.quats.data_ptr(), self.opacity_logits.data_ptr(), self.sh.data_ptr())
         hp = fgs_hexplanes()
@@ -345,14 +349,22 @@ class DeviceScene:
             S = torch.empty((self.n, 3), dtype=torch.float32, device=self.device)
             Q = torch.empty((self.n, 4), dtype=torch.float32, device=self.device)
             tens.append({"means": X, "log_scales": S, "quats": Q})
-            d = self.deformed_struct(X, S, Q)
-            d._keep = (X, S, Q)        # the struct owns its device buffers (raw pointers inside)
+            # with the P:1232 decoders the deformed opacity / SH are per-frame outputs too
+            O = torch.empty_like(self.opacity_logits) if self.has_a else None
+            C = torch.empty_like(self.sh) if self.has_c else None
+            if O is not None:
+                tens[-1]["opacity_logits"] = O
+            if C is not None:
+                tens[-1]["sh"] = C
+            d = self.deformed_struct(X, S, Q, O, C)
+            d._keep = (X, S, Q, O, C)  # the struct owns its device buffers (raw pointers inside)
             outs.append(d)
         return outs, tens
 
-    def deformed_struct(self, means, log_scales, quats) -> fgs_deformed:
+    def deformed_struct(self, means, log_scales, quats, opacity=None, sh=None) -> fgs_deformed:
         return fgs_deformed(self.n, self.sh_degree, means.data_ptr(), log_scales.data_ptr(), quats.data_ptr(),
-                            self.opacity_logits.data_ptr(), self.sh.data_ptr())
+                            (self.opacity_logits if opacity is None else opacity).data_ptr(),
+                            (self.sh if sh is None else sh).data_ptr())
 
     def canonical_struct(self) -> fgs_deformed:
         """G itself as an fgs_deformed (render the undeformed scene, e.g. the warm-up / static case)."""

@@ -75,6 +75,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(fgs.fgs_camera) == 4 * (9 + 3 + 4 + 2 + 3)
     assert fgs.fgs_hexplanes.planes.offset == 56
     assert ctypes.sizeof(fgs.fgs_render_aux) == 13 * 8
+    assert ctypes.sizeof(fgs.fgs_mlp) == 8 + 12 * 8
 
 
 def test_tuning_knob_host_only(L):

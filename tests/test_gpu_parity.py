@@ -312,3 +312,49 @@ def test_composition_of_two_models():
     ref = OR.render_ref(g, opn, shn, 0, cam)
     pix = compare_pixels(img.cpu().numpy(), ref["image"], ref["flagged"])
     assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, pix
+
+
+@pytest.mark.parametrize("heads", ["both", "colour", "opacity"])
+def test_colour_opacity_decoders(heads):
+    """P:1232 variant: phi_C / phi_alpha deform the SH coefficients and the opacity logit per frame;
+    deformed SH / opacity match the oracle (<= 1e-4), and the render of the deformed set matches the
+    oracle render of the GPU's fp32 G' (pixels, integer work); fgs_frames gives the same images."""
+    import torch
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = make_scene("dnerf", n=12_007, width=120, height=96, n_frames=3)
+    s = with_heads(s, 0.5, seed=2, bias_sigma=0.1)
+    s = with_colour_heads(s, 0.2, 0.3, seed=3, colour=heads in ("both", "colour"),
+                          opacity=heads in ("both", "opacity"))
+    ds = _ds(s)
+    t = float(s.times[1])
+    dstruct, g, _ = gpu_deform(ds, t)
+    ref = oracle.deform_ref(s, t)
+    assert set(ref) == set(g)
+    for k in ref:
+        assert np.abs(g[k].astype(np.float64) - ref[k]).max() <= DEFORM_TOL, k
+    cam = s.cameras[1]
+    out = gpu_render_debug(ds, cam, dstruct)
+    opac = g.get("opacity_logits", s.opacity_logits)
+    sh = g.get("sh", s.sh)
+    oref = OR.render_ref(g, opac, sh, s.sh_degree, cam)
+    ints = compare_integer_work(out, oref["pre"], (oref["tiles"], oref["gids"], oref["ranges"]))
+    assert ints["rect"] == 0 and ints["tile_lists"] == 0, ints
+    pix = compare_pixels(out["image"], oref["image"], oref["flagged"])
+    assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, pix
+    # whole frames through fgs_frames == per-frame deform + render
+    scratch, _ = ds.alloc_deformed(3)
+    imgs = [torch.empty((3, 96, 120), device="cuda") for _ in range(3)]
+    ws = ds.alloc_workspace(3)
+    fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, scratch, imgs, ws)
+    assert np.array_equal(imgs[1].cpu().numpy(), out["image"])
+
+
+def test_colour_decoder_rejects_canonical_alias():
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = with_colour_heads(make_scene("tiny", n=500), 0.1, 0.1)
+    ds = _ds(s)
+    outs, tens = ds.alloc_deformed(1)
+    bad = ds.deformed_struct(tens[0]["means"], tens[0]["log_scales"], tens[0]["quats"])   # canonical SH
+    with pytest.raises(fgs.FgsError) as e:
+        fgs.fgs_deform(ds.g, ds.field, ds.mlp, 0.5, bad)
+    assert e.value.code == fgs.FGS_E_INVALID
