@@ -358,3 +358,31 @@ def test_colour_decoder_rejects_canonical_alias():
     with pytest.raises(fgs.FgsError) as e:
         fgs.fgs_deform(ds.g, ds.field, ds.mlp, 0.5, bad)
     assert e.value.code == fgs.FGS_E_INVALID
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_sh_degrees_1_and_2(deg):
+    """preprocess_kernel<1>/<2> (the configs use degrees 0 and 3): SH truncated to degree `deg`."""
+    from dataclasses import replace
+    s = make_scene("dnerf", n=6_000, width=96, height=80, n_frames=1)
+    K = (deg + 1) ** 2
+    s = replace(s, sh=np.ascontiguousarray(s.sh[:, :K, :]), sh_degree=deg)
+    _render_parity(s)
+
+
+def test_screen_covering_and_near_plane_gaussians():
+    """Edge geometry: a few huge Gaussians whose rects cover every tile (the CTA aggregation box exceeds
+    its shared histogram, long lists), Gaussians straddling and behind the near plane, t at 0 and 1."""
+    from dataclasses import replace
+    s = make_scene("tiny", n=1500, width=200, height=150)
+    ls = s.log_scales.copy()
+    ls[:6] = np.float32(0.5)                          # ~1.6 world units: covers the whole image
+    means = s.means.copy()
+    eye_z = 4.0                                       # tiny camera at (0,0,4) looking at the origin
+    means[6:12, 2] = np.float32(eye_z - 0.2)          # at the near plane (z_cam ~ 0.2)
+    means[12:18, 2] = np.float32(eye_z + 0.5)         # behind the camera
+    s = replace(s, log_scales=ls, means=means)
+    s = with_heads(s, 0.0)
+    for t in (0.0, 1.0):
+        s.times[0] = np.float32(t)
+        _render_parity(s)
