@@ -636,11 +636,19 @@ struct PixelState {
 
 // Eq. 4 for one pixel and one Gaussian; e = p2 + log2(o) with p2 = power * log2(e) (R9: skip if
 // power > 0 or alpha < 1/255; stop, without adding it, when T (1 - alpha) < 1e-4).
+//  * power > 0 cannot happen for a kept Gaussian: det > 0 and a > 0 make the conic positive definite,
+//    so power <= 0 exactly (p2 > 0 could only come from fp32 rounding at power ~ 0, where the fp64
+//    oracle includes the Gaussian too) — no test.
+//  * alpha >= 1/255 is decided on the exponent, e >= log2(1/255) (min(0.99, .) cannot take alpha
+//    below 1/255), which takes the decision off the ex2 latency; the two forms differ only within the
+//    ex2.approx error of the threshold, inside the parity band of reading P1.
+constexpr float kLog2AlphaMin = -7.9943534368588578f;   // log2(1/255)
 template <bool DBG>
 __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, float r, float g, float bch,
                                            uint32_t pos) {
+  (void)lo;
   const float alpha = fminf(kAlphaMax, ex2_approx(e));
-  const bool ok = !s.done && !(e > lo) && alpha >= kAlphaMin;
+  const bool ok = !s.done && e >= kLog2AlphaMin;
   const float test_T = fmaf(-alpha, s.T, s.T);
   const bool stop = ok && test_T < kTMin;
   if (ok && !stop) {
