@@ -718,8 +718,9 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
   const int L = (int)(rg.y - rg.x);
   const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
-  __shared__ float4 s0[256], s1[256];
-  __shared__ float2 s2[256];
+  // staged records, one 48-B struct per list entry so one address serves all three loads
+  struct __align__(16) SRec { float4 a, q; float2 c; float2 pad; };
+  __shared__ SRec srec[256];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   const float lx = (float)lxi, ly = (float)lyi;
   const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, bym = (float)(by0 + 3),
@@ -738,9 +739,10 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
         const float4 c = rec[3 * g + 2];
         a.x = (a.x - tx0) + c.y;      // tile-relative mean: exact hi difference + lo part
         a.y = (a.y - ty0) + c.z;
-        s0[threadIdx.x + kBlendThreads * k] = a;
-        s1[threadIdx.x + kBlendThreads * k] = rec[3 * g + 1];
-        s2[threadIdx.x + kBlendThreads * k] = make_float2(c.x, c.w);
+        SRec& d = srec[threadIdx.x + kBlendThreads * k];
+        d.a = a;
+        d.q = rec[3 * g + 1];
+        d.c = make_float2(c.x, c.w);
       }
     }
     __syncthreads();
@@ -751,8 +753,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
       const int jt = c0 + lane;
       bool needA = false, needB = false;
       if (jt < cnt) {
-        const float4 a = s0[jt];
-        const float qa = -a.z, qb = -a.w, qc = -s1[jt].x, thr = s2[jt].y;
+        const float4 a = srec[jt].a;
+        const float qa = -a.z, qb = -a.w, qc = -srec[jt].q.x, thr = srec[jt].c.y;
         const float xl = bxl - a.x, xh = bxh - a.x;
         halfboxes_may_reach(qa, qb, qc, thr, xl, xh, byl - a.y, bym - a.y, byn - a.y, byh - a.y, needA, needB);
         needA = needA && liveA;
@@ -765,8 +767,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
         const int bit = __ffs(m) - 1;
         m &= m - 1;
         const int j = c0 + bit;
-        const float4 a = s0[j], q = s1[j];
-        const float bch = s2[j].x;
+        const float4 a = srec[j].a, q = srec[j].q;
+        const float bch = srec[j].c.x;
         const float dx = a.x - lx;
         const float bdx = a.w * dx;                              // b2 dx, shared by both pixels
         const float base = fmaf(a.z * dx, dx, q.y);              // a2 dx^2 + log2(o)
