@@ -89,7 +89,9 @@ class ShardedDeform:
         (wait() them, or let the NCCL stream ordering do it, before rendering the slot)."""
         import torch.distributed as dist
         works = []
-        if self.world == 1 or self.rows == 0:
+        # world size 1 still goes through the collective when a process group exists (the same code
+        # path as N > 1; NCCL copies in place), so the single-GPU bench exercises it
+        if self.rows == 0 or not (dist.is_available() and dist.is_initialized()):
             return works
         c0 = self.rank * self.chunk
         for k, _ in DEFORMED_FIELDS:
