@@ -134,7 +134,7 @@ __device__ __forceinline__ bool agg_fits(const AggBox& r) {
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__ RenderBatch b) {
+__global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i0 < b.n;
