@@ -212,8 +212,12 @@ int64_t fgs_launch_count(void);
  * the blend kernel's shared memory; longer lists by the global-memory sort (FGS_STAGE_TILE_SORT).
  * Range [1, 1024], default 1024.  Results are identical for every value (tests lower it to exercise
  * the long-list path).  fgs_set_tuning returns FGS_E_INVALID for an unknown key or a value out of
- * range; fgs_get_tuning returns -1 for an unknown key. */
-enum { FGS_TUNE_TILE_SORT_CAP = 0 };
+ * range; fgs_get_tuning returns -1 for an unknown key.
+ * FGS_TUNE_DEFORM_KERNEL: 0 = automatic choice (default), 1 = SIMT fp32 (deform.cu), 2 = tcgen05 v1
+ * (deform_tc.cu), 3 = TMEM-resident v2 (deform_tc2.cu), 4 = warp-specialised v3 (deform_tc3.cu); a kernel
+ * that cannot run a given field falls back to the automatic choice.  All give the same results within
+ * the 1e-4 deformation tolerance (tests compare every kernel with the oracle). */
+enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_DEFORM_KERNEL = 1 };
 int fgs_set_tuning(int32_t key, int64_t value);
 int64_t fgs_get_tuning(int32_t key);
 

@@ -109,18 +109,23 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.sh_in = g->sh; p.opac_in = g->opacity_logits;
 }
 
-// FGS_DEFORM = simt | tc1 | tc2 | tc3 forces a deform kernel (A/B comparison).  Default: tc3
-// (warp-specialised pipeline) when the field fits its line buffer and TMEM plan, else tc2, else tc1.
+// Deform kernel selection: FGS_TUNE_DEFORM_KERNEL (or env FGS_DEFORM = simt | tc1 | tc2 | tc3 at load)
+// forces one (A/B comparison and cross-checks); 0 = auto: tc3 (warp-specialised pipeline) when the
+// field fits its line buffer and TMEM plan, else tc2, else tc1.  A forced kernel that cannot run the
+// field falls back to auto.
+std::atomic<int> g_deform_kernel{-1};
 int deform_choice() {
-  static const int c = [] {
-    const char* e = getenv("FGS_DEFORM");
-    if (!e) return 0;
-    if (strcmp(e, "simt") == 0) return 1;
-    if (strcmp(e, "tc1") == 0) return 2;
-    if (strcmp(e, "tc2") == 0) return 3;
-    if (strcmp(e, "tc3") == 0) return 4;
-    return 0;
-  }();
+  int c = g_deform_kernel.load(std::memory_order_relaxed);
+  if (c < 0) {
+    c = 0;
+    if (const char* e = getenv("FGS_DEFORM")) {
+      if (strcmp(e, "simt") == 0) c = 1;
+      if (strcmp(e, "tc1") == 0) c = 2;
+      if (strcmp(e, "tc2") == 0) c = 3;
+      if (strcmp(e, "tc3") == 0) c = 4;
+    }
+    g_deform_kernel.store(c);
+  }
   return c;
 }
 
@@ -129,12 +134,12 @@ cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
   switch (deform_choice()) {
     case 1: return launch_deform(p, s);
     case 2: return launch_deform_tc(p, s);
-    case 3: return launch_deform_tc2(p, s);
-    case 4: return launch_deform_tc3(p, s);
-    default:
-      if (deform_tc3_supported(p)) return launch_deform_tc3(p, s);
-      return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
+    case 3: if (deform_tc2_supported(p)) return launch_deform_tc2(p, s); break;
+    case 4: if (deform_tc3_supported(p)) return launch_deform_tc3(p, s); break;
+    default: break;
   }
+  if (deform_tc3_supported(p)) return launch_deform_tc3(p, s);
+  return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
 }
 
 int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
@@ -474,13 +479,20 @@ int fgs_set_tuning(int32_t key, int64_t value) {
       FGS_CHECK(value >= 1 && value <= kBlendSortMax, "tile sort cap must be in [1, 1024]");
       g_tile_sort_cap.store((int)value);
       return FGS_OK;
+    case FGS_TUNE_DEFORM_KERNEL:
+      FGS_CHECK(value >= 0 && value <= 4, "deform kernel must be 0 (auto) .. 4");
+      deform_choice();                 // settle the env default first
+      g_deform_kernel.store((int)value);
+      return FGS_OK;
     default:
       return fail(FGS_E_INVALID, "unknown tuning key");
   }
 }
 
 int64_t fgs_get_tuning(int32_t key) {
-  return key == FGS_TUNE_TILE_SORT_CAP ? (int64_t)tile_sort_cap() : -1;
+  if (key == FGS_TUNE_TILE_SORT_CAP) return tile_sort_cap();
+  if (key == FGS_TUNE_DEFORM_KERNEL) return deform_choice();
+  return -1;
 }
 
 // ---- end to end with host buffers -------------------------------------------------------------

@@ -69,6 +69,8 @@ EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_batch", "fgs_render_wor
            "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version")
 STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend")
 FGS_TUNE_TILE_SORT_CAP = 0
+FGS_TUNE_DEFORM_KERNEL = 1
+DEFORM_KERNELS = {"auto": 0, "simt": 1, "tc1": 2, "tc2": 3, "tc3": 4}
 
 
 def lib():

@@ -88,6 +88,11 @@ def test_tuning_knob_host_only(L):
     assert L.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 4096) == fgs.FGS_E_INVALID
     assert L.fgs_set_tuning(99, 1) == fgs.FGS_E_INVALID
     assert fgs.fgs_get_tuning(99) == -1
+    k0 = fgs.fgs_get_tuning(fgs.FGS_TUNE_DEFORM_KERNEL)
+    fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, 2)
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_DEFORM_KERNEL) == 2
+    fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, k0)
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, 9) == fgs.FGS_E_INVALID
 
 
 def test_stage_names_match_header():

@@ -386,3 +386,25 @@ def test_screen_covering_and_near_plane_gaussians():
     for t in (0.0, 1.0):
         s.times[0] = np.float32(t)
         _render_parity(s)
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tc1", "tc2", "tc3"])
+@pytest.mark.parametrize("variant", ["tiny", "dnerf_stress", "hyper"])
+def test_every_deform_kernel_matches_oracle(kernel, variant):
+    """All four deformation kernels (SIMT fp32 v0, tcgen05 v1/v2/v3) against the oracle, incl. the
+    3xTF32 stress heads, ragged tails and phi_d widths 32/64/128."""
+    if variant == "tiny":
+        s = make_scene("tiny", n=2011)
+    elif variant == "dnerf_stress":
+        s = with_heads(make_scene("dnerf", n=7_777, n_frames=2), 1.0, seed=7, bias_sigma=0.5)
+    else:
+        s = make_scene("hypernerf", n=3_001, n_frames=2)
+    ds = _ds(s)
+    old = fgs.fgs_get_tuning(fgs.FGS_TUNE_DEFORM_KERNEL)
+    fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, fgs.DEFORM_KERNELS[kernel])
+    try:
+        for t in (0.0, float(s.times[0]), 1.0):
+            _, g, _ = gpu_deform(ds, t)
+            assert _deform_err(s, g, t) <= DEFORM_TOL, (kernel, variant, t)
+    finally:
+        fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, old)
