@@ -32,7 +32,10 @@ namespace {
 constexpr int kM = 128;
 constexpr int kTmemCols = 512;
 constexpr int kMaxG = 16;
-constexpr int kMaxLineFloats = 3 * 192 * 32;   // 72 KB: 3 planes x (64 + 128) knots x h 32
+// Shared buffer of the per-frame time lines: only the knot window each axis of a group touches is
+// staged, compactly (Morton-ordered models: ~1/6 of the axis per group at D); a group whose windows do
+// not fit reads the temporal planes from L2 instead (same arithmetic, bit-identical results).
+constexpr int kLineBufFloats = 16384;          // 64 KB
 constexpr int kEpiWarps = 4;
 // Producer warps per TMEM lane quarter (each takes FEAT / NP features of every scale).
 template <int FEAT>
@@ -83,16 +86,37 @@ __device__ __forceinline__ int knot0(float u, int R) {
   return min((int)floorf(u * (float)(R - 1)), R - 2);
 }
 
-// linear interpolation of a line [R][FEAT] (smem) at u in [0,1], channel quad c4
+// (1 - w) a + w b in a fixed evaluation order (the staged and the L2 paths must agree bit for bit)
+__device__ __forceinline__ float4 lerp4(float4 a, float4 b, float w) {
+  const float wa = 1.f - w;
+  return make_float4(fmaf(w, b.x, __fmul_rn(wa, a.x)), fmaf(w, b.y, __fmul_rn(wa, a.y)),
+                     fmaf(w, b.z, __fmul_rn(wa, a.z)), fmaf(w, b.w, __fmul_rn(wa, a.w)));
+}
+
+// linear interpolation at u in [0,1], channel quad c4, of a line whose knot i sits at float offset
+// off + i FEAT of `line` (smem; only the group's window of knots is present)
 template <int FEAT>
-__device__ __forceinline__ float4 lerp_line(const float* line, int R, float u, int c4) {
+__device__ __forceinline__ float4 lerp_line(const float* line, int off, int R, float u, int c4) {
   const float g = u * (float)(R - 1);
   const int i0 = min((int)floorf(g), R - 2);
   const float fa = g - (float)i0;
-  const float4 a = reinterpret_cast<const float4*>(line + i0 * FEAT)[swz<FEAT>(i0, c4)];
-  const float4 b = reinterpret_cast<const float4*>(line + (i0 + 1) * FEAT)[swz<FEAT>(i0 + 1, c4)];
-  const float wa = 1.f - fa;
-  return make_float4(wa * a.x + fa * b.x, wa * a.y + fa * b.y, wa * a.z + fa * b.z, wa * a.w + fa * b.w);
+  const float4 a = reinterpret_cast<const float4*>(line + off + i0 * FEAT)[swz<FEAT>(i0, c4)];
+  const float4 b = reinterpret_cast<const float4*>(line + off + (i0 + 1) * FEAT)[swz<FEAT>(i0 + 1, c4)];
+  return lerp4(a, b, fa);
+}
+
+// the same value straight from the temporal plane [t_res][R][FEAT] in global memory (L2): time lerp of
+// the two rows at knots i0, i0+1, then the lerp in u — the staged path's operations in its order
+template <int FEAT>
+__device__ __noinline__ float4 lerp_plane(const float* __restrict__ P, int R, int j0, float ft, float u, int c4) {
+  const float g = u * (float)(R - 1);
+  const int i0 = min((int)floorf(g), R - 2);
+  const float fa = g - (float)i0;
+  const float4* r0 = reinterpret_cast<const float4*>(P + ((size_t)j0 * R + i0) * FEAT) + c4;
+  const float4* r1 = reinterpret_cast<const float4*>(P + ((size_t)(j0 + 1) * R + i0) * FEAT) + c4;
+  const float4 a = lerp4(__ldg(r0), __ldg(r1), ft);
+  const float4 b = lerp4(__ldg(r0 + FEAT / 4), __ldg(r1 + FEAT / 4), ft);
+  return lerp4(a, b, fa);
 }
 
 // Head outputs (transposed weights [W][NOUTP], 12 per pass of the epilogue): 10 geometry outputs
@@ -108,12 +132,13 @@ struct Tc3Smem {
   // tiles per group the TMEM plan allows for phi_d width WIDTH at in_dim 64 (more for smaller in_dim)
   static constexpr int GMAX = WIDTH >= 128 ? 2 : (WIDTH >= 64 ? 4 : kMaxG);
   static constexpr int OFF_LINE = OFF_BLO + B_BYTES;
-  static constexpr int OFF_U = OFF_LINE + kMaxLineFloats * 4;   // [GMAX][128][4]
+  static constexpr int OFF_U = OFF_LINE + kLineBufFloats * 4;   // [GMAX][128][4]
   static constexpr int OFF_WH = OFF_U + GMAX * kM * 16;
   static constexpr int OFF_BD = OFF_WH + NOUTP * WIDTH * 4;   // head weights transposed [W][NOUTP]
   static constexpr int OFF_BH = OFF_BD + WIDTH * 4;
   static constexpr int OFF_WIN = OFF_BH + NOUTP * 4;            // int [FGS_MAX_SCALES][3][2]
-  static constexpr int OFF_BAR = OFF_WIN + FGS_MAX_SCALES * 6 * 4;
+  static constexpr int OFF_SEG = OFF_WIN + FGS_MAX_SCALES * 6 * 4;   // int [13]: window offsets + fits
+  static constexpr int OFF_BAR = OFF_SEG + 16 * 4;
   // barriers: 0 a_full, 1 a_free, 2-3 d_full, 4-5 d_free; then the TMEM base address
   static constexpr int TOTAL = OFF_BAR + 6 * 8 + 16;
 };
@@ -172,6 +197,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   float* bd = reinterpret_cast<float*>(smem + SM::OFF_BD);
   float* bh = reinterpret_cast<float*>(smem + SM::OFF_BH);
   int* win = reinterpret_cast<int*>(smem + SM::OFF_WIN);
+  int* segoff = reinterpret_cast<int*>(smem + SM::OFF_SEG);   // [3 NS] float offset of knot 0; [15] fits
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
   uint64_t* a_full = bar + 0;
   uint64_t* a_free = bar + 1;
@@ -238,15 +264,6 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     const int quarter = warp & 3, part = warp >> 2;   // part: which FT-feature slice of each scale
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    int line_off[MAXS];
-    {
-      int o = 0;
-#pragma unroll
-      for (int l = 0; l < MAXS; ++l) {
-        line_off[l] = o;
-        if (l < NS) o += 3 * p.res[l] * FEAT;
-      }
-    }
     if (part == 0) {   // zero the K padding columns of A once (never written afterwards)
       for (int k = IN; k < KP; k += 4) {
         const float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -310,35 +327,46 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         }
       }
       tc::tmem_st_wait();
+      // ---- compact layout of the group's knot windows in the line buffer (or the L2 path) ----
+      prod_sync<kProdThreads>();     // windows complete
+      if (tid == 0) {
+        int o = 0;
+        for (int sg = 0; sg < 3 * NS; ++sg) {
+          const int lo = win[2 * sg], hi = win[2 * sg + 1];
+          segoff[sg] = o - lo * FEAT;                    // knot i of segment sg at o + (i - lo) FEAT
+          if (lo <= hi) o += (hi - lo + 1) * FEAT;
+        }
+        segoff[15] = o <= kLineBufFloats ? 1 : 0;
+      }
+      prod_sync<kProdThreads>();
+      const bool staged = segoff[15] != 0;
       for (int f = 0; f < p.n_t; ++f) {
         const float t = p.t[f];
+        const int Tn = p.t_res;
+        const float gt_ = t * (float)(Tn - 1);
+        const int j0 = min((int)floorf(gt_), Tn - 2);
+        const float ft = gt_ - (float)j0;
         // ---- stage the temporal lines at t over the group's knot windows (time lerp of 2 rows) ----
         prod_sync<kProdThreads>();   // U/win visible; previous frame's line readers done
-        {
-          const int Tn = p.t_res;
-          const float gt_ = t * (float)(Tn - 1);
-          const int j0 = min((int)floorf(gt_), Tn - 2);
-          const float ft = gt_ - (float)j0, wt = 1.f - ft;
+        if (staged) {
 #pragma unroll
           for (int l = 0; l < MAXS; ++l) {
             if (l >= NS) break;
             const int R = p.res[l];
             const int per_plane = R * (FEAT / 4);
-            float4* dst = reinterpret_cast<float4*>(line + line_off[l]);
 #pragma unroll
             for (int pl = 0; pl < 3; ++pl) {
-              const int lo = win[(l * 3 + pl) * 2], hi = win[(l * 3 + pl) * 2 + 1];
+              const int sg = l * 3 + pl;
+              const int lo = win[2 * sg], hi = win[2 * sg + 1];
               if (lo > hi) continue;
+              float4* dst = reinterpret_cast<float4*>(line + segoff[sg]);
               const float4* P0 = reinterpret_cast<const float4*>(p.planes[l][3 + pl]) + (size_t)j0 * per_plane;
               const float4* P1 = P0 + per_plane;
               const int n_items = (hi - lo + 1) * (FEAT / 4);
               for (int q = tid; q < n_items; q += kProdThreads) {
                 const int rem = lo * (FEAT / 4) + q;
-                const float4 a = __ldg(P0 + rem);
-                const float4 b = __ldg(P1 + rem);
                 const int i = rem / (FEAT / 4), c4 = rem - i * (FEAT / 4);
-                dst[pl * per_plane + i * (FEAT / 4) + swz<FEAT>(i, c4)] =
-                    make_float4(wt * a.x + ft * b.x, wt * a.y + ft * b.y, wt * a.z + ft * b.z, wt * a.w + ft * b.w);
+                dst[i * (FEAT / 4) + swz<FEAT>(i, c4)] = lerp4(__ldg(P0 + rem), __ldg(P1 + rem), ft);
               }
             }
           }
@@ -354,15 +382,28 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             const int R = p.res[l];
             float sv[FT];
             tmem_ld_n<FT>(lane_base + colS + gt * IN + l * FEAT + part * FT, sv);
-            const float* lx = line + line_off[l];
-            const float* ly = lx + R * FEAT;
-            const float* lz = ly + R * FEAT;
+            float4 tl[QT][3];
+            if (staged) {
+              const int o0 = segoff[3 * l + 0], o1 = segoff[3 * l + 1], o2 = segoff[3 * l + 2];
+#pragma unroll
+              for (int qq = 0; qq < QT; ++qq) {
+                const int c4 = part * QT + qq;
+                tl[qq][0] = lerp_line<FEAT>(line, o0, R, ux, c4);
+                tl[qq][1] = lerp_line<FEAT>(line, o1, R, uy, c4);
+                tl[qq][2] = lerp_line<FEAT>(line, o2, R, uz, c4);
+              }
+            } else {
+#pragma unroll
+              for (int qq = 0; qq < QT; ++qq) {
+                const int c4 = part * QT + qq;
+                tl[qq][0] = lerp_plane<FEAT>(p.planes[l][3], R, j0, ft, ux, c4);
+                tl[qq][1] = lerp_plane<FEAT>(p.planes[l][4], R, j0, ft, uy, c4);
+                tl[qq][2] = lerp_plane<FEAT>(p.planes[l][5], R, j0, ft, uz, c4);
+              }
+            }
 #pragma unroll
             for (int qq = 0; qq < QT; ++qq) {
-              const int c4 = part * QT + qq;
-              const float4 a = lerp_line<FEAT>(lx, R, ux, c4);
-              const float4 b = lerp_line<FEAT>(ly, R, uy, c4);
-              const float4 c = lerp_line<FEAT>(lz, R, uz, c4);
+              const float4 a = tl[qq][0], b = tl[qq][1], c = tl[qq][2];
               const float fh[4] = {sv[4 * qq + 0] * (a.x * b.x * c.x), sv[4 * qq + 1] * (a.y * b.y * c.y),
                                    sv[4 * qq + 2] * (a.z * b.z * c.z), sv[4 * qq + 3] * (a.w * b.w * c.w)};
 #pragma unroll
@@ -532,9 +573,6 @@ cudaError_t launch_tc3_t(const DeformBatch& p, cudaStream_t s) {
 bool deform_tc3_supported(const DeformBatch& p) {
   if (!(p.feat == 8 || p.feat == 16 || p.feat == 32)) return false;
   if (p.in_dim > 64) return false;
-  long lines = 0;
-  for (int l = 0; l < p.n_scales; ++l) lines += 3L * p.res[l] * p.feat;
-  if (lines > kMaxLineFloats) return false;
   const int DW = p.width < 32 ? 32 : p.width, KP = (p.in_dim + 7) & ~7;
   return kTmemCols - (2 * DW + 2 * KP) >= p.in_dim;
 }

@@ -408,3 +408,19 @@ def test_every_deform_kernel_matches_oracle(kernel, variant):
             assert _deform_err(s, g, t) <= DEFORM_TOL, (kernel, variant, t)
     finally:
         fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, old)
+
+
+def test_deform_l2_fallback_bit_identical_to_staged_lines():
+    """tc3 stages the time lines of a group's knot windows in shared memory; a group whose windows do not
+    fit (a model in draw order, not spatially sorted) reads the temporal planes from L2 instead.  Both
+    paths compute the same operations in the same order: the same Gaussians give bit-identical G'."""
+    from paper_2310_08528_b200.inputs import morton_order
+    sd = make_scene("dnerf", n=20_000, n_frames=2, order="draw")       # L2 path (windows span the axes)
+    sm = make_scene("dnerf", n=20_000, n_frames=2)                     # staged path (Morton order)
+    perm = morton_order(sd.means, sd.field.bmin, sd.field.bmax)
+    t = float(sd.times[1])
+    _, gd, _ = gpu_deform(_ds(sd), t)
+    _, gm, _ = gpu_deform(_ds(sm), t)
+    assert _deform_err(sd, gd, t) <= DEFORM_TOL
+    for k in gd:
+        assert np.array_equal(gd[k][perm], gm[k]), k
