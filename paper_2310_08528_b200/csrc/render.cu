@@ -698,22 +698,41 @@ __device__ __forceinline__ void halfboxes_may_reach(float qa, float qb, float qc
   nB = face_min(qa, qb, qc, kx, ky, ex, xl, xh, ylB, yhB) <= thr;
 }
 
+// NP pixels per lane: warp w of the tile's NW = 64/NP... warps owns a column block; lane l owns pixel
+// (x, y + 4k), k < NP, of that block (x = l & 7, y = l >> 3).  Sub-box k = rows [4k, 4k+4) of the block.
+constexpr int kBlendPix = 4;                         // pixels per lane
+constexpr int kBlendWarps = 256 / (32 * kBlendPix);  // warps per 16x16 tile (2)
+
+// All kBlendPix 8x4 sub-boxes of a warp's column at once (shared x-face and minimiser ratios).
+__device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
+                                                       float y0) {
+  const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
+  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+  uint32_t need = 0;
+#pragma unroll
+  for (int k = 0; k < kBlendPix; ++k) {
+    const float yl = y0 + 4.f * k, yh = yl + 3.f;
+    if (face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr) need |= 1u << k;
+  }
+  return need;
+}
+
 template <bool DBG>
-__global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_constant__ RenderBatch b) {
-  // One CTA (4 warps) per 16x16 tile.  Warp w owns the 8x8 pixel box ((w&1)*8, (w>>1)*8); lane l owns
-  // pixel A = (l&7, l>>3) of the box's upper 8x4 half and pixel B = A + (0,4) of the lower half.  The
-  // tile's list (sorted by (depth, gid)) is walked in batches of 256 records staged in smem; per 32
-  // Gaussians each lane tests one against the exact ellipse bound over both half-boxes, and the warp
-  // evaluates, in list order, each Gaussian on the half-boxes it can reach (warp-uniform branches).
+__global__ void __launch_bounds__(32 * kBlendWarps) blend_kernel(const __grid_constant__ RenderBatch b) {
+  // One CTA (kBlendWarps warps) per 16x16 tile.  Warp w owns the 8-wide column block x in [8w, 8w+8)
+  // of all 16 rows; lane l owns the kBlendPix pixels (8w + (l&7), (l>>3) + 4k).  The tile's list (sorted
+  // by (depth, gid)) is walked in batches of 256 records staged in smem; per 32 Gaussians each lane tests
+  // one against the exact ellipse bound over the warp's kBlendPix 8x4 sub-boxes, and the warp
+  // evaluates, in list order, each Gaussian on the sub-boxes it can reach (warp-uniform branches), so
+  // the per-Gaussian loads and dx terms are shared by up to kBlendPix pixels per lane.
+  constexpr int NT = 32 * kBlendWarps;
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % b.gx, ty = tile / b.gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int bx0 = (warp & 1) * 8, by0 = (warp >> 1) * 8;          // box origin, tile-relative
-  const int lxi = bx0 + (lane & 7), lyi = by0 + (lane >> 3);
-  const int pxi = tx * kTile + lxi, pyA = ty * kTile + lyi, pyB = pyA + 4;
-  const bool inA = pxi < b.width && pyA < b.height;
-  const bool inB = pxi < b.width && pyB < b.height;
+  const int bx0 = warp * 8;                                       // column block origin, tile-relative
+  const int lxi = bx0 + (lane & 7), lyi = lane >> 3;
+  const int pxi = tx * kTile + lxi, py0 = ty * kTile + lyi;
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
   const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
@@ -723,23 +742,32 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
   __shared__ SRec srec[256];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   const float lx = (float)lxi, ly = (float)lyi;
-  const float bxl = (float)bx0, bxh = (float)(bx0 + 7), byl = (float)by0, bym = (float)(by0 + 3),
-              byn = (float)(by0 + 4), byh = (float)(by0 + 7);
-  uint32_t n_tested = 0, n_evald = 0;    // DBG: per-warp cull statistics (half-box evaluations)
-  PixelState A{1.f, 0.f, 0.f, 0.f, !inA, 0u, (uint32_t)L};
-  PixelState B{1.f, 0.f, 0.f, 0.f, !inB, 0u, (uint32_t)L};
-  for (int start = 0; start < L; start += 256) {
-    if (__syncthreads_count(A.done && B.done) == kBlendThreads) break;
+  const float bxl = (float)bx0, bxh = (float)(bx0 + 7);
+  uint32_t n_tested = 0, n_evald = 0;    // DBG: per-warp cull statistics (sub-box evaluations)
+  PixelState P[kBlendPix];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int idx = start + threadIdx.x + kBlendThreads * k;
+  for (int k = 0; k < kBlendPix; ++k) {
+    const bool in = pxi < b.width && py0 + 4 * k < b.height;
+    P[k] = PixelState{1.f, 0.f, 0.f, 0.f, !in, 0u, (uint32_t)L};
+  }
+  auto all_done = [&]() {
+    bool d = true;
+#pragma unroll
+    for (int k = 0; k < kBlendPix; ++k) d = d && P[k].done;
+    return d;
+  };
+  for (int start = 0; start < L; start += 256) {
+    if (__syncthreads_count(all_done()) == NT) break;
+#pragma unroll
+    for (int k = 0; k < 256 / NT; ++k) {
+      const int idx = start + threadIdx.x + NT * k;
       if (idx < L) {
         const uint32_t g = (uint32_t)inst[idx];
         float4 a = rec[3 * g + 0];
         const float4 c = rec[3 * g + 2];
         a.x = (a.x - tx0) + c.y;      // tile-relative mean: exact hi difference + lo part
         a.y = (a.y - ty0) + c.z;
-        SRec& d = srec[threadIdx.x + kBlendThreads * k];
+        SRec& d = srec[threadIdx.x + NT * k];
         d.a = a;
         d.q = rec[3 * g + 1];
         d.c = make_float2(c.x, c.w);
@@ -748,21 +776,28 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
     __syncthreads();
     const int cnt = min(256, L - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      const bool liveA = __any_sync(0xffffffffu, !A.done), liveB = __any_sync(0xffffffffu, !B.done);
-      if (!liveA && !liveB) break;
+      uint32_t live = 0;
+#pragma unroll
+      for (int k = 0; k < kBlendPix; ++k)
+        if (__any_sync(0xffffffffu, !P[k].done)) live |= 1u << k;
+      if (!live) break;
       const int jt = c0 + lane;
-      bool needA = false, needB = false;
+      uint32_t need = 0;
       if (jt < cnt) {
         const float4 a = srec[jt].a;
-        const float qa = -a.z, qb = -a.w, qc = -srec[jt].q.x, thr = srec[jt].c.y;
-        const float xl = bxl - a.x, xh = bxh - a.x;
-        halfboxes_may_reach(qa, qb, qc, thr, xl, xh, byl - a.y, bym - a.y, byn - a.y, byh - a.y, needA, needB);
-        needA = needA && liveA;
-        needB = needB && liveB;
+        need = subboxes_may_reach(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live;
       }
-      const uint32_t mA = __ballot_sync(0xffffffffu, needA), mB = __ballot_sync(0xffffffffu, needB);
-      if (DBG) { n_tested += (uint32_t)min(32, cnt - c0); n_evald += __popc(mA) + __popc(mB); }
-      uint32_t m = mA | mB;
+      uint32_t mk[kBlendPix];
+#pragma unroll
+      for (int k = 0; k < kBlendPix; ++k) mk[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < kBlendPix; ++k) m |= mk[k];
+      if (DBG) {
+        n_tested += (uint32_t)min(32, cnt - c0);
+#pragma unroll
+        for (int k = 0; k < kBlendPix; ++k) n_evald += __popc(mk[k]);
+      }
       while (m) {
         const int bit = __ffs(m) - 1;
         m &= m - 1;
@@ -770,18 +805,17 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
         const float4 a = srec[j].a, q = srec[j].q;
         const float bch = srec[j].c.x;
         const float dx = a.x - lx;
-        const float bdx = a.w * dx;                              // b2 dx, shared by both pixels
+        const float bdx = a.w * dx;                              // b2 dx, shared by the lane's pixels
         const float base = fmaf(a.z * dx, dx, q.y);              // a2 dx^2 + log2(o)
-        const float dyA = a.y - ly;
+        const float dy0 = a.y - ly;
         const uint32_t pos = (uint32_t)(start + j + 1);
-        if ((mA >> bit) & 1u) {
-          const float eA = fmaf(dyA, fmaf(q.x, dyA, bdx), base);
-          blend_step<DBG>(A, eA, q.y, q.z, q.w, bch, pos);
-        }
-        if ((mB >> bit) & 1u) {
-          const float dyB = dyA - 4.f;
-          const float eB = fmaf(dyB, fmaf(q.x, dyB, bdx), base);
-          blend_step<DBG>(B, eB, q.y, q.z, q.w, bch, pos);
+#pragma unroll
+        for (int k = 0; k < kBlendPix; ++k) {
+          if ((mk[k] >> bit) & 1u) {
+            const float dy = dy0 - 4.f * k;
+            const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
+            blend_step<DBG>(P[k], e, q.y, q.z, q.w, bch, pos);
+          }
         }
       }
     }
@@ -795,11 +829,11 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(const __grid_const
   float* img = b.image[f];
   const FrameCam& cm = b.cam[f];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const PixelState& s = k ? B : A;
-    const bool in = k ? inB : inA;
-    if (!in) continue;
-    const size_t pix = (size_t)(k ? pyB : pyA) * b.width + pxi;
+  for (int k = 0; k < kBlendPix; ++k) {
+    const PixelState& s = P[k];
+    const int py = py0 + 4 * k;
+    if (!(pxi < b.width && py < b.height)) continue;
+    const size_t pix = (size_t)py * b.width + pxi;
     img[pix] = s.c0 + s.T * cm.bg[0];
     img[hw + pix] = s.c1 + s.T * cm.bg[1];
     img[2 * hw + pix] = s.c2 + s.T * cm.bg[2];
@@ -859,9 +893,9 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_BLEND, true, s);
   const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;
   if (dbg)
-    blend_kernel<true><<<dim3(b.ntiles, F), kBlendThreads, 0, s>>>(b);
+    blend_kernel<true><<<dim3(b.ntiles, F), 32 * kBlendWarps, 0, s>>>(b);
   else
-    blend_kernel<false><<<dim3(b.ntiles, F), kBlendThreads, 0, s>>>(b);
+    blend_kernel<false><<<dim3(b.ntiles, F), 32 * kBlendWarps, 0, s>>>(b);
   note_launches(1);
   prof_mark(FGS_STAGE_BLEND, false, s);
   return cudaGetLastError();
