@@ -718,7 +718,7 @@ __device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float
 }
 
 template <bool DBG>
-__global__ void __launch_bounds__(32 * kBlendWarps) blend_kernel(const __grid_constant__ RenderBatch b) {
+__global__ void __launch_bounds__(32 * kBlendWarps, 20) blend_kernel(const __grid_constant__ RenderBatch b) {
   // One CTA (kBlendWarps warps) per 16x16 tile.  Warp w owns the 8-wide column block x in [8w, 8w+8)
   // of all 16 rows; lane l owns the kBlendPix pixels (8w + (l&7), (l>>3) + 4k).  The tile's list (sorted
   // by (depth, gid)) is walked in batches of 256 records staged in smem; per 32 Gaussians each lane tests
