@@ -671,8 +671,8 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
 // face whose half-space excludes 0 (KKT), so at most one x-face and one y-face are candidates; on
 // each the 1-D minimiser is clamped to the face.  An inexact minimiser only raises the computed value
 // by qc delta^2 (quadratic in its error), far inside thr's margin.
-// Both half-boxes of a warp at once: they share the x-range, so the x-face and the two minimiser
-// ratios (x* = kx ey on a y-face, y* = ky ex on an x-face) are computed once.
+// Minimum of q2 over one box [xl,xh] x [yl,yh] given the shared x-face candidate ex and the minimiser
+// ratios (x* = kx ey on a y-face, y* = ky ex on an x-face).
 __device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx, float ky, float ex, float xl,
                                           float xh, float yl, float yh) {
   const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
@@ -689,14 +689,6 @@ __device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx
   return q;
 }
 
-__device__ __forceinline__ void halfboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
-                                                    float ylA, float yhA, float ylB, float yhB, bool& nA,
-                                                    bool& nB) {
-  const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
-  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
-  nA = face_min(qa, qb, qc, kx, ky, ex, xl, xh, ylA, yhA) <= thr;
-  nB = face_min(qa, qb, qc, kx, ky, ex, xl, xh, ylB, yhB) <= thr;
-}
 
 // NP pixels per lane: warp w of the tile's NW = 64/NP... warps owns a column block; lane l owns pixel
 // (x, y + 4k), k < NP, of that block (x = l & 7, y = l >> 3).  Sub-box k = rows [4k, 4k+4) of the block.
