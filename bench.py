@@ -286,12 +286,26 @@ def run_fgs(args, scene, rank, world, local_rank):
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)   # 512 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step_eager():
         fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, images, ws)
 
     for _ in range(args.warmup):
-        step()
+        step_eager()
     fgs.fgs_render_status(ws, F)
+    graph = None
+    launches_per_step = None
+    if not args.no_graph:
+        # one step captured in a CUDA graph: the timed steps replay it (same kernels, no launch gaps)
+        graph = torch.cuda.CUDAGraph()
+        l0 = fgs.fgs_launch_count()
+        with torch.cuda.graph(graph):
+            fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, images, ws,
+                           stream=torch.cuda.current_stream())
+        launches_per_step = fgs.fgs_launch_count() - l0
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
 
     # work counts of this workload (deterministic; one debug render per frame, untimed)
     counts = {"sms": torch.cuda.get_device_properties(dev).multi_processor_count}
@@ -318,40 +332,55 @@ def run_fgs(args, scene, rank, world, local_rank):
                       instances_per_frame=float(np.mean(Mv)), blend_pixel_evals_per_frame=float(np.mean(Wv)),
                       blend_warp_tests_per_frame=float(np.mean(Tv)))
 
+    def timed(run_step, profile):
+        """K steps between CUDA events on the launching stream, L2 flushed between steps (outside the
+        events); barrier + synchronize on both sides; returns (max-over-ranks ms, launches, stages)."""
+        if profile:
+            fgs.fgs_profile_enable(True)
+            fgs.fgs_profile_read()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = fgs.fgs_launch_count()
+        evs = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run_step()
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        nl = fgs.fgs_launch_count() - l0
+        if world > 1:
+            dist.barrier()
+        st = None
+        if profile:
+            st = fgs.fgs_profile_read()
+            fgs.fgs_profile_enable(False)
+        fgs.fgs_render_status(ws, F)
+        t_ms = sum(a.elapsed_time(b) for a, b in evs)
+        if world > 1:
+            tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_ms = float(tt.item())
+        return t_ms, nl, st
+
+    # (1) eager steps with the library's per-stage CUDA events: the stage breakdown and the roofline
+    #     launch durations; (2) the headline: the same step replayed from the CUDA graph.
+    t_eager, launches_eager, stages = timed(step_eager, True)
     clocks = ClockSampler(local_rank)
-    fgs.fgs_profile_enable(True)
-    fgs.fgs_profile_read()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    launches0 = fgs.fgs_launch_count()
-    evs = []
-    for _ in range(args.steps):
-        flush.zero_()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b.record(stream)
-        evs.append((a, b))
-    torch.cuda.synchronize()
-    launches = fgs.fgs_launch_count() - launches0
-    if world > 1:
-        dist.barrier()
+    if graph is not None:
+        t_max, _, _ = timed(graph.replay, False)
+        launches = launches_per_step * args.steps
+    else:
+        t_max, launches = t_eager, launches_eager
     clk = clocks.stop()
-    stages = fgs.fgs_profile_read()
-    fgs.fgs_profile_enable(False)
-    fgs.fgs_render_status(ws, F)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    t_ms = sum(step_ms)
-    t_max = t_ms
-    if world > 1:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
     value = F * args.steps * world / (t_max / 1e3)
+    value_eager = F * args.steps * world / (t_eager / 1e3)
     deform_ms = stages["deform"][0]
 
     # ---- e2e through the C ABI with host (pinned) buffers ----
@@ -408,10 +437,14 @@ def run_fgs(args, scene, rank, world, local_rank):
         "config": {"workload": workload_desc(scene), "frames_per_step": F, "n_gaussians": scene.n,
                    "image": f"{W}x{H}", "l2": "flushed between steps (512 MiB write outside the events)",
                    "parallelism": f"frame-split x{world} (each rank its own {F}-frame batch)",
-                   "max_instances_per_frame": cap},
+                   "max_instances_per_frame": cap,
+                   "timed": "CUDA-graph replay of one fgs_frames step" if graph is not None else "eager fgs_frames"},
+        "value_eager": value_eager,
         "gaussians_deformed_per_s": scene.n * F * steps * world / (t_max / 1e3),
         "gaussians_deformed_per_s_deform_stage": scene.n * F * steps / (deform_ms / 1e3) if deform_ms else None,
         "stages_ms_per_step": {k: v / steps for k, v in stage_ms.items()},
+        "stages_note": "per-stage library CUDA events over the eager timed steps (value_eager); the graph "
+                       "replays the same kernels",
         "work_per_frame": {k: v for k, v in counts.items() if k != "sms"},
         "roofline": dict(roof[dom], kernel=dom) if dom else None,
         "roofline_stages": roof,
@@ -523,6 +556,8 @@ def main():
     ap.add_argument("--impl", default="fgs", choices=["fgs", "reference"])
     ap.add_argument("--config", default="dnerf")
     ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager fgs_frames calls instead of replaying the step captured in a CUDA graph")
     ap.add_argument("--colour-heads", action="store_true",
                     help="P:1232 variant: add the colour / opacity decoders phi_C, phi_alpha (SURVEY 8(f) rank 2)")
     ap.add_argument("--n", type=int, default=None,
