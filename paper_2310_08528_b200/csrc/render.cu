@@ -693,6 +693,7 @@ __device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx
 // NP pixels per lane: warp w of the tile's NW = 64/NP... warps owns a column block; lane l owns pixel
 // (x, y + 4k), k < NP, of that block (x = l & 7, y = l >> 3).  Sub-box k = rows [4k, 4k+4) of the block.
 constexpr int kBlendPix = 4;                         // pixels per lane
+constexpr int kBlendBatch = 128;                     // records staged per batch (6 KB of smem)
 constexpr int kBlendWarps = 256 / (32 * kBlendPix);  // warps per 16x16 tile (2)
 
 // All kBlendPix 8x4 sub-boxes of a warp's column at once (shared x-face and minimiser ratios).
@@ -710,7 +711,7 @@ __device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float
 }
 
 template <bool DBG>
-__global__ void __launch_bounds__(32 * kBlendWarps, 20) blend_kernel(const __grid_constant__ RenderBatch b) {
+__global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __grid_constant__ RenderBatch b) {
   // One CTA (kBlendWarps warps) per 16x16 tile.  Warp w owns the 8-wide column block x in [8w, 8w+8)
   // of all 16 rows; lane l owns the kBlendPix pixels (8w + (l&7), (l>>3) + 4k).  The tile's list (sorted
   // by (depth, gid)) is walked in batches of 256 records staged in smem; per 32 Gaussians each lane tests
@@ -731,7 +732,8 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 20) blend_kernel(const __gri
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, f, b.L.rec);
   // staged records, one 48-B struct per list entry so one address serves all three loads
   struct __align__(16) SRec { float4 a, q; float2 c; float2 pad; };
-  __shared__ SRec srec[256];
+  constexpr int BATCH = kBlendBatch;
+  __shared__ SRec srec[BATCH];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   const float lx = (float)lxi, ly = (float)lyi;
   const float bxl = (float)bx0, bxh = (float)(bx0 + 7);
@@ -748,10 +750,10 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 20) blend_kernel(const __gri
     for (int k = 0; k < kBlendPix; ++k) d = d && P[k].done;
     return d;
   };
-  for (int start = 0; start < L; start += 256) {
+  for (int start = 0; start < L; start += BATCH) {
     if (__syncthreads_count(all_done()) == NT) break;
 #pragma unroll
-    for (int k = 0; k < 256 / NT; ++k) {
+    for (int k = 0; k < BATCH / NT; ++k) {
       const int idx = start + threadIdx.x + NT * k;
       if (idx < L) {
         const uint32_t g = (uint32_t)inst[idx];
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 20) blend_kernel(const __gri
       }
     }
     __syncthreads();
-    const int cnt = min(256, L - start);
+    const int cnt = min(BATCH, L - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       uint32_t live = 0;
 #pragma unroll
