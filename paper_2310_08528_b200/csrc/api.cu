@@ -542,7 +542,7 @@ struct CopyStreams {
   bool ok = false;
   cudaError_t err = cudaSuccess;
   cudaStream_t copy = nullptr;
-  cudaEvent_t done = nullptr;
+  cudaEvent_t done = nullptr, fork = nullptr, sh_done = nullptr;
   std::vector<cudaEvent_t> evs;
   std::mutex mu;
   std::mutex call_mu;   // one fgs_frames_host enqueue at a time per device (events are shared)
@@ -566,6 +566,8 @@ CopyStreams& copy_streams() {
     CopyStreams& c = cs[dev];
     c.err = cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking);
     if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
+    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming);
+    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.sh_done, cudaEventDisableTiming);
     c.ok = c.err == cudaSuccess;
   });
   return cs[dev];
@@ -598,16 +600,29 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   const HostLayout L = host_layout(gh, hh, mh, F, W, H, cap);
   char* d = (char*)dev_ws;
   const size_t n = (size_t)gh->n, K = (size_t)(gh->sh_degree + 1) * (gh->sh_degree + 1);
+  CopyStreams& cs = copy_streams();
+  if (!cs.ok) return cuda_fail(cs.err, "copy stream setup");
+  std::lock_guard<std::mutex> call_lock(cs.call_mu);
   auto h2d = [&](size_t off, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(d + off, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
   };
   cudaError_t e = cudaSuccess;
+  // The SH coefficients (the bulk of the model, needed only from preprocess on) are uploaded on the
+  // side stream while the deformation runs, unless phi_C reads them in the deform.
+  const bool sh_side = n && !mh->w_c;
+  if (sh_side) {
+    if ((e = cudaEventRecord(cs.fork, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(cs.copy, cs.fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    if ((e = cudaMemcpyAsync(d + L.sh, gh->sh, 12 * K * n, cudaMemcpyHostToDevice, cs.copy)) != cudaSuccess)
+      return cuda_fail(e, "host->device copy");
+    if ((e = cudaEventRecord(cs.sh_done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
+  }
   if (n) {
     e = h2d(L.means, gh->means, 12 * n);
     if (e == cudaSuccess) e = h2d(L.log_scales, gh->log_scales, 12 * n);
     if (e == cudaSuccess) e = h2d(L.quats, gh->quats, 16 * n);
     if (e == cudaSuccess) e = h2d(L.opac, gh->opacity_logits, 4 * n);
-    if (e == cudaSuccess) e = h2d(L.sh, gh->sh, 12 * K * n);
+    if (e == cudaSuccess && !sh_side) e = h2d(L.sh, gh->sh, 12 * K * n);
   }
   fgs_hexplanes hd = *hh;
   for (int l = 0; l < hh->n_scales && e == cudaSuccess; ++l)
@@ -643,20 +658,19 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
     imgs[f] = (float*)(d + L.images + (size_t)f * L.per_img);
   }
   // Deform all frames in one launch (the spatial-plane work is shared across times), then render in
-  // chunks; the device->host copy of chunk c runs on a side stream while chunk c+1 renders.
+  // growing chunks; the device->host copy of chunk c runs on the side stream while chunk c+1 renders.
   std::vector<fgs_deformed> rdefs;
   rc = frames_deform(&gd, &hd, &md, ts, F, defs.data(), s, rdefs);
   if (rc != FGS_OK) return rc;
-  CopyStreams& cs = copy_streams();
-  if (!cs.ok) return cuda_fail(cs.err, "copy stream setup");
-  std::lock_guard<std::mutex> call_lock(cs.call_mu);
-  const int chunk = std::max(1, std::min(F, kHostChunkFrames));
-  for (int f0 = 0; f0 < F; f0 += chunk) {
+  if (sh_side && (e = cudaStreamWaitEvent(s, cs.sh_done, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+  // chunks of 1, 2, 4, 4, ... frames: the first image leaves the device as early as possible
+  int ci = 0;
+  for (int f0 = 0, chunk = 1; f0 < F; f0 += chunk, chunk = std::min(2 * chunk, kHostChunkFrames), ++ci) {
     const int nf = std::min(chunk, F - f0);
     rc = render_impl(cams + f0, rdefs.data() + f0, imgs.data() + f0, nf, d + L.render + (size_t)f0 * L.per_render,
                      L.per_render * (size_t)nf, nullptr, s);
     if (rc != FGS_OK) return rc;
-    cudaEvent_t ev = cs.event(f0 / chunk);
+    cudaEvent_t ev = cs.event(ci);
     if ((e = cudaEventRecord(ev, s)) != cudaSuccess) return cuda_fail(e, "event record");
     if ((e = cudaStreamWaitEvent(cs.copy, ev, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     for (int f = f0; f < f0 + nf; ++f) {
