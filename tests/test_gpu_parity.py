@@ -476,3 +476,10 @@ def test_frames_cuda_graph_capture_and_replay():
     torch.cuda.synchronize()
     for a, b in zip(eager, imgs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (17, 1), (1, 33), (16, 16), (31, 47)])
+def test_degenerate_image_sizes(W, H):
+    """Images smaller than a tile or one pixel wide/high: partial tiles everywhere."""
+    s = make_scene("tiny", n=700, width=W, height=H)
+    _render_parity(s)
