@@ -38,8 +38,24 @@ def needs_build():
 
 
 def build(force=False, verbose=False):
+    """Compile libfgs.so if it is missing or older than its sources.  Safe to call from several
+    processes at once (torchrun ranks): one builds under an exclusive file lock, the others wait and
+    then find the library up to date."""
     if not force and not needs_build():
         return LIB
+    import fcntl
+    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    with open(os.path.join(HERE, "build", ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_build():
+                return LIB
+            return _build(verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build(verbose=False):
     nvcc = nvcc_path()
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
