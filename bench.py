@@ -110,63 +110,107 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle (CPU) arm
-def oracle_sample(scene, frame, n_tiles, rng_seed=0, deform_subset=10_000):
-    """Time the fp64 oracle on a bounded sample of one frame and extrapolate the frame time.
+# state shared with the oracle worker processes (fork start method: inherited, not pickled)
+_ORACLE = {}
 
-    Sample: deform of `deform_subset` Gaussians (scaled to N), full preprocess and binning, blend of
-    `n_tiles` random tiles (scaled to all tiles).  Returns (frame_seconds, deform_seconds_per_N, desc).
-    """
-    import numpy as np
+
+def _oracle_task(task):
+    """One unit of oracle work in a worker process (single-threaded BLAS): ("deform", t, lo, hi),
+    ("pre", lo, hi) or ("blend", tiles)."""
+    from threadpoolctl import threadpool_limits
 
     import oracle
     from oracle import render as OR
+    sc, cam = _ORACLE["scene"], _ORACLE["cam"]
+    t0 = time.perf_counter()
+    with threadpool_limits(1):
+        if task[0] == "deform":
+            oracle.deform_ref(sc, task[1], begin=task[2], end=task[3])
+        elif task[0] == "pre":
+            lo, hi = task[1], task[2]
+            OR.preprocess_ref(sc.means[lo:hi], sc.log_scales[lo:hi], sc.quats[lo:hi], sc.opacity_logits[lo:hi],
+                              sc.sh[lo:hi], sc.sh_degree, cam)
+        else:
+            d = {"means": sc.means, "log_scales": sc.log_scales, "quats": sc.quats}
+            OR.render_ref(d, sc.opacity_logits, sc.sh, sc.sh_degree, cam, tiles_subset=task[1],
+                          pre=_ORACLE["pre"], full_bins=False)
+    return time.perf_counter() - t0
 
+
+def oracle_procs():
+    try:
+        return max(1, min(32, len(os.sched_getaffinity(0))))
+    except Exception:
+        return max(1, min(32, os.cpu_count() or 1))
+
+
+def oracle_sample(scene, frame, n_tiles, rng_seed=0, deform_per_proc=2_000, procs=None):
+    """Time the fp64 oracle on a bounded sample of one frame on `procs` host cores and extrapolate the
+    frame time (SURVEY 8(d) oracle timing (ii): a process pool over Gaussian chunks and tiles).
+
+    Sample: deform of procs x deform_per_proc Gaussians (scaled to N), preprocess of all N (chunks),
+    binning (bin_ref, serial), blend of n_tiles random tiles (scaled to all tiles).  Each stage's wall
+    time is measured around its pool map.  Returns (frame_seconds, deform_seconds_per_N, desc, procs).
+    """
+    import multiprocessing as mp
+
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import render as OR
+
+    P = procs or oracle_procs()
     N = scene.n
     cam = scene.cameras[frame]
     t = float(scene.times[frame])
-    sub = min(deform_subset, N)
-    t0 = time.perf_counter()
-    oracle.deform_ref(scene, t, begin=0, end=sub)
-    t_def = (time.perf_counter() - t0) * N / max(sub, 1)
-    # the render input: canonical + the oracle deform is not re-run for all N (scaled above)
-    d = {"means": scene.means, "log_scales": scene.log_scales, "quats": scene.quats}
-    t0 = time.perf_counter()
-    pre = OR.preprocess_ref(d["means"], d["log_scales"], d["quats"], scene.opacity_logits, scene.sh,
-                            scene.sh_degree, cam)
-    t_pre = time.perf_counter() - t0
+    _ORACLE.update(scene=scene, cam=cam, pre=None)
+    with threadpool_limits(1):
+        pre = OR.preprocess_ref(scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh,
+                                scene.sh_degree, cam)                  # the blend's input (not timed)
+    _ORACLE["pre"] = pre
     gx, gy = OR.tile_grid(cam.width, cam.height)
     rng = np.random.default_rng(rng_seed)
     tiles = sorted(rng.choice(gx * gy, min(n_tiles, gx * gy), replace=False).tolist())
-    t0 = time.perf_counter()
-    OR.render_ref(d, scene.opacity_logits, scene.sh, scene.sh_degree, cam, tiles_subset=tiles, pre=pre)
-    t_bin_blend = time.perf_counter() - t0
-    # split binning from blending by timing bin_ref alone
-    t0 = time.perf_counter()
-    OR.bin_ref(pre, cam)
-    t_bin = time.perf_counter() - t0
-    t_blend = max(t_bin_blend - t_bin, 0.0) * (gx * gy) / len(tiles)
+    sub = min(N, P * deform_per_proc)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(P) as pool:
+        pool.map(_oracle_task, [("pre", 0, 1)] * P)          # start the workers (not timed)
+
+        def timed_map(tasks):
+            t0 = time.perf_counter()
+            pool.map(_oracle_task, tasks)
+            return time.perf_counter() - t0
+        edges = np.linspace(0, sub, P + 1).astype(int)
+        t_def = timed_map([("deform", t, int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a])
+        t_def *= N / max(sub, 1)
+        edges = np.linspace(0, N, P + 1).astype(int)
+        t_pre = timed_map([("pre", int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a])
+        chunks = [tiles[i::P] for i in range(P) if tiles[i::P]]
+        t_blend = timed_map([("blend", c) for c in chunks]) * (gx * gy) / len(tiles)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        OR.bin_ref(pre, cam)
+        t_bin = time.perf_counter() - t0
     frame_s = t_def + t_pre + t_bin + t_blend
-    desc = (f"1 frame of {scene.name}: oracle deform of {sub}/{N} Gaussians (x{N / max(sub, 1):.0f}), "
-            f"full preprocess + binning, blend of {len(tiles)}/{gx * gy} random tiles "
-            f"(x{gx * gy / len(tiles):.1f}) of the canonical G; fp64 numpy, 1 thread")
-    return frame_s, t_def, desc
+    desc = (f"1 frame of {scene.name} on {P} host processes: oracle deform of {sub}/{N} Gaussians "
+            f"(x{N / max(sub, 1):.0f}), preprocess of all {N}, binning (serial), blend of {len(tiles)}/{gx * gy} "
+            f"random tiles (x{gx * gy / len(tiles):.1f}) of the canonical G; fp64 numpy, 1 BLAS thread per process")
+    return frame_s, t_def, desc, P
 
 
 def run_reference(args, scene, rank):
     if rank != 0:
         return
-    from threadpoolctl import threadpool_limits
-    per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    n_tiles = int(min(200, max(10, per_step / 0.04)))
-    with threadpool_limits(1):
-        for w in range(args.warmup):
-            oracle_sample(scene, w % scene.n_frames, n_tiles, rng_seed=w)
-        frame_s = []
-        t_defs = []
-        for k in range(args.steps):
-            fs, td, desc = oracle_sample(scene, k % scene.n_frames, n_tiles, rng_seed=100 + k)
-            frame_s.append(fs)
-            t_defs.append(td)
+    P = oracle_procs()
+    n_tiles = 24 * P
+    for w in range(args.warmup):
+        oracle_sample(scene, w % scene.n_frames, n_tiles, rng_seed=w, procs=P)
+    frame_s = []
+    t_defs = []
+    for k in range(args.steps):
+        fs, td, desc, _ = oracle_sample(scene, k % scene.n_frames, n_tiles, rng_seed=100 + k, procs=P)
+        frame_s.append(fs)
+        t_defs.append(td)
     F = scene.n_frames
     step_s = [F * s for s in frame_s]
     total = sum(step_s)
@@ -176,9 +220,9 @@ def run_reference(args, scene, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_desc(scene), "frames_per_step": F, "parallelism": "none (host cores)"},
+        "config": {"workload": workload_desc(scene), "frames_per_step": F, "parallelism": f"{P} host processes (oracle over Gaussian chunks and tiles)"},
         "gaussians_deformed_per_s": scene.n * len(t_defs) / sum(t_defs),
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": P, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -456,10 +500,9 @@ def run_fgs(args, scene, rank, world, local_rank):
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world >= 1:
-        from threadpoolctl import threadpool_limits
-        with threadpool_limits(1):
-            fs, td, desc = oracle_sample(scene, 0, n_tiles=150)
-        line["cpu_baseline"] = {"value": 1.0 / fs, "unit": "frames/s", "cores": 1, "kind": "oracle",
+        P = oracle_procs()
+        fs, td, desc, P = oracle_sample(scene, 0, n_tiles=24 * P, procs=P)
+        line["cpu_baseline"] = {"value": 1.0 / fs, "unit": "frames/s", "cores": P, "kind": "oracle",
                                 "sample": desc, "gaussians_deformed_per_s": scene.n / td}
     print(json.dumps(line), flush=True)
 
