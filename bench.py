@@ -404,7 +404,9 @@ def run_fgs(args, scene, rank, world, local_rank):
             st = fgs.fgs_profile_read()
             fgs.fgs_profile_enable(False)
         fgs.fgs_render_status(ws, F)
-        t_ms = sum(a.elapsed_time(b) for a, b in evs)
+        per = [a.elapsed_time(b) for a, b in evs]
+        timed.per_step = per
+        t_ms = sum(per)
         if world > 1:
             tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -422,6 +424,9 @@ def run_fgs(args, scene, rank, world, local_rank):
         launches = launches_per_step * args.steps
     else:
         t_max, launches = t_eager, launches_eager
+    per_step = sorted(timed.per_step)
+    step_stats = {"median": statistics.median(per_step), "p10": per_step[int(0.1 * (len(per_step) - 1))],
+                  "p90": per_step[int(round(0.9 * (len(per_step) - 1)))], "unit": "ms (this rank)"}
     clk = clocks.stop()
     value = F * args.steps * world / (t_max / 1e3)
     value_eager = F * args.steps * world / (t_eager / 1e3)
@@ -484,6 +489,7 @@ def run_fgs(args, scene, rank, world, local_rank):
                    "max_instances_per_frame": cap,
                    "timed": "CUDA-graph replay of one fgs_frames step" if graph is not None else "eager fgs_frames"},
         "value_eager": value_eager,
+        "step_ms": step_stats,
         "gaussians_deformed_per_s": scene.n * F * steps * world / (t_max / 1e3),
         "gaussians_deformed_per_s_deform_stage": scene.n * F * steps / (deform_ms / 1e3) if deform_ms else None,
         "stages_ms_per_step": {k: v / steps for k, v in stage_ms.items()},
