@@ -508,3 +508,22 @@ def test_gpu_image_invariant_to_array_order():
         mask[16 * y0:16 * y1, 16 * x0:16 * x1] = True
     assert np.array_equal(a["image"][:, ~mask], b["image"][:, ~mask])
     assert np.abs(a["image"] - b["image"]).max() <= PIX_TOL
+
+
+def test_batches_longer_than_one_launch():
+    """More frames than one launch's frame table (kMaxFrames = 32): fgs_frames / fgs_deform_batch split
+    the batch; every frame equals its single-frame deform + render."""
+    import torch
+    s = make_scene("dnerf", n=6_000, width=64, height=48, n_frames=35)
+    ds = _ds(s)
+    scratch, _ = ds.alloc_deformed(35)
+    imgs = [torch.empty((3, 48, 64), device="cuda") for _ in range(35)]
+    ws = ds.alloc_workspace(35)
+    fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, scratch, imgs, ws)
+    fgs.fgs_render_status(ws, 35)
+    for f in (0, 31, 32, 34):
+        d, _, _ = gpu_deform(ds, float(s.times[f]))
+        ws1 = ds.alloc_workspace(1)
+        im = torch.empty((3, 48, 64), device="cuda")
+        fgs.fgs_render(ds.cams[f], d, im, ws1)
+        assert torch.equal(im, imgs[f]), f
