@@ -88,9 +88,12 @@ __device__ __forceinline__ int knot0(float u, int R) {
 
 // (1 - w) a + w b in a fixed evaluation order (the staged and the L2 paths must agree bit for bit)
 __device__ __forceinline__ float4 lerp4(float4 a, float4 b, float w) {
+  // packed fp32x2 (FMUL2 / FFMA2): per lane exactly fmaf(w, b, wa * a)
   const float wa = 1.f - w;
-  return make_float4(fmaf(w, b.x, __fmul_rn(wa, a.x)), fmaf(w, b.y, __fmul_rn(wa, a.y)),
-                     fmaf(w, b.z, __fmul_rn(wa, a.z)), fmaf(w, b.w, __fmul_rn(wa, a.w)));
+  const float2 wa2 = make_float2(wa, wa), w2 = make_float2(w, w);
+  const float2 lo = ffma2(w2, make_float2(b.x, b.y), fmul2(wa2, make_float2(a.x, a.y)));
+  const float2 hi = ffma2(w2, make_float2(b.z, b.w), fmul2(wa2, make_float2(a.z, a.w)));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
 // linear interpolation at u in [0,1], channel quad c4, of a line whose knot i sits at float offset
@@ -404,8 +407,12 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 #pragma unroll
             for (int qq = 0; qq < QT; ++qq) {
               const float4 a = tl[qq][0], b = tl[qq][1], c = tl[qq][2];
-              const float fh[4] = {sv[4 * qq + 0] * (a.x * b.x * c.x), sv[4 * qq + 1] * (a.y * b.y * c.y),
-                                   sv[4 * qq + 2] * (a.z * b.z * c.z), sv[4 * qq + 3] * (a.w * b.w * c.w)};
+              // S . (a . b . c), packed two channels per instruction
+              const float2 p0 = fmul2(make_float2(sv[4 * qq + 0], sv[4 * qq + 1]),
+                                      fmul2(fmul2(make_float2(a.x, a.y), make_float2(b.x, b.y)), make_float2(c.x, c.y)));
+              const float2 p1 = fmul2(make_float2(sv[4 * qq + 2], sv[4 * qq + 3]),
+                                      fmul2(fmul2(make_float2(a.z, a.w), make_float2(b.z, b.w)), make_float2(c.z, c.w)));
+              const float fh[4] = {p0.x, p0.y, p1.x, p1.y};
 #pragma unroll
               for (int e = 0; e < 4; ++e) tc::tf32_split(fh[e], hi[l][4 * qq + e], lo[l][4 * qq + e]);
             }
