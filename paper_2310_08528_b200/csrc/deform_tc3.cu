@@ -67,12 +67,17 @@ __device__ __forceinline__ float4 bilerp4(const float* __restrict__ P, int na, i
   const float4 v10 = __ldg(row1), v11 = __ldg(row1 + FEAT / 4);
   const float w00 = (1.f - fa) * (1.f - fb), w01 = fa * (1.f - fb);
   const float w10 = (1.f - fa) * fb, w11 = fa * fb;
-  float4 r;
-  r.x = w00 * v00.x + w01 * v01.x + w10 * v10.x + w11 * v11.x;
-  r.y = w00 * v00.y + w01 * v01.y + w10 * v10.y + w11 * v11.y;
-  r.z = w00 * v00.z + w01 * v01.z + w10 * v10.z + w11 * v11.z;
-  r.w = w00 * v00.w + w01 * v01.w + w10 * v10.w + w11 * v11.w;
-  return r;
+  // ((w00 v00 + w01 v01) + w10 v10) + w11 v11, two channels per instruction
+  const float2 a00 = make_float2(w00, w00), a01 = make_float2(w01, w01);
+  const float2 a10 = make_float2(w10, w10), a11 = make_float2(w11, w11);
+  float2 lo = fmul2(a00, make_float2(v00.x, v00.y)), hi = fmul2(a00, make_float2(v00.z, v00.w));
+  lo = ffma2(a01, make_float2(v01.x, v01.y), lo);
+  hi = ffma2(a01, make_float2(v01.z, v01.w), hi);
+  lo = ffma2(a10, make_float2(v10.x, v10.y), lo);
+  hi = ffma2(a10, make_float2(v10.z, v10.w), hi);
+  lo = ffma2(a11, make_float2(v11.x, v11.y), lo);
+  hi = ffma2(a11, make_float2(v11.z, v11.w), hi);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
 // Lines are stored [R][FEAT/4] float4 with the quad index XOR-swizzled by the knot index.
