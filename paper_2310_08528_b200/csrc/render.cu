@@ -839,15 +839,11 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
   }
 }
 
-int num_sms_cached() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
+int num_sms_current() {   // SM count of the calling thread's current device (cheap attribute query)
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
 }
 
 }  // namespace
@@ -877,10 +873,11 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
   tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
   // long lists: persistent CTAs (3 per SM over the batch) walk each frame's worklist (usually empty)
-  static const cudaError_t attr = cudaFuncSetAttribute(long_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)kLongSortSmem);
+  // (per call: the attribute is per device, and the calling thread's current device may change)
+  const cudaError_t attr = cudaFuncSetAttribute(long_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)kLongSortSmem);
   if (attr != cudaSuccess) return attr;
-  long_sort_kernel<<<dim3((unsigned)std::max(1, (3 * num_sms_cached() + F - 1) / F), F), kLargeSortThreads,
+  long_sort_kernel<<<dim3((unsigned)std::max(1, (3 * num_sms_current() + F - 1) / F), F), kLargeSortThreads,
                      kLongSortSmem, s>>>(b);
   note_launches(2);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
