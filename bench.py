@@ -250,8 +250,10 @@ def ncu_traffic(scene, stage):
     return sum(ks) if stage == "binning" else ks[0]
 
 
-def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
-    """Algorithmic work per launch / measured launch time for each stage."""
+def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz, steps):
+    """Algorithmic work per launch / measured launch time for each stage.  A stage may
+    take several launches per step (render batches of > FGS_MAX_BATCH frames): the work of one launch
+    is the step's work / launches per step, so achieved = step work / step time of the stage."""
     F = scene.n_frames
     N = scene.n
     K = (scene.sh_degree + 1) ** 2
@@ -265,8 +267,8 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
     out = {}
 
     def avg_launch_s(stage):
-        n = max(stage_launches.get(stage, 0), 1)
-        return stage_ms.get(stage, 0.0) / 1e3 / n
+        # per-step stage time; the F frames below are the step's (= launches per step x one launch's)
+        return stage_ms.get(stage, 0.0) / 1e3 / max(steps, 1)
 
     # deform: bound by the on-chip gathers of the time lines: per Gaussian-frame
     # 3 temporal planes x L scales x 2 knots x h fp32 read from shared memory (the spatial product is
@@ -298,7 +300,6 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz):
     t_sort = stage_ms.get("tile_scan", 0) + stage_ms.get("duplicate", 0) + stage_ms.get("tile_sort", 0)
     if t_sort > 0 and M:
         by = (16 * M + 16 * N) * F
-        steps = max(stage_launches.get("blend", 1), 1)
         out["binning"] = {"bound": "hbm", "achieved": by / (t_sort / 1e3 / steps) / 1e9, "peak": hbm,
                           "unit": "GB/s", "frac": by / (t_sort / 1e3 / steps) / 1e9 / hbm, "traffic": None,
                           "algorithmic": "16 B per instance + 16 B per Gaussian (lower bound)"}
@@ -476,7 +477,7 @@ def run_fgs(args, scene, rank, world, local_rank):
     steps = args.steps
     stage_ms = {k: v[0] for k, v in stages.items()}
     stage_launches = {k: v[1] for k, v in stages.items()}
-    roof = roofline_objects(scene, stage_ms, stage_launches, peaks, counts, clk.get("sm_mhz"))
+    roof = roofline_objects(scene, stage_ms, stage_launches, peaks, counts, clk.get("sm_mhz"), steps)
     # dominant kernel = largest share of the step
     dom = max(roof, key=lambda k: stage_ms.get(k, 0.0) if k != "binning" else 0.0) if roof else None
     line = {

@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   constexpr int FT = FEAT / RL::NP;            // features per (producer thread, scale)
   constexpr int QT = FT / 4;
   constexpr int MAXS = 64 / FEAT;              // max scales (IN <= 64)
+  static_assert(32 * FEAT * RL::PROD_WARPS <= kLineBufFloats, "prologue transpose tiles exceed the line buffer");
   constexpr int DW = WIDTH < 32 ? 32 : WIDTH;  // columns of one accumulator
   constexpr uint32_t IDESC = tc::idesc_tf32(kM, WIDTH);
   const int NS = p.n_scales;
@@ -287,51 +288,85 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       prod_sync<kProdThreads>();     // previous group's line / U readers are done
       if (tid < FGS_MAX_SCALES * 3) { win[2 * tid] = INT_MAX; win[2 * tid + 1] = INT_MIN; }
       prod_sync<kProdThreads>();
-      for (int gt = 0; gt < ng; ++gt) {
+      // (1) grid coordinates u (smem U) and knot windows: thread (quarter, part) takes the tiles
+      //     gt = part mod NP of the group
+      for (int gt = part; gt < ng; gt += RL::NP) {
         const int64_t g = p.begin + (gstart + gt) * kM + row;
-        const bool valid = g < p.end;
         float u[3] = {0.f, 0.f, 0.f};
-        if (valid) {
+        if (g < p.end) {
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const float m = __ldg(p.means + g * 3 + a);
             u[a] = fminf(fmaxf((m - p.bmin[a]) / p.ext[a], 0.f), 1.f);
           }
-        }
-        if (part == 0) {
-          float* Ur = U + (gt * kM + row) * 4;
-          Ur[0] = u[0]; Ur[1] = u[1]; Ur[2] = u[2];
-          if (valid) {
 #pragma unroll
-            for (int l = 0; l < MAXS; ++l) {
-              if (l >= NS) break;
+          for (int l = 0; l < MAXS; ++l) {
+            if (l >= NS) break;
 #pragma unroll
-              for (int a = 0; a < 3; ++a) {
-                const int i0 = knot0<FEAT>(u[a], p.res[l]);
-                atomicMin(win + (l * 3 + a) * 2, i0);
-                atomicMax(win + (l * 3 + a) * 2 + 1, i0 + 1);
-              }
+            for (int a = 0; a < 3; ++a) {
+              const int i0 = knot0<FEAT>(u[a], p.res[l]);
+              atomicMin(win + (l * 3 + a) * 2, i0);
+              atomicMax(win + (l * 3 + a) * 2 + 1, i0 + 1);
             }
           }
         }
-#pragma unroll
-        for (int l = 0; l < MAXS; ++l) {
-          if (l >= NS) break;
+        float* Ur = U + (gt * kM + row) * 4;
+        Ur[0] = u[0]; Ur[1] = u[1]; Ur[2] = u[2];
+      }
+      prod_sync<kProdThreads>();     // U complete
+      // (2) S = xy . xz . yz (bilinear, Eq. 7's spatial planes) of every (Gaussian, feature): one warp
+      //     per (tile, scale) of its lane quarter, LANES OVER FEATURES so that every corner read is one
+      //     coalesced 128-B plane row; the 32 x FEAT result is transposed through the (idle) line
+      //     buffer so thread = Gaussian row for the TMEM store.
+      {
+        float* T = line + warp * (32 * FEAT);
+        const bool fl = lane < FEAT;
+        for (int unit = part; unit < ng * NS; unit += RL::NP) {
+          const int gt = unit / NS, l = unit - gt * NS;
           const int R = p.res[l];
-          float sv[FT];
+          const float Rm = (float)(R - 1);
+          const float* Ur = U + (gt * kM + row) * 4;
+          const float vm = p.begin + (gstart + gt) * kM + row < p.end ? 1.f : 0.f;
+          int off[3];
+          float fa[3], fb[3];
 #pragma unroll
-          for (int qq = 0; qq < QT; ++qq) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) {
-              const int c4 = part * QT + qq;
-              v = bilerp4<FEAT>(p.planes[l][0], R, R, u[0], u[1], c4);
-              const float4 b = bilerp4<FEAT>(p.planes[l][1], R, R, u[0], u[2], c4);
-              const float4 c = bilerp4<FEAT>(p.planes[l][2], R, R, u[1], u[2], c4);
-              v = make_float4(v.x * b.x * c.x, v.y * b.y * c.y, v.z * b.z * c.z, v.w * b.w * c.w);
-            }
-            sv[4 * qq + 0] = v.x; sv[4 * qq + 1] = v.y; sv[4 * qq + 2] = v.z; sv[4 * qq + 3] = v.w;
+          for (int pl = 0; pl < 3; ++pl) {
+            const float ga = Ur[pl < 2 ? 0 : 1] * Rm, gb = Ur[pl == 0 ? 1 : 2] * Rm;
+            const int i0 = min((int)floorf(ga), R - 2), j0 = min((int)floorf(gb), R - 2);
+            fa[pl] = ga - (float)i0;
+            fb[pl] = gb - (float)j0;
+            off[pl] = (j0 * R + i0) * FEAT;
           }
-          tmem_st_n<FT>(lane_base + colS + gt * IN + l * FEAT + part * FT, sv);
+          const float* P0 = p.planes[l][0] + lane;
+          const float* P1 = p.planes[l][1] + lane;
+          const float* P2 = p.planes[l][2] + lane;
+          const int rs = R * FEAT;
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) {
+            float s = __shfl_sync(0xffffffffu, vm, i);
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl) {
+              const int o = __shfl_sync(0xffffffffu, off[pl], i);
+              const float a = __shfl_sync(0xffffffffu, fa[pl], i);
+              const float b = __shfl_sync(0xffffffffu, fb[pl], i);
+              const float* P = (pl == 0 ? P0 : pl == 1 ? P1 : P2) + o;
+              float v00 = 0.f, v01 = 0.f, v10 = 0.f, v11 = 0.f;
+              if (fl) {
+                v00 = __ldg(P); v01 = __ldg(P + FEAT);
+                v10 = __ldg(P + rs); v11 = __ldg(P + rs + FEAT);
+              }
+              const float top = fmaf(a, v01, (1.f - a) * v00);
+              const float bot = fmaf(a, v11, (1.f - a) * v10);
+              s *= fmaf(b, bot, (1.f - b) * top);
+            }
+            if (fl) T[i * FEAT + (lane ^ (i & (FEAT - 1)))] = s;
+          }
+          __syncwarp();
+          float sv[FEAT];
+#pragma unroll
+          for (int c = 0; c < FEAT; ++c) sv[c] = T[lane * FEAT + (c ^ (lane & (FEAT - 1)))];
+          tmem_st_n<FEAT>(lane_base + colS + gt * IN + l * FEAT, sv);
+          __syncwarp();
         }
       }
       tc::tmem_st_wait();
