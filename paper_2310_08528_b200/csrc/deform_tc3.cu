@@ -266,7 +266,9 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 
   const int64_t count = p.end - p.begin;
   const int64_t tiles = (count + kM - 1) / kM;
-  const int64_t t_beg = tiles * blockIdx.x / gridDim.x, t_end = tiles * (blockIdx.x + 1) / gridDim.x;
+  // tile indices fit 32 bits (the host rejects ranges of >= 2^31 tiles); 32-bit loop state keeps the
+  // producers' register budget for the hot loop
+  const int t_beg = (int)(tiles * blockIdx.x / gridDim.x), t_end = (int)(tiles * (blockIdx.x + 1) / gridDim.x);
 
   if (warp < kProdWarps) {
     // =============================================================== producers
@@ -282,8 +284,8 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       tc::tmem_st_wait();
     }
     uint32_t it = 0;   // tile-frame counter
-    for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
-      const int ng = (int)min((int64_t)G, t_end - gstart);
+    for (int gstart = t_beg; gstart < t_end; gstart += G) {
+      const int ng = min(G, t_end - gstart);
       // ---- group prologue: grid coordinates (smem), knot windows, spatial products S (TMEM) ----
       prod_sync<kProdThreads>();     // previous group's line / U readers are done
       if (tid < FGS_MAX_SCALES * 3) { win[2 * tid] = INT_MAX; win[2 * tid + 1] = INT_MIN; }
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       // (1) grid coordinates u (smem U) and knot windows: thread (quarter, part) takes the tiles
       //     gt = part mod NP of the group
       for (int gt = part; gt < ng; gt += RL::NP) {
-        const int64_t g = p.begin + (gstart + gt) * kM + row;
+        const int64_t g = p.begin + (int64_t)(gstart + gt) * kM + row;
         float u[3] = {0.f, 0.f, 0.f};
         if (g < p.end) {
 #pragma unroll
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           const int R = p.res[l];
           const float Rm = (float)(R - 1);
           const float* Ur = U + (gt * kM + row) * 4;
-          const float vm = p.begin + (gstart + gt) * kM + row < p.end ? 1.f : 0.f;
+          const float vm = p.begin + (int64_t)(gstart + gt) * kM + row < p.end ? 1.f : 0.f;
           int off[3];
           float fa[3], fb[3];
 #pragma unroll
@@ -416,8 +418,8 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         }
         prod_sync<kProdThreads>();
         for (int gt = 0; gt < ng; ++gt, ++it) {
-          const float* Ur = U + (gt * kM + row) * 4;
-          const float ux = Ur[0], uy = Ur[1], uz = Ur[2];
+          const float4 u4 = *reinterpret_cast<const float4*>(U + (gt * kM + row) * 4);   // one LDS.128
+          const float ux = u4.x, uy = u4.y, uz = u4.z;
           float hi[MAXS][FT], lo[MAXS][FT];
 #pragma unroll
           for (int l = 0; l < MAXS; ++l) {
@@ -478,8 +480,8 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     if (lane == 0) {
       const uint32_t b_hi = tc::smem_u32(smem + SM::OFF_BHI), b_lo = tc::smem_u32(smem + SM::OFF_BLO);
       uint32_t it = 0;
-      for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
-        const int ng = (int)min((int64_t)G, t_end - gstart);
+      for (int gstart = t_beg; gstart < t_end; gstart += G) {
+        const int ng = min(G, t_end - gstart);
         for (int f = 0; f < p.n_t; ++f) {
           for (int gt = 0; gt < ng; ++gt, ++it) {
             const uint32_t buf = it & 1u;
@@ -507,11 +509,11 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     uint32_t it = 0;
-    for (int64_t gstart = t_beg; gstart < t_end; gstart += G) {
-      const int ng = (int)min((int64_t)G, t_end - gstart);
+    for (int gstart = t_beg; gstart < t_end; gstart += G) {
+      const int ng = min(G, t_end - gstart);
       for (int f = 0; f < p.n_t; ++f) {
         for (int gt = 0; gt < ng; ++gt, ++it) {
-          const int64_t g = p.begin + (gstart + gt) * kM + row;
+          const int64_t g = p.begin + (int64_t)(gstart + gt) * kM + row;
           const bool valid = g < p.end;
           float cx[10];
           if (valid) {
@@ -626,6 +628,7 @@ bool deform_tc3_supported(const DeformBatch& p) {
 
 cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s) {
   if (p.end <= p.begin || p.n_t <= 0) return cudaSuccess;
+  if ((p.end - p.begin + kM - 1) / kM >= (int64_t)INT_MAX) return cudaErrorInvalidValue;
   const bool color = p.w_c || p.w_a;
   if (p.n_c + 11 > kNoutColor) return cudaErrorInvalidValue;
 #define FGS_DISPATCH_W(FEAT)                                                                        \
