@@ -64,7 +64,8 @@ def _build(verbose=False):
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        # FGS_NVCC_EXTRA: extra flags for experiments (e.g. -D switches); not set in normal builds
+        cmd = [nvcc] + NVCC_FLAGS + os.environ.get("FGS_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for src, obj, p in procs:
         out = p.communicate()[0].decode(errors="replace")

@@ -17,6 +17,10 @@
 //                          additive update -> global stores; releases D[i % 2].
 // Producer work on tile-frame i+1 and the epilogue of i-1 overlap the MMAs of i (mbarrier pipeline).
 // TMEM columns: D0 | D1 | A_hi | A_lo | S[0..G).  Thread (warp w, lane) touches TMEM lane quarter w % 4.
+// Experiment switches (never set in normal builds; FGS_NVCC_EXTRA="-DFGS_EXP_..." with tools/gpu_exp.sh):
+// FGS_EXP_NOSTAGE (no time-line staging), FGS_EXP_NOLINE (no line reads), FGS_EXP_NOMMA (no MMAs),
+// FGS_EXP_NOEPI (epilogue releases D without the heads) — each removes one part of the schedule so its
+// share of the kernel time can be measured; results are wrong under any of them.
 #include <cuda_runtime.h>
 #include <limits.h>
 
@@ -37,6 +41,8 @@ constexpr int kMaxG = 16;
 // not fit reads the temporal planes from L2 instead (same arithmetic, bit-identical results).
 constexpr int kLineBufFloats = 16384;          // 64 KB
 constexpr int kEpiWarps = 4;
+// Gaussians per pass of the spatial-plane sampling in the group prologue
+constexpr int kProB = 4;
 // Producer warps per TMEM lane quarter (each takes FEAT / NP features of every scale).
 template <int FEAT>
 struct Roles {
@@ -45,7 +51,15 @@ struct Roles {
   static constexpr int PROD_THREADS = 32 * PROD_WARPS;
   static constexpr int EPI0 = PROD_WARPS;                 // first epilogue warp
   static constexpr int MMA_WARP = PROD_WARPS + kEpiWarps;
-  static constexpr int THREADS = 32 * (MMA_WARP + 1);     // 672 (FEAT >= 16) or 416
+  // the MMA warp's warpgroup is padded with 3 idle warps so that every role is whole warpgroups and the
+  // register file can be re-split with setmaxnreg (producers up, epilogue and MMA down)
+  static constexpr int THREADS = 32 * (MMA_WARP + 4);     // 768 (FEAT >= 16) or 512
+  static constexpr bool REALLOC = PROD_WARPS == 16;
+  // the CTA's pool is what the launch allocated (768 x 80 = 61440): 512 x 96 + 128 x 72 + 128 x 24 fills
+  // it exactly (an increase the pool cannot serve blocks forever)
+  static constexpr int REG_PROD = 96, REG_EPI = 72, REG_MMA = 24;
+  static_assert(!REALLOC || (THREADS == 768 && 16 * REG_PROD + 4 * REG_EPI + 4 * REG_MMA == 24 * 80),
+                "setmaxnreg budget must equal the launch allocation (768 threads x 80 registers)");
 };
 
 __device__ __forceinline__ uint32_t core_off(int row, int k, int rows) {
@@ -272,6 +286,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 
   if (warp < kProdWarps) {
     // =============================================================== producers
+    if constexpr (RL::REALLOC) tc::setmaxnreg_inc<RL::REG_PROD>();
     const int quarter = warp & 3, part = warp >> 2;   // part: which FT-feature slice of each scale
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -343,25 +358,37 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           const float* P1 = p.planes[l][1] + lane;
           const float* P2 = p.planes[l][2] + lane;
           const int rs = R * FEAT;
-#pragma unroll 2
-          for (int i = 0; i < 32; ++i) {
-            float s = __shfl_sync(0xffffffffu, vm, i);
+          // kProB Gaussians per pass: their 12 kProB corner reads are issued before any is used (the
+          // prologue is bound by L2 latency, not bandwidth)
+          for (int i0 = 0; i0 < 32; i0 += kProB) {
+            float v[kProB][3][4];
 #pragma unroll
-            for (int pl = 0; pl < 3; ++pl) {
-              const int o = __shfl_sync(0xffffffffu, off[pl], i);
-              const float a = __shfl_sync(0xffffffffu, fa[pl], i);
-              const float b = __shfl_sync(0xffffffffu, fb[pl], i);
-              const float* P = (pl == 0 ? P0 : pl == 1 ? P1 : P2) + o;
-              float v00 = 0.f, v01 = 0.f, v10 = 0.f, v11 = 0.f;
-              if (fl) {
-                v00 = __ldg(P); v01 = __ldg(P + FEAT);
-                v10 = __ldg(P + rs); v11 = __ldg(P + rs + FEAT);
+            for (int b = 0; b < kProB; ++b) {
+#pragma unroll
+              for (int pl = 0; pl < 3; ++pl) {
+                const int o = __shfl_sync(0xffffffffu, off[pl], i0 + b);
+                const float* P = (pl == 0 ? P0 : pl == 1 ? P1 : P2) + o;
+                v[b][pl][0] = v[b][pl][1] = v[b][pl][2] = v[b][pl][3] = 0.f;
+                if (fl) {
+                  v[b][pl][0] = __ldg(P); v[b][pl][1] = __ldg(P + FEAT);
+                  v[b][pl][2] = __ldg(P + rs); v[b][pl][3] = __ldg(P + rs + FEAT);
+                }
               }
-              const float top = fmaf(a, v01, (1.f - a) * v00);
-              const float bot = fmaf(a, v11, (1.f - a) * v10);
-              s *= fmaf(b, bot, (1.f - b) * top);
             }
-            if (fl) T[i * FEAT + (lane ^ (i & (FEAT - 1)))] = s;
+#pragma unroll
+            for (int b = 0; b < kProB; ++b) {
+              const int i = i0 + b;
+              float s = __shfl_sync(0xffffffffu, vm, i);
+#pragma unroll
+              for (int pl = 0; pl < 3; ++pl) {
+                const float a = __shfl_sync(0xffffffffu, fa[pl], i);
+                const float bb = __shfl_sync(0xffffffffu, fb[pl], i);
+                const float top = fmaf(a, v[b][pl][1], (1.f - a) * v[b][pl][0]);
+                const float bot = fmaf(a, v[b][pl][3], (1.f - a) * v[b][pl][2]);
+                s *= fmaf(bb, bot, (1.f - bb) * top);
+              }
+              if (fl) T[i * FEAT + (lane ^ (i & (FEAT - 1)))] = s;
+            }
           }
           __syncwarp();
           float sv[FEAT];
@@ -393,7 +420,11 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         const float ft = gt_ - (float)j0;
         // ---- stage the temporal lines at t over the group's knot windows (time lerp of 2 rows) ----
         prod_sync<kProdThreads>();   // U/win visible; previous frame's line readers done
+#ifdef FGS_EXP_NOSTAGE
+        if (false) {
+#else
         if (staged) {
+#endif
 #pragma unroll
           for (int l = 0; l < MAXS; ++l) {
             if (l >= NS) break;
@@ -428,6 +459,12 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             float sv[FT];
             tmem_ld_n<FT>(lane_base + colS + gt * IN + l * FEAT + part * FT, sv);
             float4 tl[QT][3];
+#ifdef FGS_EXP_NOLINE
+            if (true) {
+#pragma unroll
+              for (int qq = 0; qq < QT; ++qq) tl[qq][0] = tl[qq][1] = tl[qq][2] = make_float4(ux, uy, uz, 1.f);
+            } else
+#endif
             if (staged) {
               const int o0 = segoff[3 * l + 0], o1 = segoff[3 * l + 1], o2 = segoff[3 * l + 2];
 #pragma unroll
@@ -475,9 +512,10 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         }
       }
     }
-  } else if (warp == kMmaWarp) {
-    // =============================================================== MMA issuer
-    if (lane == 0) {
+  } else if (warp >= kMmaWarp) {
+    // =============================================================== MMA issuer (+3 idle warps)
+    if constexpr (RL::REALLOC) tc::setmaxnreg_dec<RL::REG_MMA>();
+    if (warp == kMmaWarp && lane == 0) {
       const uint32_t b_hi = tc::smem_u32(smem + SM::OFF_BHI), b_lo = tc::smem_u32(smem + SM::OFF_BLO);
       uint32_t it = 0;
       for (int gstart = t_beg; gstart < t_end; gstart += G) {
@@ -489,6 +527,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             if (it >= 2) tc::mbar_wait(d_free + buf, ((it >> 1) - 1) & 1u);
             tc::fence_after_sync();
             const uint32_t d = tmem + buf * DW;
+#ifndef FGS_EXP_NOMMA
             for (int s = 0; s < KP / 8; ++s) {
               const uint32_t bo = (uint32_t)s * (2 * (WIDTH / 8) * 128);
               const uint64_t dbh = tc::smem_desc(b_hi + bo, (WIDTH / 8) * 128, 128);
@@ -497,6 +536,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
               tc::mma_tf32_ts(d, tmem + colA_hi + 8 * s, dbl, IDESC, 1u);
               tc::mma_tf32_ts(d, tmem + colA_hi + 8 * s, dbh, IDESC, 1u);
             }
+#endif
             tc::mma_commit(a_free);
             tc::mma_commit(d_full + buf);
           }
@@ -505,6 +545,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     }
   } else {
     // =============================================================== epilogue
+    if constexpr (RL::REALLOC) tc::setmaxnreg_dec<RL::REG_EPI>();
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -527,6 +568,12 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           const uint32_t buf = it & 1u;
           tc::mbar_wait(d_full + buf, (it >> 1) & 1u);
           tc::fence_after_sync();
+#ifdef FGS_EXP_NOEPI
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(d_free + buf);
+          continue;
+#endif
           // head outputs in passes of 12 over the hidden columns (one pass without the P:1232
           // decoders); the geometry outputs (pass 0) are kept, the colour / opacity ones stored
           float ho[12];
