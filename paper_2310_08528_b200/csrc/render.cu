@@ -135,8 +135,10 @@ __device__ __forceinline__ bool agg_fits(const AggBox& r) {
 
 template <int DEG>
 __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
-  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // frame-minor CTA order: the F CTAs of one Gaussian block are adjacent in launch order, so its SH
+  // (192 B per Gaussian at degree 3, frame-invariant) come from HBM once and from L2 for the other frames
+  const int f = (int)(blockIdx.x % (unsigned)b.n_frames);
+  const int64_t i0 = (int64_t)(blockIdx.x / (unsigned)b.n_frames) * blockDim.x + threadIdx.x;
   const bool valid = i0 < b.n;
   const int64_t i = valid ? i0 : b.n - 1;     // out-of-range threads mirror the last Gaussian, write nothing
   uint32_t* keys = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.keys);
@@ -854,11 +856,12 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   const unsigned nb = (unsigned)std::max<int64_t>(1, (n + 255) / 256);
   prof_mark(FGS_STAGE_PREPROCESS, true, s);
   clear_kernel<<<dim3((unsigned)std::min(64, (b.ntiles + 255) / 256), F), 256, 0, s>>>(b);
+  const dim3 pre_grid((unsigned)(nb * (unsigned)F));   // 1-D, frame-minor (see preprocess_kernel)
   switch (b.sh_degree) {
-    case 0: preprocess_kernel<0><<<dim3(nb, F), 256, 0, s>>>(b); break;
-    case 1: preprocess_kernel<1><<<dim3(nb, F), 256, 0, s>>>(b); break;
-    case 2: preprocess_kernel<2><<<dim3(nb, F), 256, 0, s>>>(b); break;
-    default: preprocess_kernel<3><<<dim3(nb, F), 256, 0, s>>>(b); break;
+    case 0: preprocess_kernel<0><<<pre_grid, 256, 0, s>>>(b); break;
+    case 1: preprocess_kernel<1><<<pre_grid, 256, 0, s>>>(b); break;
+    case 2: preprocess_kernel<2><<<pre_grid, 256, 0, s>>>(b); break;
+    default: preprocess_kernel<3><<<pre_grid, 256, 0, s>>>(b); break;
   }
   note_launches(2);
   prof_mark(FGS_STAGE_PREPROCESS, false, s);
