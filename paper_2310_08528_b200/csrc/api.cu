@@ -608,15 +608,10 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   };
   cudaError_t e = cudaSuccess;
   // The SH coefficients (the bulk of the model, needed only from preprocess on) are uploaded on the
-  // side stream while the deformation runs, unless phi_C reads them in the deform.
+  // side stream while the deformation runs, unless phi_C reads them in the deform.  They are queued
+  // AFTER the deformation's inputs so the two uploads do not share the link: the deformation starts
+  // once its ~14 MB (D) are on the device, and the SH upload hides behind it.
   const bool sh_side = n && !mh->w_c;
-  if (sh_side) {
-    if ((e = cudaEventRecord(cs.fork, s)) != cudaSuccess) return cuda_fail(e, "event record");
-    if ((e = cudaStreamWaitEvent(cs.copy, cs.fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
-    if ((e = cudaMemcpyAsync(d + L.sh, gh->sh, 12 * K * n, cudaMemcpyHostToDevice, cs.copy)) != cudaSuccess)
-      return cuda_fail(e, "host->device copy");
-    if ((e = cudaEventRecord(cs.sh_done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
-  }
   if (n) {
     e = h2d(L.means, gh->means, 12 * n);
     if (e == cudaSuccess) e = h2d(L.log_scales, gh->log_scales, 12 * n);
@@ -641,6 +636,13 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
     *dsts[i] = (const float*)(d + L.mlp[i]);
   }
   if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
+  if (sh_side) {
+    if ((e = cudaEventRecord(cs.fork, s)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(cs.copy, cs.fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    if ((e = cudaMemcpyAsync(d + L.sh, gh->sh, 12 * K * n, cudaMemcpyHostToDevice, cs.copy)) != cudaSuccess)
+      return cuda_fail(e, "host->device copy");
+    if ((e = cudaEventRecord(cs.sh_done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
+  }
   fgs_gaussians gd = *gh;
   gd.means = (const float*)(d + L.means); gd.log_scales = (const float*)(d + L.log_scales);
   gd.quats = (const float*)(d + L.quats); gd.opacity_logits = (const float*)(d + L.opac);
