@@ -537,7 +537,7 @@ HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs
 
 namespace {
 constexpr int kHostChunkFrames = 4;
-// Side stream + events of fgs_frames_host (one set per process and device 0..7, created on first use).
+// Side stream + events of fgs_frames_host (one set per process and device, created on first use).
 struct CopyStreams {
   bool ok = false;
   cudaError_t err = cudaSuccess;
@@ -556,12 +556,17 @@ struct CopyStreams {
     return evs[i];
   }
 };
+constexpr int kMaxDevices = 64;
 CopyStreams& copy_streams() {
-  static CopyStreams cs[8];
-  static std::once_flag once[8];
+  static CopyStreams cs[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
+  static CopyStreams unsupported;   // ok = false: device ordinal beyond kMaxDevices
   int dev = 0;
   cudaGetDevice(&dev);
-  dev = std::max(0, std::min(dev, 7));
+  if (dev < 0 || dev >= kMaxDevices) {
+    unsupported.err = cudaErrorInvalidDevice;
+    return unsupported;
+  }
   std::call_once(once[dev], [&] {
     CopyStreams& c = cs[dev];
     c.err = cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking);

@@ -4,17 +4,20 @@
 //
 // One persistent CTA per SM over a contiguous range of 128-Gaussian tiles, processed in groups of G
 // tiles; per group, for every time t of the batch, every tile of the group is one "tile-frame" i.
-// Roles (416 threads):
-//   producers (warps 0-7)  group prologue: the spatial-plane product S = xy . xz . yz of every
+// Roles (FEAT >= 16: 768 threads = 6 warpgroups; FEAT = 8: 512 threads, 8 producer warps):
+//   producers (warps 0-15) group prologue: the spatial-plane product S = xy . xz . yz of every
 //                          (Gaussian, feature) of the group, parked in TENSOR MEMORY, and the knot
 //                          window each axis of the group touches; per time t: the three temporal planes
 //                          collapsed to 1-D lines at t over those windows only (smem); per tile-frame:
 //                          f_h = S . line_x(u_x) . line_y(u_y) . line_z(u_z), split hi/lo (3xTF32) and
 //                          stored to TMEM as the A operand.
-//   MMA issuer (warp 12)   one thread: 3 x K/8 tcgen05.mma.kind::tf32 (A from TMEM, W_d hi/lo from
-//                          smem) into accumulator D[i % 2]; commits to "A free" and "D[i % 2] full".
-//   epilogue (warps 8-11)  one thread per Gaussian row: D -> bias + ReLU -> the 10 head dot products ->
+//   epilogue (warps 16-19) one thread per Gaussian row: D -> bias + ReLU -> the 10 head dot products ->
 //                          additive update -> global stores; releases D[i % 2].
+//   MMA issuer (warp 20)   one thread: 3 x K/8 tcgen05.mma.kind::tf32 (A from TMEM, W_d hi/lo from
+//                          smem) into accumulator D[i % 2]; commits to "A free" and "D[i % 2] full".
+//                          Warps 21-23 are idle: they make the MMA role a whole warpgroup, so that
+//                          setmaxnreg can move registers from the epilogue and MMA warpgroups (72, 24)
+//                          to the producers (96) out of the launch's 80 per thread.
 // Producer work on tile-frame i+1 and the epilogue of i-1 overlap the MMAs of i (mbarrier pipeline).
 // TMEM columns: D0 | D1 | A_hi | A_lo | S[0..G).  Thread (warp w, lane) touches TMEM lane quarter w % 4.
 // Experiment switches (never set in normal builds; FGS_NVCC_EXTRA="-DFGS_EXP_..." with tools/gpu_exp.sh):
