@@ -716,7 +716,7 @@ template <bool DBG>
 __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __grid_constant__ RenderBatch b) {
   // One CTA (kBlendWarps warps) per 16x16 tile.  Warp w owns the 8-wide column block x in [8w, 8w+8)
   // of all 16 rows; lane l owns the kBlendPix pixels (8w + (l&7), (l>>3) + 4k).  The tile's list (sorted
-  // by (depth, gid)) is walked in batches of 256 records staged in smem; per 32 Gaussians each lane tests
+  // by (depth, gid)) is walked in batches of kBlendBatch records staged in smem; per 32 Gaussians each lane tests
   // one against the exact ellipse bound over the warp's kBlendPix 8x4 sub-boxes, and the warp
   // evaluates, in list order, each Gaussian on the sub-boxes it can reach (warp-uniform branches), so
   // the per-Gaussian loads and dx terms are shared by up to kBlendPix pixels per lane.
