@@ -545,7 +545,17 @@ def run_shard(args, scene, rank, world, local_rank):
     images = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in mine]
     per_t = max(len(v) for v in views)
     ws = ds.alloc_workspace(max(per_t, 1), 16 * scene.n)
-    sd = ShardedDeform(scene.n, world, rank, dev, n_slots=2)
+    fused = getattr(args, "fused", False)
+    if fused and not (dist.is_available() and dist.is_initialized()):
+        # symmetric memory needs a process group: a one-rank NCCL group on 127.0.0.1
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=dev)
+    sd = ShardedDeform(scene.n, world, rank, dev, n_slots=2, fused=fused)
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -590,10 +600,12 @@ def run_shard(args, scene, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(scene), "frames_per_step": F, "distinct_times": len(uniq),
-                   "parallelism": f"views split x{world}; deformation sharded by Gaussian + all_gather (e2)",
+                   "parallelism": f"views split x{world}; deformation sharded by Gaussian + "
+                                  + ("peer stores from the deform epilogue into symmetric memory + barrier (e2 fused)"
+                                     if fused else "all_gather (e2)"),
                    "l2": "flushed between steps (512 MiB write outside the events)"},
         "gaussians_deformed_per_s": scene.n * len(uniq) * args.steps / (t_max / 1e3),
-        "gpu_launches": launches, "clocks": clk, "mode": "shard",
+        "gpu_launches": launches, "clocks": clk, "mode": "shard-fused" if fused else "shard",
     }
     print(json.dumps(line), flush=True)
 
@@ -617,6 +629,9 @@ def main():
     ap.add_argument("--mode", default="frames", choices=["frames", "shard"],
                     help="frames: every rank renders its own frame batch (e1); shard: multi-view batch, views "
                          "split across ranks, deformation sharded by Gaussian + NCCL all-gather (e2)")
+    ap.add_argument("--fused", action="store_true",
+                    help="with --mode shard: the deform epilogue stores every rank's copy into symmetric "
+                         "memory (fgs_deform_range_peers) instead of the NCCL all-gather (SURVEY 8(e2) fused)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "fgs":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)

@@ -142,6 +142,18 @@ int fgs_deform(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp
  * Results are bit-identical to the same rows of fgs_deform. */
 int fgs_deform_range(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
                      int64_t begin, int64_t end, fgs_deformed* out, fgs_stream_t stream);
+/* §8(e2) fused deform + gather: as fgs_deform_range, but means / log_scales / quats of rows
+ * [begin, end) are stored n_peers times, replica q at byte offset peer_offsets[q] from the `out`
+ * address (peer_offsets: HOST array of int64, multiples of 4; 1 <= n_peers <= 8).  With the
+ * symmetric-memory gather buffers of a process group (offset q = buffer_ptrs[q] - buffer_ptrs[rank])
+ * the deform epilogue itself writes every rank's copy — over NVLink, tile by tile, overlapped with
+ * the deformation — and no separate all-gather pass is needed; the caller orders the ranks with a
+ * stream-ordered barrier before rendering.  Every replica must lie in caller-owned memory the device
+ * can write (peer access).  Not with phi_C / phi_alpha.  Results are bit-identical to
+ * fgs_deform_range in every replica. */
+int fgs_deform_range_peers(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+                           int64_t begin, int64_t end, fgs_deformed* out, const int64_t* peer_offsets,
+                           int32_t n_peers, fgs_stream_t stream);
 /* n_t times ts[0..n_t) (HOST array) into outs[0..n_t) (HOST array of structs) in one pass that
  * shares the spatial-plane work across times.  Bit-identical to n_t calls of fgs_deform. */
 int fgs_deform_batch(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,

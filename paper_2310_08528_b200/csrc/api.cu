@@ -107,6 +107,7 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.w_c = m->w_c; p.b_c = m->b_c; p.w_a = m->w_a; p.b_a = m->b_a;
   p.n_c = m->w_c ? 3 * (g->sh_degree + 1) * (g->sh_degree + 1) : 0;
   p.sh_in = g->sh; p.opac_in = g->opacity_logits;
+  p.n_peer = 1;                          // one replica at offset 0 (memset)
 }
 
 // Deform kernel selection: FGS_TUNE_DEFORM_KERNEL (or env FGS_DEFORM = simt | tc1 | tc2 | tc3 at load)
@@ -143,7 +144,8 @@ cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
 }
 
 int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
-                int64_t begin, int64_t end, fgs_deformed* outs, cudaStream_t s) {
+                int64_t begin, int64_t end, fgs_deformed* outs, cudaStream_t s, const int64_t* peer_off = nullptr,
+                int n_peers = 0) {
   int rc;
   if ((rc = check_gaussians(g)) != FGS_OK) return rc;
   if ((rc = check_field(h, m)) != FGS_OK) return rc;
@@ -166,6 +168,14 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
   p.begin = begin; p.end = end;
   if ((heads_c || heads_a) && !deform_tc3_supported(p))
     return fail(FGS_E_NOTIMPL, "colour/opacity decoders need the warp-specialised deform (field too large)");
+  if (peer_off) {
+    FGS_CHECK(n_peers >= 1 && n_peers <= kMaxPeers, "n_peers must be in [1, 8]");
+    FGS_CHECK(!heads_c && !heads_a, "peer replicas: only means / log_scales / quats (no phi_C / phi_alpha)");
+    FGS_CHECK(deform_tc3_supported(p), "peer replicas need the warp-specialised deform (field too large)");
+    for (int q = 0; q < n_peers; ++q) FGS_CHECK(peer_off[q] % 4 == 0, "peer offsets must be multiples of 4 bytes");
+    p.n_peer = n_peers;
+    for (int q = 0; q < n_peers; ++q) p.peer_off[q] = peer_off[q];
+  }
   for (int f0 = 0; f0 < n_t; f0 += kMaxFrames) {
     p.n_t = std::min(kMaxFrames, n_t - f0);
     for (int f = 0; f < p.n_t; ++f) {
@@ -176,7 +186,7 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
       p.out_sh[f] = outs[f0 + f].sh;
       p.out_opacity[f] = outs[f0 + f].opacity_logits;
     }
-    cudaError_t e = launch_deform_any(p, s);
+    cudaError_t e = peer_off ? launch_deform_tc3(p, s) : launch_deform_any(p, s);
     if (e != cudaSuccess) return cuda_fail(e, "deform launch");
   }
   return FGS_OK;
@@ -360,6 +370,13 @@ int fgs_deform(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp
 int fgs_deform_range(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
                      int64_t begin, int64_t end, fgs_deformed* out, fgs_stream_t stream) {
   return deform_impl(g, field, mlp, &t, 1, begin, end, out, (cudaStream_t)stream);
+}
+
+int fgs_deform_range_peers(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+                           int64_t begin, int64_t end, fgs_deformed* out, const int64_t* peer_offsets,
+                           int32_t n_peers, fgs_stream_t stream) {
+  if (!peer_offsets) return fail(FGS_E_INVALID, "peer_offsets is NULL");
+  return deform_impl(g, field, mlp, &t, 1, begin, end, out, (cudaStream_t)stream, peer_offsets, n_peers);
 }
 
 int fgs_deform_batch(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, const float* ts,

@@ -627,12 +627,20 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           if (valid) {
 #pragma unroll
             for (int o = 0; o < 10; ++o) ho[o] = cx[o] + (ho[o] + bh[o]);
+            // every replica (one by default; with fgs_deform_range_peers each rank's gather buffer,
+            // remote ones written over NVLink right here, tile by tile)
+            for (int q = 0; q < p.n_peer; ++q) {
+              const int64_t off = p.peer_off[q];
+              float* om = reinterpret_cast<float*>(reinterpret_cast<char*>(p.out_means[f] + g * 3) + off);
+              float* oq = reinterpret_cast<float*>(reinterpret_cast<char*>(p.out_quats[f] + g * 4) + off);
+              float* os = reinterpret_cast<float*>(reinterpret_cast<char*>(p.out_log_scales[f] + g * 3) + off);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) p.out_means[f][g * 3 + c] = ho[c];
+              for (int c = 0; c < 3; ++c) om[c] = ho[c];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) p.out_quats[f][g * 4 + c] = ho[3 + c];
+              for (int c = 0; c < 4; ++c) oq[c] = ho[3 + c];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) p.out_log_scales[f][g * 3 + c] = ho[7 + c];
+              for (int c = 0; c < 3; ++c) os[c] = ho[7 + c];
+            }
           }
         }
       }

@@ -9,6 +9,7 @@ namespace fgs {
 
 constexpr int kTile = FGS_TILE;              // 16x16 pixel tiles ([3dgs] rasterizer, reading R8)
 constexpr int kMaxFrames = 32;               // frames per launch (kernel-parameter table)
+constexpr int kMaxPeers = 8;                 // replicas of the deform outputs (fgs_deform_range_peers)
 constexpr int kScanThreads = 1024;           // tile-count scan CTA (one per frame)
 constexpr int kBlendThreads = 128;           // blend CTA: 4 warps x 8x8 pixel boxes of a 16x16 tile
 constexpr int kBlendSortMax = 1024;          // longest tile list the blend sorts in shared memory
@@ -89,6 +90,10 @@ struct DeformBatch {
   float* out_quats[kMaxFrames];
   float* out_sh[kMaxFrames];            // written when phi_C is present
   float* out_opacity[kMaxFrames];       // written when phi_alpha is present
+  // means / log_scales / quats are stored n_peer times, replica q at byte offset peer_off[q] from the
+  // out_* address (1 replica at offset 0 by default; §8(e2) fused: every rank's gather buffer)
+  int n_peer;
+  int64_t peer_off[kMaxPeers];
 };
 
 // Kernel launchers (return cudaError_t of the launch).

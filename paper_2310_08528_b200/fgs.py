@@ -63,7 +63,7 @@ class fgs_render_aux(ctypes.Structure):
 
 
 _LIB = None
-EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_batch", "fgs_render_workspace_bytes",
+EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_range_peers", "fgs_deform_batch", "fgs_render_workspace_bytes",
            "fgs_render", "fgs_render_batch", "fgs_render_debug", "fgs_render_status", "fgs_frames",
            "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_profile_enable", "fgs_profile_read",
            "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version")
@@ -84,6 +84,8 @@ def lib():
         L.fgs_deform.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float, P(fgs_deformed), c_void_p]
         L.fgs_deform_range.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float, c_int64, c_int64,
                                        P(fgs_deformed), c_void_p]
+        L.fgs_deform_range_peers.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float, c_int64,
+                                             c_int64, P(fgs_deformed), P(c_int64), c_int32, c_void_p]
         L.fgs_deform_batch.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(c_float), c_int32,
                                        P(fgs_deformed), c_void_p]
         L.fgs_render_workspace_bytes.argtypes = [c_int64, c_int32, c_int32, c_int64]
@@ -142,6 +144,16 @@ def fgs_deform(g, field, mlp, t, out, stream=None):
 def fgs_deform_range(g, field, mlp, t, begin, end, out, stream=None):
     return _check(lib().fgs_deform_range(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
                                          c_int64(begin), c_int64(end), ctypes.byref(out), _stream(stream)))
+
+
+def fgs_deform_range_peers(g, field, mlp, t, begin, end, out, peer_offsets: Sequence[int], stream=None):
+    """fgs_deform_range whose outputs are also stored at byte offsets peer_offsets[q] from `out`'s
+    arrays (the §8(e2) fused deform + gather; include/fgs.h)."""
+    n = len(peer_offsets)
+    arr = (c_int64 * max(n, 1))(*[int(x) for x in peer_offsets])
+    return _check(lib().fgs_deform_range_peers(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
+                                               c_int64(begin), c_int64(end), ctypes.byref(out), arr, n,
+                                               _stream(stream)))
 
 
 def fgs_deform_batch(g, field, mlp, ts: Sequence[float], outs: Sequence[fgs_deformed], stream=None):

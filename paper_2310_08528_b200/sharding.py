@@ -12,6 +12,10 @@ Two ways to use one 8xB200 box (one process per GPU, torch.distributed):
      attributes X', r', s' (40 B per Gaussian) are assembled on every rank with
      `all_gather_into_tensor` (NCCL over NVLink/NVSwitch).  The gather is issued async_op so the caller
      can render the previous time while it is in flight (the one exchange step of the path).
+     `fused=True` (SURVEY §8(e2) "fused option"): the gather buffers are symmetric memory
+     (torch.distributed._symmetric_memory) and fgs_deform_range_peers stores every deformed row
+     straight into ALL ranks' buffers from the deform epilogue (NVLink peer stores, overlapped with
+     the deformation tile by tile); the exchange step is then one stream-ordered barrier.
 
 Host logic only: every arithmetic step of the method runs in libfgs.so (or, in the CPU tests, in a
 deform callback supplied by the test); this module partitions, allocates and exchanges.
@@ -68,27 +72,60 @@ class ShardedDeform:
     (in place: each rank's input is its own chunk of the output).
     """
 
-    def __init__(self, n: int, world: int, rank: int, device, n_slots: int = 2, group=None):
+    def __init__(self, n: int, world: int, rank: int, device, n_slots: int = 2, group=None, fused: bool = False):
         import torch
         self.n, self.world, self.rank, self.group = n, world, rank, group
         self.rows = padded_rows(n, world)
         self.chunk = self.rows // world if world else 0
         self.begin, self.end = shard_range(n, rank, world)
+        self.fused = fused
         self.bufs: List[dict] = []
+        self.handles: list = []
+        self.offsets: List[List[int]] = []
+        rows = max(self.rows, 1)
         for _ in range(n_slots):
-            # padding rows are zero-filled once so a gathered buffer never holds uninitialised memory
-            self.bufs.append({k: torch.zeros((max(self.rows, 1), w), dtype=torch.float32, device=device)
-                              for k, w in DEFORMED_FIELDS})
+            if not fused:
+                # padding rows are zero-filled once so a gathered buffer never holds uninitialised memory
+                self.bufs.append({k: torch.zeros((rows, w), dtype=torch.float32, device=device)
+                                  for k, w in DEFORMED_FIELDS})
+                continue
+            # one symmetric buffer per slot holding the three arrays back to back, so a replica's
+            # offset from the local copy is the same for all three (fgs_deform_range_peers)
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = group if group is not None else dist.group.WORLD
+            flat = symm_mem.empty(rows * 10, dtype=torch.float32, device=device)
+            flat.zero_()
+            h = symm_mem.rendezvous(flat, grp)
+            ptrs = [int(x) for x in h.buffer_ptrs]
+            self.handles.append(h)
+            self.offsets.append([ptrs[q] - ptrs[h.rank] for q in range(h.world_size)])
+            # quats first: they need 16-byte alignment (float4 loads), means / log_scales only 4
+            views, o = {}, 0
+            for k, w in (("quats", 4), ("means", 3), ("log_scales", 3)):
+                views[k] = flat[o:o + rows * w].view(rows, w)
+                o += rows * w
+            self.bufs.append(views)
 
-    def deform(self, slot: int, t: float, deform_fn: Callable[[int, float, int, int, dict], None]) -> None:
+    def deform(self, slot: int, t: float, deform_fn: Callable[..., None]) -> None:
+        """deform_fn(slot, t, begin, end, bufs) — with fused=True also the peer offsets of the slot's
+        replicas: deform_fn(slot, t, begin, end, bufs, offsets)."""
         if self.end > self.begin:
-            deform_fn(slot, t, self.begin, self.end, self.bufs[slot])
+            if self.fused:
+                deform_fn(slot, t, self.begin, self.end, self.bufs[slot], self.offsets[slot])
+            else:
+                deform_fn(slot, t, self.begin, self.end, self.bufs[slot])
 
     def gather(self, slot: int, async_op: bool = True):
         """all_gather_into_tensor of the three deformed arrays of `slot`; returns the work handles
         (wait() them, or let the NCCL stream ordering do it, before rendering the slot)."""
         import torch.distributed as dist
         works = []
+        if self.fused:
+            # the rows are already in every rank's buffer (peer stores of the deform epilogue): a
+            # stream-ordered barrier over the group makes them visible before the render
+            self.handles[slot].barrier(channel=slot)
+            return works
         # world size 1 still goes through the collective when a process group exists (the same code
         # path as N > 1; NCCL copies in place), so the single-GPU bench exercises it
         if self.rows == 0 or not (dist.is_available() and dist.is_initialized()):
@@ -106,13 +143,17 @@ class ShardedDeform:
         return {k: v[:self.n] for k, v in self.bufs[slot].items()}
 
 
-def fgs_range_deformer(ds, stream=None) -> Callable[[int, float, int, int, dict], None]:
-    """deform_fn for ShardedDeform running fgs_deform_range (libfgs.so) on a fgs.DeviceScene."""
+def fgs_range_deformer(ds, stream=None) -> Callable[..., None]:
+    """deform_fn for ShardedDeform running fgs_deform_range (libfgs.so) on a fgs.DeviceScene, or
+    fgs_deform_range_peers when given the replicas' offsets (fused mode)."""
     from . import fgs
 
-    def run(slot, t, begin, end, bufs):
+    def run(slot, t, begin, end, bufs, offsets=None):
         d = ds.deformed_struct(bufs["means"], bufs["log_scales"], bufs["quats"])
-        fgs.fgs_deform_range(ds.g, ds.field, ds.mlp, float(t), begin, end, d, stream)
+        if offsets is None:
+            fgs.fgs_deform_range(ds.g, ds.field, ds.mlp, float(t), begin, end, d, stream)
+        else:
+            fgs.fgs_deform_range_peers(ds.g, ds.field, ds.mlp, float(t), begin, end, d, offsets, stream)
 
     return run
 

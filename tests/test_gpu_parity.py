@@ -260,6 +260,81 @@ def test_sharded_frames_single_rank_equals_fgs_frames():
         assert torch.equal(a, b)
 
 
+def _flat_deformed(ds, rows):
+    """One flat [rows x 10] fp32 buffer holding quats | means | log_scales back to back (the layout of
+    ShardedDeform's symmetric buffers): returns (flat, struct, views)."""
+    import torch
+    flat = torch.full((rows * 10,), float("nan"), dtype=torch.float32, device="cuda")
+    q, m, ls = flat[:rows * 4].view(rows, 4), flat[rows * 4:rows * 7].view(rows, 3), flat[rows * 7:].view(rows, 3)
+    return flat, ds.deformed_struct(m, ls, q), {"means": m, "log_scales": ls, "quats": q}
+
+
+@pytest.mark.parametrize("n_peers", [1, 2, 3])
+def test_deform_range_peers_writes_every_replica(n_peers):
+    """§8(e2) fused deform + gather on one GPU: fgs_deform_range_peers stores rows [begin, end) into
+    every replica (here other local buffers at the given byte offsets) — each replica equals
+    fgs_deform_range's rows bit for bit and the rows outside the range stay untouched."""
+    import torch
+    s = make_scene("dnerf", n=20_011, width=64, height=64, n_frames=1)
+    ds = _ds(s)
+    t = float(s.times[0])
+    n, lo, hi = s.n, 3_001, 17_777
+    bufs = [_flat_deformed(ds, n) for _ in range(n_peers)]
+    offs = [bufs[q][0].data_ptr() - bufs[0][0].data_ptr() for q in range(n_peers)]
+    fgs.fgs_deform_range_peers(ds.g, ds.field, ds.mlp, t, lo, hi, bufs[0][1], offs)
+    ref_flat, ref_struct, ref = _flat_deformed(ds, n)
+    fgs.fgs_deform_range(ds.g, ds.field, ds.mlp, t, lo, hi, ref_struct)
+    torch.cuda.synchronize()
+    for flat, _, views in bufs:
+        for k in ("means", "log_scales", "quats"):
+            assert torch.equal(views[k][lo:hi], ref[k][lo:hi]), k
+            assert torch.isnan(views[k][:lo]).all() and torch.isnan(views[k][hi:]).all(), k
+
+
+def test_deform_range_peers_rejects_bad_arguments():
+    s = make_scene("tiny")
+    ds = _ds(s)
+    _, st, _ = _flat_deformed(ds, s.n)
+    for offs in ([], [0] * 9, [0, 2]):
+        with pytest.raises(fgs.FgsError):
+            fgs.fgs_deform_range_peers(ds.g, ds.field, ds.mlp, 0.5, 0, s.n, st, offs)
+
+
+def test_sharded_frames_fused_world1_equals_fgs_frames():
+    """(e2) fused mode: symmetric-memory gather buffers, the deform epilogue writes every rank's copy
+    (fgs_deform_range_peers), a stream-ordered barrier replaces the all-gather — at world size 1 (a
+    one-rank NCCL group) the images equal fgs_frames bit for bit."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2310_08528_b200.sharding import ShardedDeform, sharded_frames
+    assert not dist.is_initialized()
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        s = make_scene("dnerf", n=20_000, width=128, height=96, n_frames=3)
+        ds = _ds(s)
+        sd = ShardedDeform(s.n, 1, 0, "cuda", n_slots=2, fused=True)
+        assert sd.offsets[0] == [0]
+        imgs = [torch.empty((3, 96, 128), device="cuda") for _ in range(3)]
+        ws = ds.alloc_workspace(1)
+        views = [[(ds.cams[k], k)] for k in range(3)]
+        sharded_frames(ds, sd, ds.times, views, imgs, ws)
+        scratch, _ = ds.alloc_deformed(3)
+        ref = [torch.empty((3, 96, 128), device="cuda") for _ in range(3)]
+        ws3 = ds.alloc_workspace(3)
+        fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, scratch, ref, ws3)
+        torch.cuda.synchronize()
+        for a, b in zip(imgs, ref):
+            assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_frames_sharing_a_time_share_the_deformation():
     """fgs_frames deforms each distinct t once; frames at the same t (views of one instant) render
     from it — images equal the per-frame deform + render path bit for bit."""
