@@ -122,3 +122,40 @@ def test_sharded_deform_allgather_gloo(n):
             for key in ref:
                 assert out[k][key].shape == ref[key].shape
                 assert np.array_equal(out[k][key], ref[key].astype(np.float32)), (rank, k, key)
+
+
+def test_sharded_deform_fused_host_logic(monkeypatch):
+    """Fused (e2) host logic without a GPU: one symmetric buffer per slot carved quats | means |
+    log_scales, replica offsets = buffer_ptrs[q] - buffer_ptrs[rank] handed to the deform callback,
+    and gather() = the handle's stream-ordered barrier on the slot's channel (no collective call)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+
+    calls = {"barrier": []}
+
+    class FakeHandle:
+        def __init__(self, t):
+            self.rank, self.world_size = 1, 3
+            base = t.data_ptr()
+            self.buffer_ptrs = [base - 4096, base, base + 8192]
+
+        def barrier(self, channel=0):
+            calls["barrier"].append(channel)
+
+    monkeypatch.setattr(symm_mem, "empty", lambda n, dtype, device: torch.zeros(n, dtype=dtype))
+    monkeypatch.setattr(symm_mem, "rendezvous", lambda t, grp: FakeHandle(t))
+    import torch.distributed as dist
+    monkeypatch.setattr(dist, "group", type("G", (), {"WORLD": "world"}))
+    n, world, rank = 101, 3, 1
+    sd = ShardedDeform(n, world, rank, "cpu", n_slots=2, fused=True)
+    rows = padded_rows(n, world)
+    assert sd.offsets == [[-4096, 0, 8192]] * 2
+    b = sd.bufs[0]
+    assert b["quats"].shape == (rows, 4) and b["means"].shape == (rows, 3) and b["log_scales"].shape == (rows, 3)
+    # one flat buffer: quats at offset 0 (16-byte aligned), means after them, log_scales last
+    assert b["means"].data_ptr() - b["quats"].data_ptr() == rows * 4 * 4
+    assert b["log_scales"].data_ptr() - b["means"].data_ptr() == rows * 3 * 4
+    seen = []
+    sd.deform(1, 0.25, lambda slot, t, lo, hi, bufs, offsets: seen.append((slot, t, lo, hi, offsets)))
+    assert seen == [(1, 0.25) + shard_range(n, rank, world) + ([-4096, 0, 8192],)]
+    assert sd.gather(1) == [] and calls["barrier"] == [1]
