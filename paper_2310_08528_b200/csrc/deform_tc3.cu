@@ -168,6 +168,11 @@ struct Tc3Smem {
   static constexpr int TOTAL = OFF_BAR + 6 * 8 + 16;
 };
 
+// With the colour decoders the epilogue (59 head outputs) is the bottleneck: it gets the registers
+// (512 x 88 + 128 x 104 + 128 x 24 = 61440, the same pool)
+constexpr int kRegProdColor = 88, kRegEpiColor = 104;
+static_assert(16 * kRegProdColor + 4 * kRegEpiColor + 4 * 24 == 24 * 80, "setmaxnreg budget (colour)");
+
 template <int N>
 __device__ __forceinline__ void tmem_st_n(uint32_t taddr, const float* v) {
   if constexpr (N % 16 == 0) {
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 
   if (warp < kProdWarps) {
     // =============================================================== producers
-    if constexpr (RL::REALLOC) tc::setmaxnreg_inc<RL::REG_PROD>();
+    if constexpr (RL::REALLOC) tc::setmaxnreg_inc<COLOR ? kRegProdColor : RL::REG_PROD>();
     const int quarter = warp & 3, part = warp >> 2;   // part: which FT-feature slice of each scale
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -548,7 +553,10 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     }
   } else {
     // =============================================================== epilogue
-    if constexpr (RL::REALLOC) tc::setmaxnreg_dec<RL::REG_EPI>();
+    if constexpr (RL::REALLOC) {
+      if constexpr (COLOR) tc::setmaxnreg_inc<kRegEpiColor>();
+      else tc::setmaxnreg_dec<RL::REG_EPI>();
+    }
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
