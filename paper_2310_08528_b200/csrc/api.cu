@@ -333,6 +333,7 @@ WsLayout make_layout(int64_t n, int width, int height, int64_t cap) {
   L.cursor = take(4 * nt);
   L.ranges = take(8 * nt);
   L.long_list = take(4 * nt);
+  L.order = take(4 * nt);
   L.inst = take(8 * cc);
   L.inst2 = take(8 * cc);
   L.total = o;

@@ -29,6 +29,7 @@ struct WsLayout {
   size_t cursor = 0;         // uint32[ntiles] scatter cursors
   size_t ranges = 0;         // uint2[ntiles]  [start, end) of each tile's list (clamped to cap)
   size_t long_list = 0;      // uint32[ntiles] tiles whose lists exceed the warp-sort cap (count in cnt[4])
+  size_t order = 0;          // uint32[ntiles] tiles by descending list length (blend dispatch order)
   size_t inst = 0;           // uint64[cap] instances (depth_key << 32 | gid), bucketed by tile
   size_t inst2 = 0;          // uint64[cap] scratch of the long-list sort
   size_t total = 0;

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
 }
 
 // ------------------------------------------------------------------------------ tile scan (a7)
+constexpr int kOrderBuckets = 1024;     // list-length buckets of the blend dispatch order
 // Block-wide exclusive scan of one value per thread; returns the block total.
 template <int NT>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& excl, uint32_t* sw) {
@@ -336,6 +337,31 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_co
     cnt[3] = total;
     cnt[1] = (uint32_t)((uint64_t)total < cap ? (uint64_t)total : cap);
     cnt[2] = (uint64_t)total > cap ? 1u : 0u;
+  }
+  // Blend dispatch order: the frame's tiles by descending list length (counting sort on the length,
+  // capped), so the longest tiles start first and the grid does not end on a long tile — the blend
+  // grid runs (rank-major, frame-minor) through it.  Order within a length bucket is arbitrary: every
+  // tile is blended independently, so the images do not depend on it.
+  __shared__ uint32_t hist[kOrderBuckets];
+  for (int i = threadIdx.x; i < kOrderBuckets; i += kScanThreads) hist[i] = 0u;
+  __syncthreads();
+  for (int t = beg; t < end; ++t) {
+    const uint32_t len = tc[t];
+    atomicAdd(hist + (kOrderBuckets - 1 - (int)min(len, (uint32_t)(kOrderBuckets - 1))), 1u);
+  }
+  __syncthreads();
+  static_assert(kOrderBuckets == kScanThreads, "one bucket per thread");
+  uint32_t bexcl;
+  const uint32_t hb = hist[threadIdx.x];
+  block_exclusive_scan<kScanThreads>(hb, bexcl, sw);
+  __syncthreads();
+  hist[threadIdx.x] = bexcl;
+  __syncthreads();
+  uint32_t* order = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.order);
+  for (int t = beg; t < end; ++t) {
+    const uint32_t len = tc[t];
+    const uint32_t pos = atomicAdd(hist + (kOrderBuckets - 1 - (int)min(len, (uint32_t)(kOrderBuckets - 1))), 1u);
+    order[pos] = (uint32_t)t;
   }
 }
 
@@ -737,8 +763,11 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
   // evaluates, in list order, each Gaussian on the sub-boxes it can reach (warp-uniform branches), so
   // the per-Gaussian loads and dx terms are shared by up to kBlendPix pixels per lane.
   constexpr int NT = 32 * kBlendWarps;
-  const int f = blockIdx.y;
-  const int tile = blockIdx.x;
+  // 1-D grid over (rank, frame), frame-minor: the tiles of every frame in descending list length
+  // (tile_scan_kernel), so the longest lists of all frames are dispatched first
+  const int f = (int)(blockIdx.x % (unsigned)b.n_frames);
+  const int rank = (int)(blockIdx.x / (unsigned)b.n_frames);
+  const int tile = (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.order)[rank];
   const int tx = tile % b.gx, ty = tile / b.gx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bx0 = warp * 8;                                       // column block origin, tile-relative
@@ -925,9 +954,9 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_BLEND, true, s);
   const bool dbg = b.final_T[0] || b.n_contrib[0] || b.n_eval[0] || b.debug;
   if (dbg)
-    blend_kernel<true><<<dim3(b.ntiles, F), 32 * kBlendWarps, 0, s>>>(b);
+    blend_kernel<true><<<(unsigned)(F * b.ntiles), 32 * kBlendWarps, 0, s>>>(b);
   else
-    blend_kernel<false><<<dim3(b.ntiles, F), 32 * kBlendWarps, 0, s>>>(b);
+    blend_kernel<false><<<(unsigned)(F * b.ntiles), 32 * kBlendWarps, 0, s>>>(b);
   note_launches(1);
   prof_mark(FGS_STAGE_BLEND, false, s);
   return cudaGetLastError();
