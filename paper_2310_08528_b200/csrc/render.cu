@@ -525,10 +525,12 @@ __device__ __forceinline__ void warp_merge(const unsigned long long* a, int na, 
 // Longer lists are queued for long_sort_kernel.
 constexpr int kTileSortWarps = 4;
 __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __grid_constant__ RenderBatch b) {
-  const int f = blockIdx.y;
+  // 1-D grid over (rank group, frame), frame-minor, tiles in descending list length (as the blend)
+  const int f = (int)(blockIdx.x % (unsigned)b.n_frames);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kTileSortWarps + warp;
-  if (tile >= b.ntiles) return;                 // no CTA-wide barriers below
+  const int rank = (int)(blockIdx.x / (unsigned)b.n_frames) * kTileSortWarps + warp;
+  if (rank >= b.ntiles) return;                 // no CTA-wide barriers below
+  const int tile = (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.order)[rank];
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
   if (L <= 1) return;
@@ -941,7 +943,7 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   note_launches(1);
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
-  tile_sort_kernel<<<dim3((b.ntiles + kTileSortWarps - 1) / kTileSortWarps, F), 32 * kTileSortWarps, 0, s>>>(b);
+  tile_sort_kernel<<<(unsigned)(F * ((b.ntiles + kTileSortWarps - 1) / kTileSortWarps)), 32 * kTileSortWarps, 0, s>>>(b);
   // long lists: persistent CTAs (3 per SM over the batch) walk each frame's worklist (usually empty)
   // (per call: the attribute is per device, and the calling thread's current device may change)
   const cudaError_t attr = cudaFuncSetAttribute(long_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
