@@ -19,7 +19,8 @@ constexpr int kLargeSortThreads = 256;       // CTA sort of lists longer than th
 struct WsLayout {
   int64_t n = 0, cap = 0;
   int width = 0, height = 0, gx = 0, gy = 0, ntiles = 0;
-  size_t cnt = 0;            // uint32[16]: 0 n, 1 M clamped to cap, 2 overflow flag, 3 M raw, 4 long lists
+  size_t cnt = 0;            // uint32[16]: 0 n, 1 M clamped to cap, 2 overflow flag, 3 M raw, 4 long lists,
+                             // 5 (frame 0) long-list claim counter of the batch
   size_t keys = 0;           // uint32[n] depth key (IEEE bits of fp32 view depth), gid order
   size_t tt = 0;             // uint32[n] tiles_touched
   size_t rect = 0;           // uint2[n]  (x0 | y0<<16, x1 | y1<<16)

@@ -640,13 +640,27 @@ __device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned lo
   }
 }
 
+// Persistent CTAs share ONE queue over the long lists of all frames of the batch (frame 0's cnt[5] is
+// the claim counter, zeroed by clear_kernel), so frames with many long lists do not leave the CTAs of
+// frames with few idle; within a frame the worklist is roughly longest-first (tile_sort_kernel runs
+// the tiles in descending length order).
 __global__ void __launch_bounds__(kLargeSortThreads) long_sort_kernel(const __grid_constant__ RenderBatch b) {
   extern __shared__ unsigned long long long_sm[];
-  const int f = blockIdx.y;
-  const uint32_t n_long = cnt_ptr(b, f)[4];
-  const uint32_t* work = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list);
-  for (uint32_t w = blockIdx.x; w < n_long; w += gridDim.x) {
-    long_sort_one(b, f, (int)work[w], long_sm);
+  __shared__ uint32_t s_item;
+  uint32_t* claim = cnt_ptr(b, 0) + 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(claim, 1u);
+    __syncthreads();
+    uint32_t w = s_item;
+    __syncthreads();
+    int f = 0;
+    for (; f < b.n_frames; ++f) {
+      const uint32_t n_long = cnt_ptr(b, f)[4];
+      if (w < n_long) break;
+      w -= n_long;
+    }
+    if (f == b.n_frames) return;                    // CTA-uniform
+    long_sort_one(b, f, (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list)[w], long_sm);
     __syncthreads();
   }
 }
@@ -949,7 +963,7 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   const cudaError_t attr = cudaFuncSetAttribute(long_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)kLongSortSmem);
   if (attr != cudaSuccess) return attr;
-  long_sort_kernel<<<dim3((unsigned)std::max(1, (3 * num_sms_current() + F - 1) / F), F), kLargeSortThreads,
+  long_sort_kernel<<<(unsigned)(3 * num_sms_current()), kLargeSortThreads,
                      kLongSortSmem, s>>>(b);
   note_launches(2);
   prof_mark(FGS_STAGE_TILE_SORT, false, s);
