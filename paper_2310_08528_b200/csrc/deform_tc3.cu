@@ -202,7 +202,7 @@ __device__ __forceinline__ void prod_sync() {   // named barrier over the produc
   asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
 }
 
-template <int FEAT, int WIDTH, bool COLOR>
+template <int FEAT, int WIDTH, bool COLOR, bool SPLIT>
 __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(const __grid_constant__ DeformBatch p) {
   using SM = Tc3Smem<WIDTH, COLOR>;
   constexpr int NOUTP = SM::NOUTP;
@@ -290,7 +290,32 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   const int64_t tiles = (count + kM - 1) / kM;
   // tile indices fit 32 bits (the host rejects ranges of >= 2^31 tiles); 32-bit loop state keeps the
   // producers' register budget for the hot loop
-  const int t_beg = (int)(tiles * blockIdx.x / gridDim.x), t_end = (int)(tiles * (blockIdx.x + 1) / gridDim.x);
+  // Work split: whole tiles per CTA when there are at least as many tiles as CTAs; otherwise (small
+  // models) CTAs take contiguous ranges of TILE-FRAMES (w = tile * n_t + f), so every SM works — at
+  // most a CTA's first and last tile are shared with its neighbours (their spatial products are then
+  // computed twice).  CTA c owns w in [w_beg, w_end).
+  const int64_t NT = p.n_t;
+  constexpr bool split = SPLIT;                    // chosen at launch: tiles < CTAs
+  int64_t w_beg, w_end;
+  if (!split) {
+    w_beg = tiles * blockIdx.x / gridDim.x * NT;
+    w_end = tiles * (blockIdx.x + 1) / gridDim.x * NT;
+  } else {
+    w_beg = tiles * NT * blockIdx.x / gridDim.x;
+    w_end = tiles * NT * (blockIdx.x + 1) / gridDim.x;
+  }
+  const int t_beg = (int)(w_beg / NT), t_end = w_end > w_beg ? (int)((w_end - 1) / NT) + 1 : t_beg;
+  auto in_range = [&](int t, int f) {
+    if (!split) return true;
+    const int64_t w = (int64_t)t * NT + f;
+    return w >= w_beg && w < w_end;
+  };
+  auto group_needs = [&](int gstart, int ng, int f) {   // some tile of the group has frame f here
+    if (!split) return true;
+    bool any = false;
+    for (int gt = 0; gt < ng; ++gt) any = any || in_range(gstart + gt, f);
+    return any;
+  };
 
   if (warp < kProdWarps) {
     // =============================================================== producers
@@ -421,6 +446,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       prod_sync<kProdThreads>();
       const bool staged = segoff[15] != 0;
       for (int f = 0; f < p.n_t; ++f) {
+        if (!group_needs(gstart, ng, f)) continue;    // CTA-uniform
         const float t = p.t[f];
         const int Tn = p.t_res;
         const float gt_ = t * (float)(Tn - 1);
@@ -456,7 +482,9 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           }
         }
         prod_sync<kProdThreads>();
-        for (int gt = 0; gt < ng; ++gt, ++it) {
+        for (int gt = 0; gt < ng; ++gt) {
+          if (!in_range(gstart + gt, f)) continue;
+          const uint32_t itc = it++;
           const float4 u4 = *reinterpret_cast<const float4*>(U + (gt * kM + row) * 4);   // one LDS.128
           const float ux = u4.x, uy = u4.y, uz = u4.z;
           float hi[MAXS][FT], lo[MAXS][FT];
@@ -505,7 +533,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             }
           }
           // A is single-buffered: wait until the MMAs of tile-frame it-1 have read it
-          if (it > 0) tc::mbar_wait(a_free, (it - 1) & 1u);
+          if (itc > 0) tc::mbar_wait(a_free, (itc - 1) & 1u);
           tc::fence_after_sync();
 #pragma unroll
           for (int l = 0; l < MAXS; ++l) {
@@ -529,10 +557,12 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       for (int gstart = t_beg; gstart < t_end; gstart += G) {
         const int ng = min(G, t_end - gstart);
         for (int f = 0; f < p.n_t; ++f) {
-          for (int gt = 0; gt < ng; ++gt, ++it) {
-            const uint32_t buf = it & 1u;
-            tc::mbar_wait(a_full, it & 1u);
-            if (it >= 2) tc::mbar_wait(d_free + buf, ((it >> 1) - 1) & 1u);
+          for (int gt = 0; gt < ng; ++gt) {
+            if (!in_range(gstart + gt, f)) continue;
+            const uint32_t itc = it++;
+            const uint32_t buf = itc & 1u;
+            tc::mbar_wait(a_full, itc & 1u);
+            if (itc >= 2) tc::mbar_wait(d_free + buf, ((itc >> 1) - 1) & 1u);
             tc::fence_after_sync();
             const uint32_t d = tmem + buf * DW;
 #ifndef FGS_EXP_NOMMA
@@ -564,7 +594,9 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     for (int gstart = t_beg; gstart < t_end; gstart += G) {
       const int ng = min(G, t_end - gstart);
       for (int f = 0; f < p.n_t; ++f) {
-        for (int gt = 0; gt < ng; ++gt, ++it) {
+        for (int gt = 0; gt < ng; ++gt) {
+          if (!in_range(gstart + gt, f)) continue;
+          const uint32_t itc = it++;
           const int64_t g = p.begin + (int64_t)(gstart + gt) * kM + row;
           const bool valid = g < p.end;
           float cx[10];
@@ -576,8 +608,8 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 #pragma unroll
             for (int c = 0; c < 3; ++c) cx[7 + c] = __ldg(p.log_scales + g * 3 + c);
           }
-          const uint32_t buf = it & 1u;
-          tc::mbar_wait(d_full + buf, (it >> 1) & 1u);
+          const uint32_t buf = itc & 1u;
+          tc::mbar_wait(d_full + buf, (itc >> 1) & 1u);
           tc::fence_after_sync();
 #ifdef FGS_EXP_NOEPI
           tc::fence_before_sync();
@@ -665,14 +697,17 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 template <int FEAT, int WIDTH, bool COLOR>
 cudaError_t launch_tc3_t(const DeformBatch& p, cudaStream_t s) {
   using SM = Tc3Smem<WIDTH, COLOR>;
-  auto kern = deform_tc3_kernel<FEAT, WIDTH, COLOR>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
-  if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (p.end - p.begin + kM - 1) / kM;
-  int64_t grid = std::min<int64_t>(sms, tiles);   // 1 CTA/SM: it owns all 512 TMEM columns
+  // 1 CTA/SM (it owns all 512 TMEM columns); fewer tiles than SMs: split tiles by frame (the colour
+  // decoders keep whole tiles)
+  const bool split = !COLOR && tiles < sms;
+  auto kern = split ? deform_tc3_kernel<FEAT, WIDTH, COLOR, !COLOR> : deform_tc3_kernel<FEAT, WIDTH, COLOR, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+  if (e != cudaSuccess) return e;
+  int64_t grid = split ? std::min<int64_t>(sms, tiles * (int64_t)p.n_t) : std::min<int64_t>(sms, tiles);
   if (grid < 1) return cudaSuccess;
   prof_mark(FGS_STAGE_DEFORM, true, s);
   kern<<<(unsigned)grid, Roles<FEAT>::THREADS, SM::TOTAL, s>>>(p);
