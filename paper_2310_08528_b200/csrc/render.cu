@@ -672,7 +672,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Eq. 4 per pixel and Gaussian; e = p2 + log2(o) with p2 = power * log2(e) (R9: skip if
+struct PixelState {
+  float T, c0, c1, c2;
+  bool done;
+  uint32_t ncon, nev;
+};
+
+// Eq. 4 for one pixel and one Gaussian; e = p2 + log2(o) with p2 = power * log2(e) (R9: skip if
 // power > 0 or alpha < 1/255; stop, without adding it, when T (1 - alpha) < 1e-4).
 //  * power > 0 cannot happen for a kept Gaussian: det > 0 and a > 0 make the conic positive definite,
 //    so power <= 0 exactly (p2 > 0 could only come from fp32 rounding at power ~ 0, where the fp64
@@ -681,48 +687,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
 //    below 1/255), which takes the decision off the ex2 latency; the two forms differ only within the
 //    ex2.approx error of the threshold, inside the parity band of reading P1.
 constexpr float kLog2AlphaMin = -7.9943534368588578f;   // log2(1/255)
-// Pixel state as float2 pairs (sub-boxes k = 2p, 2p+1 of a lane): T2 = transmittance, C* = colour.
-// A finished pixel is marked by a NEGATIVE T (its final transmittance negated), so "live" is T > 0
-// (a live T never falls below 1e-4) and the Eq. 4 step needs no separate done flag.
-// One Eq. 4 step for pixel (T, c0..c2) on exponent e: skip if alpha < 1/255
-// or done; stop (and mark done) before adding the Gaussian whose T' < 1e-4.
 template <bool DBG>
-__device__ __forceinline__ void blend_step1(float& T, float& c0, float& c1, float& c2, float e, float r, float g,
-                                            float bch, uint32_t pos, uint32_t& ncon, uint32_t& nev) {
-  const bool ok = e >= kLog2AlphaMin && T > 0.f;
-  const float a = ok ? fminf(kAlphaMax, ex2_approx(e)) : 0.f;
-  const float tt = fmaf(-a, T, T);
-  const bool st = ok && tt < kTMin;
-  const float w = (st ? 0.f : a) * T;
-  c0 = fmaf(r, w, c0);
-  c1 = fmaf(g, w, c1);
-  c2 = fmaf(bch, w, c2);
-  if (DBG) {
-    ncon += (ok && !st) ? 1u : 0u;
-    if (st) nev = pos;
+__device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, float r, float g, float bch,
+                                           uint32_t pos) {
+  (void)lo;
+  const float alpha = fminf(kAlphaMax, ex2_approx(e));
+  const bool ok = !s.done && e >= kLog2AlphaMin;
+  const float test_T = fmaf(-alpha, s.T, s.T);
+  const bool stop = ok && test_T < kTMin;
+  if (ok && !stop) {
+    const float w = alpha * s.T;
+    s.c0 = fmaf(r, w, s.c0);
+    s.c1 = fmaf(g, w, s.c1);
+    s.c2 = fmaf(bch, w, s.c2);
+    s.T = test_T;
+    if (DBG) s.ncon += 1u;
   }
-  T = st ? -T : tt;
-}
-// The same step for both pixels of a pair, the FP32 work packed two lanes per instruction.
-template <bool DBG>
-__device__ __forceinline__ void blend_step2(float2& T, float2& c0, float2& c1, float2& c2, float2 e, float r,
-                                            float g, float bch, uint32_t pos, uint32_t* ncon, uint32_t* nev) {
-  const bool ok0 = e.x >= kLog2AlphaMin && T.x > 0.f, ok1 = e.y >= kLog2AlphaMin && T.y > 0.f;
-  const float a0 = ok0 ? fminf(kAlphaMax, ex2_approx(e.x)) : 0.f;
-  const float a1 = ok1 ? fminf(kAlphaMax, ex2_approx(e.y)) : 0.f;
-  const float2 tt = ffma2(make_float2(-a0, -a1), T, T);
-  const bool st0 = ok0 && tt.x < kTMin, st1 = ok1 && tt.y < kTMin;
-  const float2 w = fmul2(make_float2(st0 ? 0.f : a0, st1 ? 0.f : a1), T);
-  c0 = ffma2(make_float2(r, r), w, c0);
-  c1 = ffma2(make_float2(g, g), w, c1);
-  c2 = ffma2(make_float2(bch, bch), w, c2);
-  if (DBG) {
-    ncon[0] += (ok0 && !st0) ? 1u : 0u;
-    ncon[1] += (ok1 && !st1) ? 1u : 0u;
-    if (st0) nev[0] = pos;
-    if (st1) nev[1] = pos;
+  if (stop) {
+    s.done = true;
+    if (DBG) s.nev = pos;
   }
-  T = make_float2(st0 ? -T.x : tt.x, st1 ? -T.y : tt.y);
 }
 
 // Conservative ellipse-vs-box cull: a half-box is skipped only if q2(d) = qa dx^2 + qb dx dy + qc dy^2
@@ -801,24 +785,16 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
   const float lx = (float)lxi, ly = (float)lyi;
   const float bxl = (float)bx0, bxh = (float)(bx0 + 7);
   uint32_t n_tested = 0, n_evald = 0;    // DBG: per-warp cull statistics (sub-box evaluations)
-  static_assert(kBlendPix == 4, "pixel pairs (0,1), (2,3)");
-  float2 T2[2], C0[2], C1[2], C2[2];
-  uint32_t ncon[kBlendPix], nev[kBlendPix];
+  PixelState P[kBlendPix];
 #pragma unroll
   for (int k = 0; k < kBlendPix; ++k) {
     const bool in = pxi < b.width && py0 + 4 * k < b.height;
-    const float t0 = in ? 1.f : -1.f;     // pixels outside the image start finished
-    if (k & 1) T2[k >> 1].y = t0; else T2[k >> 1].x = t0;
-    ncon[k] = 0u;
-    nev[k] = (uint32_t)L;
+    P[k] = PixelState{1.f, 0.f, 0.f, 0.f, !in, 0u, (uint32_t)L};
   }
-#pragma unroll
-  for (int q = 0; q < 2; ++q) C0[q] = C1[q] = C2[q] = make_float2(0.f, 0.f);
-  auto Tk = [&](int k) { return (k & 1) ? T2[k >> 1].y : T2[k >> 1].x; };
   auto all_done = [&]() {
     bool d = true;
 #pragma unroll
-    for (int k = 0; k < kBlendPix; ++k) d = d && !(Tk(k) > 0.f);
+    for (int k = 0; k < kBlendPix; ++k) d = d && P[k].done;
     return d;
   };
   for (int start = 0; start < L; start += BATCH) {
@@ -844,7 +820,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
       uint32_t live = 0;
 #pragma unroll
       for (int k = 0; k < kBlendPix; ++k)
-        if (__any_sync(0xffffffffu, Tk(k) > 0.f)) live |= 1u << k;
+        if (__any_sync(0xffffffffu, !P[k].done)) live |= 1u << k;
       if (!live) break;
       const int jt = c0 + lane;
       uint32_t need = 0;
@@ -875,22 +851,11 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         const float dy0 = a.y - ly;
         const uint32_t pos = (uint32_t)(start + j + 1);
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const int k0 = 2 * pp, k1 = 2 * pp + 1;
-          const bool n0 = (mk[k0] >> bit) & 1u, n1 = (mk[k1] >> bit) & 1u;   // warp-uniform
-          if (n0 && n1) {
-            const float2 dy = fadd2(make_float2(dy0, dy0), make_float2(-4.f * k0, -4.f * k1));
-            const float2 e = ffma2(dy, ffma2(make_float2(q.x, q.x), dy, make_float2(bdx, bdx)),
-                                   make_float2(base, base));
-            blend_step2<DBG>(T2[pp], C0[pp], C1[pp], C2[pp], e, q.z, q.w, bch, pos, ncon + k0, nev + k0);
-          } else if (n0) {
-            const float dy = dy0 - 4.f * k0;
+        for (int k = 0; k < kBlendPix; ++k) {
+          if ((mk[k] >> bit) & 1u) {
+            const float dy = dy0 - 4.f * k;
             const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
-            blend_step1<DBG>(T2[pp].x, C0[pp].x, C1[pp].x, C2[pp].x, e, q.z, q.w, bch, pos, ncon[k0], nev[k0]);
-          } else if (n1) {
-            const float dy = dy0 - 4.f * k1;
-            const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
-            blend_step1<DBG>(T2[pp].y, C0[pp].y, C1[pp].y, C2[pp].y, e, q.z, q.w, bch, pos, ncon[k1], nev[k1]);
+            blend_step<DBG>(P[k], e, q.y, q.z, q.w, bch, pos);
           }
         }
       }
@@ -906,20 +871,17 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
   const FrameCam& cm = b.cam[f];
 #pragma unroll
   for (int k = 0; k < kBlendPix; ++k) {
+    const PixelState& s = P[k];
     const int py = py0 + 4 * k;
     if (!(pxi < b.width && py < b.height)) continue;
-    const float T = fabsf(Tk(k));           // a finished pixel holds its final T negated
-    const float c0 = (k & 1) ? C0[k >> 1].y : C0[k >> 1].x;
-    const float c1 = (k & 1) ? C1[k >> 1].y : C1[k >> 1].x;
-    const float c2 = (k & 1) ? C2[k >> 1].y : C2[k >> 1].x;
     const size_t pix = (size_t)py * b.width + pxi;
-    img[pix] = c0 + T * cm.bg[0];
-    img[hw + pix] = c1 + T * cm.bg[1];
-    img[2 * hw + pix] = c2 + T * cm.bg[2];
+    img[pix] = s.c0 + s.T * cm.bg[0];
+    img[hw + pix] = s.c1 + s.T * cm.bg[1];
+    img[2 * hw + pix] = s.c2 + s.T * cm.bg[2];
     if (DBG) {
-      if (b.final_T[f]) b.final_T[f][pix] = T;
-      if (b.n_contrib[f]) b.n_contrib[f][pix] = ncon[k];
-      if (b.n_eval[f]) b.n_eval[f][pix] = nev[k];
+      if (b.final_T[f]) b.final_T[f][pix] = s.T;
+      if (b.n_contrib[f]) b.n_contrib[f][pix] = s.ncon;
+      if (b.n_eval[f]) b.n_eval[f][pix] = s.nev;
     }
   }
 }
