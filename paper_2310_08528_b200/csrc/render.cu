@@ -624,6 +624,16 @@ __device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned lo
   unsigned long long* A = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
   unsigned long long* B = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst2) + rg.x;
   for (int c0 = 0; c0 < L; c0 += kCtaSortMax) cta_sort(A + c0, A + c0, min(kCtaSortMax, L - c0), sm, sm + kCtaSortMax);
+  if (L > kCtaSortMax && L <= 2 * kCtaSortMax) {
+    // two sorted segments: both back into shared memory and one merge-path merge straight into the
+    // list (the merge reads shared memory, not dependent L2 loads as the global levels below)
+    const int L1 = L - kCtaSortMax;
+    for (int q = threadIdx.x; q < L; q += kLargeSortThreads) sm[q] = A[q];
+    __syncthreads();
+    block_merge(sm, kCtaSortMax, sm + kCtaSortMax, L1, A, threadIdx.x, kLargeSortThreads);
+    __syncthreads();
+    return;
+  }
   unsigned long long* src = A;
   unsigned long long* dst = B;
   for (int w = kCtaSortMax; w < L; w <<= 1) {
