@@ -502,27 +502,33 @@ def test_deform_l2_fallback_bit_identical_to_staged_lines():
 
 
 @pytest.mark.parametrize("heads", [False, True])
-def test_frames_host_equals_device_path(heads):
+def test_frames_host_equals_device_path(heads, F=9):
     """fgs_frames_host (host model in, host images out; copies overlapped with rendering on a side
     stream) gives the device path's images bit for bit, with and without the P:1232 decoders."""
     import torch
     from paper_2310_08528_b200.inputs import with_colour_heads
-    s = make_scene("dnerf", n=15_000, width=144, height=112, n_frames=9)
+    s = make_scene("dnerf", n=15_000, width=144, height=112, n_frames=F)
     if heads:
         s = with_colour_heads(s, 0.1, 0.2)
     ds = _ds(s)
-    scratch, _ = ds.alloc_deformed(9)
-    imgs = [torch.empty((3, 112, 144), device="cuda") for _ in range(9)]
-    ws = ds.alloc_workspace(9)
+    scratch, _ = ds.alloc_deformed(F)
+    imgs = [torch.empty((3, 112, 144), device="cuda") for _ in range(F)]
+    ws = ds.alloc_workspace(F)
     fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, scratch, imgs, ws)
     hs = fgs.HostScene(s)
-    himgs = [torch.full((3, 112, 144), float("nan")).pin_memory() for _ in range(9)]
-    nbytes = fgs.fgs_frames_host_workspace_bytes(hs.g, hs.field, hs.mlp, 9, 144, 112, 16 * s.n)
+    himgs = [torch.full((3, 112, 144), float("nan")).pin_memory() for _ in range(F)]
+    nbytes = fgs.fgs_frames_host_workspace_bytes(hs.g, hs.field, hs.mlp, F, 144, 112, 16 * s.n)
     dws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     fgs.fgs_frames_host(hs.g, hs.field, hs.mlp, hs.times, hs.cams, himgs, dws)
     torch.cuda.synchronize()
     for a, b in zip(imgs, himgs):
         assert torch.equal(a.cpu(), b)
+
+
+def test_frames_host_long_batch():
+    """The host path over a batch longer than one render launch (37 frames: chunks 1, 2, 4, 4, ...
+    across the 32-frame launch limit) equals the device path bit for bit."""
+    test_frames_host_equals_device_path(False, F=37)
 
 
 def test_frames_cuda_graph_capture_and_replay():
