@@ -502,12 +502,12 @@ def test_deform_l2_fallback_bit_identical_to_staged_lines():
 
 
 @pytest.mark.parametrize("heads", [False, True])
-def test_frames_host_equals_device_path(heads, F=9):
+def test_frames_host_equals_device_path(heads, F=9, n=15_000):
     """fgs_frames_host (host model in, host images out; copies overlapped with rendering on a side
     stream) gives the device path's images bit for bit, with and without the P:1232 decoders."""
     import torch
     from paper_2310_08528_b200.inputs import with_colour_heads
-    s = make_scene("dnerf", n=15_000, width=144, height=112, n_frames=F)
+    s = make_scene("dnerf", n=n, width=144, height=112, n_frames=F)
     if heads:
         s = with_colour_heads(s, 0.1, 0.2)
     ds = _ds(s)
@@ -523,6 +523,12 @@ def test_frames_host_equals_device_path(heads, F=9):
     torch.cuda.synchronize()
     for a, b in zip(imgs, himgs):
         assert torch.equal(a.cpu(), b)
+
+
+def test_frames_host_ragged_model():
+    """The host path on a model spanning more than two Gaussian tiles per SM with a ragged last tile
+    (n = 60,001): same images as the device path bit for bit."""
+    test_frames_host_equals_device_path(False, F=5, n=60_001)
 
 
 def test_frames_host_long_batch():
