@@ -111,7 +111,7 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ sh, float X,
 // [bx0,bx1) x [by0,by1); when it holds at most kAggTiles tiles (spatially ordered models: a CTA's
 // Gaussians are neighbours), per-tile sums are formed in shared memory and each touched tile gets one
 // global atomic; otherwise every instance goes to global memory directly.
-constexpr int kAggTiles = 2048;
+constexpr int kAggTiles = 4096;
 struct AggBox {
   int x0, y0, x1, y1;
 };
