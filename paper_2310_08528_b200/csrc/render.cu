@@ -425,10 +425,18 @@ __device__ __forceinline__ int pow2_at_least(int v) {
 // partners at distance j < R are compare-exchanged inside a thread and those at j >= R are exchanged
 // with shuffles (lane ^ j/R) — and writes it back in place.  Longer lists are queued for
 // long_sort_kernel.
-// Compare-exchange of two 64-bit keys: (a, c) <- (min, max) if up else (max, min).
-__device__ __forceinline__ void cmp_swap(unsigned long long& a, unsigned long long& c, bool up) {
+//
+// The network runs on 32-bit words, not on the 64-bit (depth_key << 32 | gid) instances: word e =
+// ((depth_key - min) >> s) << log2(N2) | e, the list's depth keys relative to its minimum, shifted
+// right by the s bits that do not fit next to the slot index e.  The map from depth key to prefix is
+// monotone, so the words order the list by (depth key, gid) except inside groups of equal prefix,
+// whose members come out in slot order; each sorted word's slot then fetches its 64-bit instance, and
+// only when two neighbours share a prefix (an exact depth tie, or s > 0 and a near one) does an
+// odd-even transposition over the written list put every such group in (depth key, gid) order.
+// Half the registers, shuffles and compare instructions of the 64-bit network.
+__device__ __forceinline__ void cmp_swap(uint32_t& a, uint32_t& c, bool up) {
   const bool sw = (a > c) == up;
-  const unsigned long long lo = sw ? c : a, hi = sw ? a : c;
+  const uint32_t lo = sw ? c : a, hi = sw ? a : c;
   a = lo;
   c = hi;
 }
@@ -437,11 +445,25 @@ template <int R>
 __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsigned long long* dst, int L,
                                             int lane) {
   constexpr int N2 = 32 * R;
-  unsigned long long v[R];
+  constexpr int LB = R == 1 ? 5 : R == 2 ? 6 : R == 4 ? 7 : R == 8 ? 8 : 9;   // log2(N2)
+  static_assert((1 << LB) == N2, "slot bits");
+  uint32_t hk[R];
+  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = R * lane + r;
-    v[r] = e < L ? src[e] : ~0ull;
+    hk[r] = e < L ? (uint32_t)(src[e] >> 32) : 0u;
+    if (e < L) { mn = min(mn, hk[r]); mx = max(mx, hk[r]); }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  const uint32_t range = mx - mn;                       // L >= 1: mn <= mx
+  const int s = max(0, (32 - __clz(range)) - (32 - LB));
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * lane + r;
+    v[r] = e < L ? (((hk[r] - mn) >> s) << LB) | (uint32_t)e : 0xFFFFFFFFu;
   }
   // k < R: every stage is thread-local and every direction a compile-time function of r
 #pragma unroll
@@ -464,7 +486,7 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
       const bool keep_min = ((lane & jl) == 0) == up;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], jl);
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], jl);
         const bool lt = v[r] < o;
         v[r] = (lt == keep_min) ? v[r] : o;
       }
@@ -479,10 +501,42 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
       }
     }
   }
+  // slots -> instances (all fetched before any write: src may alias dst), then prefix ties
+  unsigned long long out[R];
+  bool tie = false;
+  const uint32_t next0 = __shfl_down_sync(0xffffffffu, v[0], 1);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = R * lane + r;
-    if (e < L) dst[e] = v[r];
+    out[r] = e < L ? src[v[r] & (uint32_t)(N2 - 1)] : 0ull;
+    const uint32_t nx = r + 1 < R ? v[r + 1 < R ? r + 1 : r] : next0;
+    if (e + 1 < L && (v[r] >> LB) == (nx >> LB)) tie = true;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * lane + r;
+    if (e < L) dst[e] = out[r];
+  }
+  if (__any_sync(0xffffffffu, tie)) {
+    // odd-even transposition restricted to neighbours of equal prefix, until no swap (rare: ties)
+    __syncwarp();
+    for (;;) {
+      bool swapped = false;
+#pragma unroll 1
+      for (int ph = 0; ph < 2; ++ph) {
+        for (int e = 2 * lane + ph; e + 1 < L; e += 64) {
+          const unsigned long long x = dst[e], y = dst[e + 1];
+          if (((((uint32_t)(x >> 32) - mn) >> s) == (((uint32_t)(y >> 32) - mn) >> s)) && x > y) {
+            dst[e] = y;
+            dst[e + 1] = x;
+            swapped = true;
+          }
+        }
+        __syncwarp();
+      }
+      if (!__any_sync(0xffffffffu, swapped)) break;
+    }
   }
 }
 
@@ -519,10 +573,9 @@ __device__ __forceinline__ void warp_merge(const unsigned long long* a, int na, 
 }
 
 // One warp per tile.  Lists of up to 256 keys are sorted by one register network; longer ones (up to
-// sort_cap <= 1024) as runs of 256 sorted in registers into the warp's shared buffer and merged
-// pairwise by merge path — 2 runs: straight to the list in global memory; 3-4 runs: the first level
-// writes the two 512-runs to the list itself, which is copied back (coalesced) for the last level.
-// Longer lists are queued for long_sort_kernel.
+// sort_cap <= 1024) as two runs sorted in registers into the warp's shared buffer (256-key runs up to
+// 512, 512-key runs beyond: one merge level either way) and merged by merge path straight into the
+// list.  Longer lists are queued for long_sort_kernel.
 constexpr int kTileSortWarps = 4;
 __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __grid_constant__ RenderBatch b) {
   // 1-D grid over (rank group, frame), frame-minor, tiles in descending list length (as the blend)
@@ -546,22 +599,17 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
     warp_sort_upto256(inst, inst, L, lane);
     return;
   }
+  // two runs sorted in registers into the warp's shared buffer (256 + up to 256, or 512 + up to 512,
+  // each by the smallest network that holds it), one merge-path merge into the list
   __shared__ unsigned long long buf[kTileSortWarps][kBlendSortMax];
   unsigned long long* A = buf[warp];
-  for (int c0 = 0; c0 < L; c0 += 256) warp_sort_upto256(inst + c0, A + c0, min(256, L - c0), lane);
+  const int h = L <= 512 ? 256 : 512;
+  if (h == 256) warp_sort_upto256(inst, A, 256, lane);
+  else warp_sort_tile<16>(inst, A, 512, lane);
+  if (L - h <= 256) warp_sort_upto256(inst + h, A + h, L - h, lane);
+  else warp_sort_tile<16>(inst + h, A + h, L - h, lane);
   __syncwarp();
-  if (L > 512) {
-    // level 1: runs (0,1) and (2,3) -> two sorted 512-runs in the list's own storage
-    warp_merge(A, 256, A + 256, 256, inst, lane);
-    warp_merge(A + 512, min(256, L - 512), A + 768, max(0, L - 768), inst + 512, lane);
-    __syncwarp();
-    __threadfence_block();
-    for (int q = lane; q < L; q += 32) A[q] = inst[q];
-    __syncwarp();
-    warp_merge(A, 512, A + 512, L - 512, inst, lane);
-  } else {
-    warp_merge(A, 256, A + 256, L - 256, inst, lane);
-  }
+  warp_merge(A, h, A + h, L - h, inst, lane);
 }
 
 // Lists longer than b.sort_cap: one CTA (8 warps) per list, persistent over the frame's worklist.
