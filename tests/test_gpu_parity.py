@@ -224,6 +224,42 @@ def test_long_list_sort_path_matches(cap):
         assert np.array_equal(out[k], base[k]), k
 
 
+@pytest.mark.parametrize("cap", [None, 100])
+def test_sort_exact_and_near_depth_ties(cap):
+    """The tile sort's 32-bit prefix words (depth key relative to the list minimum, shifted right when
+    the list's depth range does not fit beside the slot index): groups of Gaussians at bit-identical
+    depths (exact ties, ordered by index) and Gaussians along view rays from depth 0.5 to 500 (wide
+    ranges: shifted prefixes, near ties resolved on the full key) give the oracle's (tile, depth,
+    index) lists bit for bit, through the warp sorts and (cap 100) the long-list sort."""
+    s = with_heads(make_scene("tiny", n=3000, width=64, height=64), 0.0)   # zero heads: means as given
+    rng = np.random.default_rng(7)
+    i = 0
+    for k in range(40):                       # 40 groups of 2..41 copies of one mean
+        m = 2 + k
+        s.means[i:i + m] = s.means[rng.integers(i + m, s.n)]
+        i += m
+    cam = s.cameras[0]
+    idx = np.arange(2000, 2400)
+    z = np.geomspace(0.5, 500.0, idx.size)
+    u = rng.uniform(-0.4, 0.4, (idx.size, 2))
+    pc = np.stack([u[:, 0] * z, u[:, 1] * z, z], 1)
+    s.means[idx] = ((pc - cam.t.astype(np.float64)) @ cam.R.astype(np.float64)).astype(np.float32)
+    old = fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_SORT_CAP)
+    if cap is not None:
+        fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, cap)
+    try:
+        out, ref, _, _ = _render_parity(s, check_tiles=True)
+    finally:
+        fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, old)
+    tiles, gids = np.asarray(ref["tiles"]), np.asarray(ref["gids"])
+    dk = np.asarray(ref["pre"]["depth_key"]).astype(np.int64)[gids]
+    same = tiles[1:] == tiles[:-1]
+    assert np.any(same & (dk[1:] == dk[:-1])), "no exact depth ties in the lists"
+    starts = np.flatnonzero(np.r_[True, ~same])
+    spans = np.maximum.reduceat(dk, starts) - np.minimum.reduceat(dk, starts)
+    assert spans.max() >= 1 << 25, "no list with a depth range wider than the prefix bits"
+
+
 def test_long_lists_multi_run_merge():
     """A list longer than several 2048-entry runs (merge passes) sorted in global memory: many
     Gaussians piled on one tile."""
