@@ -441,30 +441,11 @@ __device__ __forceinline__ void cmp_swap(uint32_t& a, uint32_t& c, bool up) {
   c = hi;
 }
 
+// Bitonic network over the 32 R words of a warp in the blocked layout (word e = R lane + r in
+// register r): thread-local stages for partner distances j < R, shuffles (lane ^ j/R) beyond.
 template <int R>
-__device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsigned long long* dst, int L,
-                                            int lane) {
+__device__ __forceinline__ void warp_sort_words(uint32_t (&v)[R], int lane) {
   constexpr int N2 = 32 * R;
-  constexpr int LB = R == 1 ? 5 : R == 2 ? 6 : R == 4 ? 7 : R == 8 ? 8 : 9;   // log2(N2)
-  static_assert((1 << LB) == N2, "slot bits");
-  uint32_t hk[R];
-  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int e = R * lane + r;
-    hk[r] = e < L ? (uint32_t)(src[e] >> 32) : 0u;
-    if (e < L) { mn = min(mn, hk[r]); mx = max(mx, hk[r]); }
-  }
-  mn = __reduce_min_sync(0xffffffffu, mn);
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  const uint32_t range = mx - mn;                       // L >= 1: mn <= mx
-  const int s = max(0, (32 - __clz(range)) - (32 - LB));
-  uint32_t v[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int e = R * lane + r;
-    v[r] = e < L ? (((hk[r] - mn) >> s) << LB) | (uint32_t)e : 0xFFFFFFFFu;
-  }
   // k < R: every stage is thread-local and every direction a compile-time function of r
 #pragma unroll
   for (int k = 2; k < R; k <<= 1) {
@@ -501,6 +482,33 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
       }
     }
   }
+}
+
+template <int R>
+__device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsigned long long* dst, int L,
+                                            int lane) {
+  constexpr int N2 = 32 * R;
+  constexpr int LB = R == 1 ? 5 : R == 2 ? 6 : R == 4 ? 7 : R == 8 ? 8 : 9;   // log2(N2)
+  static_assert((1 << LB) == N2, "slot bits");
+  uint32_t hk[R];
+  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * lane + r;
+    hk[r] = e < L ? (uint32_t)(src[e] >> 32) : 0u;
+    if (e < L) { mn = min(mn, hk[r]); mx = max(mx, hk[r]); }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  const uint32_t range = mx - mn;                       // L >= 1: mn <= mx
+  const int s = max(0, (32 - __clz(range)) - (32 - LB));
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * lane + r;
+    v[r] = e < L ? (((hk[r] - mn) >> s) << LB) | (uint32_t)e : 0xFFFFFFFFu;
+  }
+  warp_sort_words<R>(v, lane);
   // slots -> instances (all fetched before any write: src may alias dst), then prefix ties
   unsigned long long out[R];
   bool tie = false;
@@ -617,10 +625,11 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
 // all 256 threads, ping-ponging between two shared buffers.  Longer lists: segments of kCtaSortMax
 // sorted that way in place, then merge-path levels in global memory through the inst2 scratch.
 constexpr int kCtaSortMax = 4096;
+constexpr int kCtaWordsMin = 3072;   // segments longer than this sort on 32-bit prefix words (cta_sort_words)
 constexpr size_t kLongSortSmem = 2 * kCtaSortMax * sizeof(unsigned long long);   // 64 KB dynamic
 
-__device__ __forceinline__ void block_merge(const unsigned long long* a, int na, const unsigned long long* bq,
-                                            int nb, unsigned long long* out, int t, int nt) {
+template <typename K>
+__device__ __forceinline__ void block_merge(const K* a, int na, const K* bq, int nb, K* out, int t, int nt) {
   const int n = na + nb;
   const int per = (n + nt - 1) / nt;
   const int d0 = min(n, t * per), d1 = min(n, d0 + per);
@@ -631,17 +640,101 @@ __device__ __forceinline__ void block_merge(const unsigned long long* a, int na,
     if (a[m] < bq[d0 - 1 - m]) lo = m + 1; else hi = m;
   }
   int ia = lo, ib = d0 - lo;
-  unsigned long long va = ia < na ? a[ia] : ~0ull, vb = ib < nb ? bq[ib] : ~0ull;
+  const K kmax = (K)~(K)0;
+  K va = ia < na ? a[ia] : kmax, vb = ib < nb ? bq[ib] : kmax;
   for (int d = d0; d < d1; ++d) {
     const bool ta = va < vb;
     out[d] = ta ? va : vb;
-    if (ta) { ++ia; va = ia < na ? a[ia] : ~0ull; }
-    else { ++ib; vb = ib < nb ? bq[ib] : ~0ull; }
+    if (ta) { ++ia; va = ia < na ? a[ia] : kmax; }
+    else { ++ib; vb = ib < nb ? bq[ib] : kmax; }
   }
 }
 
-// Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA.
-__device__ void cta_sort(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sA,
+// Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA, on 32-bit
+// words as the warp sorts: prefix of the depth key relative to the segment minimum (shifted right by
+// the range bits that do not fit beside 12 slot bits) | slot.  Register runs of 256 by the warps,
+// merge-path levels over all threads on the words in shared memory (unique words: exact splits), then
+// each word's slot fetches its instance and neighbours of equal prefix are put in (depth key, gid)
+// order by an odd-even transposition (skipped by a vote when there are none).  sm: kLongSortSmem.
+__device__ void cta_sort_words(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sm) {
+  static_assert(kCtaSortMax == 4096, "12 slot bits");
+  constexpr int SB = 12;
+  constexpr int NT = kLargeSortThreads, NW = NT / 32;
+  uint32_t* wA = reinterpret_cast<uint32_t*>(sm);
+  uint32_t* wB = wA + kCtaSortMax;
+  unsigned long long* stage = sm + kCtaSortMax;
+  __shared__ uint32_t s_mn, s_mx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+  for (int q = threadIdx.x; q < L; q += NT) {
+    const uint32_t h = (uint32_t)(src[q] >> 32);
+    mn = min(mn, h);
+    mx = max(mx, h);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (threadIdx.x == 0) { s_mn = 0xFFFFFFFFu; s_mx = 0u; }
+  __syncthreads();
+  if (lane == 0) { atomicMin(&s_mn, mn); atomicMax(&s_mx, mx); }
+  __syncthreads();
+  mn = s_mn;
+  mx = s_mx;
+  const int s = max(0, (32 - __clz(mx - mn)) - (32 - SB));
+  for (int r0 = warp * 256; r0 < L; r0 += NW * 256) {
+    const int l = min(256, L - r0);
+    uint32_t v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = 8 * lane + r;
+      v[r] = e < l ? (((((uint32_t)(src[r0 + e] >> 32)) - mn) >> s) << SB) | (uint32_t)(r0 + e) : 0xFFFFFFFFu;
+    }
+    warp_sort_words<8>(v, lane);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = 8 * lane + r;
+      if (e < l) wA[r0 + e] = v[r];
+    }
+  }
+  __syncthreads();
+  uint32_t* A = wA;
+  uint32_t* B = wB;
+  for (int w = 256; w < L; w <<= 1) {
+    for (int s0 = 0; s0 < L; s0 += 2 * w) {
+      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
+      block_merge<uint32_t>(A + s0, na, A + s0 + na, nb, B + s0, threadIdx.x, NT);
+    }
+    __syncthreads();
+    uint32_t* t = A; A = B; B = t;
+  }
+  bool tie = false;
+  for (int q = threadIdx.x; q < L; q += NT) {
+    stage[q] = src[A[q] & ((1u << SB) - 1u)];
+    if (q + 1 < L && (A[q] >> SB) == (A[q + 1] >> SB)) tie = true;
+  }
+  if (__syncthreads_or(tie)) {
+    for (;;) {
+      bool swapped = false;
+      for (int ph = 0; ph < 2; ++ph) {
+        for (int e = 2 * threadIdx.x + ph; e + 1 < L; e += 2 * NT) {
+          const unsigned long long x = stage[e], y = stage[e + 1];
+          if (((((uint32_t)(x >> 32)) - mn) >> s) == ((((uint32_t)(y >> 32)) - mn) >> s) && x > y) {
+            stage[e] = y;
+            stage[e + 1] = x;
+            swapped = true;
+          }
+        }
+        __syncthreads();
+      }
+      if (!__syncthreads_or(swapped)) break;
+    }
+  }
+  for (int q = threadIdx.x; q < L; q += NT) dst[q] = stage[q];
+  __syncthreads();
+}
+
+// Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA on the 64-bit
+// instances (segments up to kCtaWordsMin: the word path's range pass and staging cost more there).
+__device__ void cta_sort_keys(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sA,
                          unsigned long long* sB) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kLargeSortThreads / 32;
@@ -655,7 +748,7 @@ __device__ void cta_sort(const unsigned long long* src, unsigned long long* dst,
     unsigned long long* out = last ? dst : B;
     for (int s0 = 0; s0 < L; s0 += 2 * w) {
       const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
-      block_merge(A + s0, na, A + s0 + na, nb, out + s0, threadIdx.x, kLargeSortThreads);
+      block_merge<unsigned long long>(A + s0, na, A + s0 + na, nb, out + s0, threadIdx.x, kLargeSortThreads);
     }
     __syncthreads();
     unsigned long long* t = A; A = B; B = t;
@@ -671,7 +764,11 @@ __device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned lo
   const int L = (int)(rg.y - rg.x);
   unsigned long long* A = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst) + rg.x;
   unsigned long long* B = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst2) + rg.x;
-  for (int c0 = 0; c0 < L; c0 += kCtaSortMax) cta_sort(A + c0, A + c0, min(kCtaSortMax, L - c0), sm, sm + kCtaSortMax);
+  for (int c0 = 0; c0 < L; c0 += kCtaSortMax) {
+    const int l = min(kCtaSortMax, L - c0);
+    if (l > kCtaWordsMin) cta_sort_words(A + c0, A + c0, l, sm);
+    else cta_sort_keys(A + c0, A + c0, l, sm, sm + kCtaSortMax);
+  }
   if (L > kCtaSortMax && L <= 2 * kCtaSortMax) {
     // two sorted segments: both back into shared memory and one merge-path merge straight into the
     // list (the merge reads shared memory, not dependent L2 loads as the global levels below)

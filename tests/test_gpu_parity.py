@@ -260,10 +260,17 @@ def test_sort_exact_and_near_depth_ties(cap):
     assert spans.max() >= 1 << 25, "no list with a depth range wider than the prefix bits"
 
 
-def test_long_lists_multi_run_merge():
+@pytest.mark.parametrize("ties", [False, True])
+def test_long_lists_multi_run_merge(ties):
     """A list longer than several 2048-entry runs (merge passes) sorted in global memory: many
-    Gaussians piled on one tile."""
+    Gaussians piled on one tile (segments of 4096 on the 32-bit prefix-word CTA sort); with ties,
+    groups of bit-identical depths inside those segments (the word sort's tie fixup)."""
     s = make_scene("tiny", n=9000, width=32, height=32)
+    if ties:
+        s = with_heads(s, 0.0)
+        rng = np.random.default_rng(5)
+        for k in range(60):
+            s.means[100 * k:100 * k + 2 + k] = s.means[rng.integers(6100, s.n)]
     ds = _ds(s)
     dstruct, g, _ = gpu_deform(ds, float(s.times[0]))
     out = gpu_render_debug(ds, s.cameras[0], dstruct)
