@@ -210,8 +210,8 @@ enum {
   FGS_STAGE_PREPROCESS,         /* counter clear + preprocess incl. per-tile instance counts (a4)   */
   FGS_STAGE_TILE_SCAN,          /* scan of the tile counts -> ranges (a7)                           */
   FGS_STAGE_DUPLICATE,          /* key duplication into tile buckets (a5)                           */
-  FGS_STAGE_TILE_SORT,          /* global-memory sort of tile lists longer than the smem cap (a6)   */
-  FGS_STAGE_BLEND,              /* per-tile (depth, index) sort in smem (a6) + alpha blending (a8)  */
+  FGS_STAGE_TILE_SORT,          /* per-tile (depth, index) sort: warp sorts + long-list CTA sort (a6) */
+  FGS_STAGE_BLEND,              /* front-to-back alpha blending of the sorted lists (a8, Eq. 4)     */
   FGS_N_STAGES
 };
 int fgs_profile_enable(int enable);
@@ -220,8 +220,9 @@ int fgs_profile_read(double* ms, int64_t* launches);
 int64_t fgs_launch_count(void);
 
 /* ---- tuning (process-global; change only while no call of this library is enqueueing) --------
- * FGS_TUNE_TILE_SORT_CAP: tile lists of at most this many instances are sorted by (depth, index) in
- * the blend kernel's shared memory; longer lists by the global-memory sort (FGS_STAGE_TILE_SORT).
+ * FGS_TUNE_TILE_SORT_CAP: tile lists of at most this many instances are sorted by (depth, index) by
+ * one warp (registers + shared memory); longer lists by the persistent long-list CTA sort (shared-
+ * memory segments, global-memory merge levels).  Both run in FGS_STAGE_TILE_SORT.
  * Range [1, 1024], default 1024.  Results are identical for every value (tests lower it to exercise
  * the long-list path).  fgs_set_tuning returns FGS_E_INVALID for an unknown key or a value out of
  * range; fgs_get_tuning returns -1 for an unknown key.

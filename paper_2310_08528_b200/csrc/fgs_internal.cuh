@@ -12,7 +12,7 @@ constexpr int kMaxFrames = 32;               // frames per launch (kernel-parame
 constexpr int kMaxPeers = 8;                 // replicas of the deform outputs (fgs_deform_range_peers)
 constexpr int kScanThreads = 1024;           // tile-count scan CTA (one per frame)
 constexpr int kBlendThreads = 128;           // blend CTA: 4 warps x 8x8 pixel boxes of a 16x16 tile
-constexpr int kBlendSortMax = 1024;          // longest tile list the blend sorts in shared memory
+constexpr int kBlendSortMax = 1024;          // longest tile list one warp sorts (tile_sort_kernel); longer: long_sort_kernel
 constexpr int kLargeSortThreads = 256;       // CTA sort of lists longer than the warp-sort cap
 
 // Per-frame workspace layout (all offsets in bytes from the frame's slice, 256-B aligned).

@@ -13,8 +13,9 @@
 //                tile bucket of its rect, at an atomically claimed slot.  The order
 //                inside a bucket is arbitrary here; the sort below makes it unique.
 //   tile sort    (a6) every tile's list sorted ascending by (depth key, gid): lists of up to
-//                sort_cap instances by a bitonic sort in the blend CTA's shared memory, longer
-//                lists by long_sort_kernel (shared-memory runs + merge-path merges in global memory).
+//                sort_cap instances by one warp (tile_sort_kernel: register bitonic networks on 32-bit
+//                depth-prefix words + merge path), longer lists by long_sort_kernel (shared-memory
+//                segments + merge-path merges in global memory).
 //                Result: the [3dgs] (tile, depth, index) order (reading R14), without global passes.
 //   blend        Eq. 4 front to back per pixel; 16x16 tile per CTA.
 #include <cuda_runtime.h>
