@@ -11,8 +11,10 @@ config (BASELINE.json configs[1]: 100k Gaussians, 800x800, SH 3, 20 frames per s
 Timing (rank-local, then max over ranks): W untimed warm-up steps; K timed steps, each bracketed by
 CUDA events on the launching stream, with a 512 MiB buffer written between steps (outside the
 events) to flush the 126 MB L2; barrier + torch.cuda.synchronize() on both sides of the region.
-Under torchrun (N > 1) every rank renders its own F-frame batch (frame-batch split, no collective):
-value = all frames of all ranks / max-over-ranks time ("scaling": "weak").
+Under torchrun (N > 1) the config's F-frame batch is split across the ranks (frame_split: contiguous
+chunks, no collective on the data path): value = F frames / max-over-ranks time ("scaling": "strong");
+the ranks' images are gathered to rank 0 afterwards (untimed) and checked against a one-GPU render of the
+whole batch.  --weak replicates the batch on every rank instead ("scaling": "weak").
 
 Also reported: per-stage device times (library CUDA events), the roofline of the dominant kernel,
 e2e through fgs_frames_host (pinned host buffers, copies inside the timed region), the launch
@@ -110,31 +112,34 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle (CPU) arm
-# state shared with the oracle worker processes (fork start method: inherited, not pickled)
+# state shared with the oracle worker processes (fork start method: inherited, not pickled); every stage
+# forks its pool after the state it needs is in place
 _ORACLE = {}
 
 
 def _oracle_task(task):
-    """One unit of oracle work in a worker process (single-threaded BLAS): ("deform", t, lo, hi),
-    ("pre", lo, hi) or ("blend", tiles)."""
+    """One unit of oracle work in a worker process (single-threaded BLAS):
+    ("deform", t, lo, hi) -> G' rows; ("pre", lo, hi) -> preprocess dict of rows; ("blend", tiles) ->
+    (flat pixel indices, image [3,P], final_T, n_contrib, flagged) of those tiles."""
+    import numpy as np
     from threadpoolctl import threadpool_limits
 
     import oracle
     from oracle import render as OR
-    sc, cam = _ORACLE["scene"], _ORACLE["cam"]
-    t0 = time.perf_counter()
+    st = _ORACLE
+    sc, cam = st["scene"], st["cam"]
     with threadpool_limits(1):
         if task[0] == "deform":
-            oracle.deform_ref(sc, task[1], begin=task[2], end=task[3])
-        elif task[0] == "pre":
+            return oracle.deform_ref(sc, task[1], begin=task[2], end=task[3])
+        if task[0] == "pre":
             lo, hi = task[1], task[2]
-            OR.preprocess_ref(sc.means[lo:hi], sc.log_scales[lo:hi], sc.quats[lo:hi], sc.opacity_logits[lo:hi],
-                              sc.sh[lo:hi], sc.sh_degree, cam)
-        else:
-            d = {"means": sc.means, "log_scales": sc.log_scales, "quats": sc.quats}
-            OR.render_ref(d, sc.opacity_logits, sc.sh, sc.sh_degree, cam, tiles_subset=task[1],
-                          pre=_ORACLE["pre"], full_bins=False)
-    return time.perf_counter() - t0
+            g = st["g"]
+            return OR.preprocess_ref(g["means"][lo:hi], g["log_scales"][lo:hi], g["quats"][lo:hi],
+                                     sc.opacity_logits[lo:hi], sc.sh[lo:hi], sc.sh_degree, cam)
+        out = OR.render_ref(st["g"], sc.opacity_logits, sc.sh, sc.sh_degree, cam, tiles_subset=task[1],
+                            pre=st["pre"], bins=st["bins"])
+        m = np.isfinite(out["final_T"])
+        return (np.flatnonzero(m), out["image"][:, m], out["final_T"][m], out["n_contrib"][m], out["flagged"][m])
 
 
 def oracle_procs():
@@ -144,92 +149,157 @@ def oracle_procs():
         return max(1, min(32, os.cpu_count() or 1))
 
 
-def oracle_sample(scene, frame, n_tiles, rng_seed=0, deform_per_proc=2_000, procs=None):
-    """Time the fp64 oracle on a bounded sample of one frame on `procs` host cores and extrapolate the
-    frame time (SURVEY 8(d) oracle timing (ii): a process pool over Gaussian chunks and tiles).
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
-    Sample: deform of procs x deform_per_proc Gaussians (scaled to N), preprocess of all N (chunks),
-    binning (bin_ref, serial), blend of n_tiles random tiles (scaled to all tiles).  Each stage's wall
-    time is measured around its pool map.  Returns (frame_seconds, deform_seconds_per_N, desc, procs).
-    """
+
+def oracle_full_frame(scene, frame, procs, g_render=None):
+    """The fp64 oracle on ONE FULL frame of `scene` (SURVEY 8(d) oracle timing (ii)): deform of all N
+    Gaussians (a fork pool of `procs` single-BLAS-thread workers over contiguous chunks), preprocess of all
+    N (chunks), binning (bin_ref, serial: one sort of all instances), blend of EVERY tile (the pool over
+    tile chunks, longest lists spread round-robin).  Nothing is sampled or extrapolated; each stage's wall
+    time includes forking its pool.  g_render: the G' to render (the GPU's fp32 G' for the parity summary,
+    protocol P3); default the oracle's own deform output.  Returns a dict with the per-stage seconds and
+    the oracle's outputs (deformed, pre, bins, image, final_T, n_contrib, flagged)."""
     import multiprocessing as mp
 
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     from oracle import render as OR
-
-    P = procs or oracle_procs()
+    P = procs
     N = scene.n
     cam = scene.cameras[frame]
     t = float(scene.times[frame])
-    _ORACLE.update(scene=scene, cam=cam, pre=None)
-    with threadpool_limits(1):
-        pre = OR.preprocess_ref(scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh,
-                                scene.sh_degree, cam)                  # the blend's input (not timed)
-    _ORACLE["pre"] = pre
-    gx, gy = OR.tile_grid(cam.width, cam.height)
-    rng = np.random.default_rng(rng_seed)
-    tiles = sorted(rng.choice(gx * gy, min(n_tiles, gx * gy), replace=False).tolist())
-    sub = min(N, P * deform_per_proc)
+    W, H = cam.width, cam.height
     ctx = mp.get_context("fork")
+    _ORACLE.clear()
+    _ORACLE.update(scene=scene, cam=cam)
+    sec = {}
+    # (1) deformation of all N
+    t0 = time.perf_counter()
+    edges = np.linspace(0, N, 4 * P + 1).astype(int)
     with ctx.Pool(P) as pool:
-        pool.map(_oracle_task, [("pre", 0, 1)] * P)          # start the workers (not timed)
+        parts = pool.map(_oracle_task, [("deform", t, int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a],
+                         chunksize=1)
+    deformed = {k: np.concatenate([q[k] for q in parts], axis=0) for k in parts[0]}
+    sec["deform"] = time.perf_counter() - t0
+    g = deformed if g_render is None else g_render
+    _ORACLE["g"] = g
+    # (2) preprocess of all N
+    t0 = time.perf_counter()
+    with ctx.Pool(P) as pool:
+        parts = pool.map(_oracle_task, [("pre", int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a],
+                         chunksize=1)
+    pre = {k: np.concatenate([q[k] for q in parts], axis=0) for k in parts[0]}
+    sec["preprocess"] = time.perf_counter() - t0
+    # (3) binning: instances sorted by (tile, depth key, index), tile ranges
+    t0 = time.perf_counter()
+    with threadpool_limits(1):
+        bins = OR.bin_ref(pre, cam)
+    sec["binning"] = time.perf_counter() - t0
+    _ORACLE.update(pre=pre, bins=bins)
+    # (4) blend of every tile
+    t0 = time.perf_counter()
+    gx, gy = OR.tile_grid(W, H)
+    lens = np.diff(bins[2], axis=1)[:, 0]
+    order = np.argsort(-lens, kind="stable")
+    n_chunks = min(gx * gy, 8 * P)
+    chunks = [sorted(order[i::n_chunks].tolist()) for i in range(n_chunks)]
+    img = np.full((3, H * W), np.nan)
+    fT = np.full(H * W, np.nan)
+    nc = np.full(H * W, -1, np.int64)
+    fl = np.zeros(H * W, bool)
+    with ctx.Pool(P) as pool:
+        for idx, im, T, c, f in pool.imap_unordered(_oracle_task, [("blend", ch) for ch in chunks if ch]):
+            img[:, idx] = im
+            fT[idx] = T
+            nc[idx] = c
+            fl[idx] = f
+    sec["blend"] = time.perf_counter() - t0
+    _ORACLE.clear()
+    return {"seconds": sum(sec.values()), "stages_s": sec, "deformed": deformed, "pre": pre, "bins": bins,
+            "image": img.reshape(3, H, W), "final_T": fT.reshape(H, W), "n_contrib": nc.reshape(H, W),
+            "flagged": fl.reshape(H, W), "procs": P}
 
-        def timed_map(tasks):
-            t0 = time.perf_counter()
-            pool.map(_oracle_task, tasks)
-            return time.perf_counter() - t0
-        edges = np.linspace(0, sub, P + 1).astype(int)
-        t_def = timed_map([("deform", t, int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a])
-        t_def *= N / max(sub, 1)
-        edges = np.linspace(0, N, P + 1).astype(int)
-        t_pre = timed_map([("pre", int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a])
-        chunks = [tiles[i::P] for i in range(P) if tiles[i::P]]
-        t_blend = timed_map([("blend", c) for c in chunks]) * (gx * gy) / len(tiles)
+
+def oracle_single_process(scene, frame, g, pre, bins, t_bin, n_def=2000, n_pre=20000, n_tiles=24, seed=0):
+    """SURVEY 8(d) oracle timing (i): one process, one BLAS thread, on a bounded sample of the frame,
+    scaled to the whole frame (marked extrapolated): deform of n_def Gaussians, preprocess of n_pre, the
+    binning time of the full frame (it is serial anyway), blend of n_tiles random tiles."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    import oracle
+    from oracle import render as OR
+    N = scene.n
+    cam = scene.cameras[frame]
+    t = float(scene.times[frame])
+    gx, gy = OR.tile_grid(cam.width, cam.height)
+    rng = np.random.default_rng(seed)
+    tiles = sorted(rng.choice(gx * gy, min(n_tiles, gx * gy), replace=False).tolist())
+    nd, npre = min(n_def, N), min(n_pre, N)
     with threadpool_limits(1):
         t0 = time.perf_counter()
-        OR.bin_ref(pre, cam)
-        t_bin = time.perf_counter() - t0
+        oracle.deform_ref(scene, t, begin=0, end=nd)
+        t_def = (time.perf_counter() - t0) * N / max(nd, 1)
+        t0 = time.perf_counter()
+        OR.preprocess_ref(g["means"][:npre], g["log_scales"][:npre], g["quats"][:npre], scene.opacity_logits[:npre],
+                          scene.sh[:npre], scene.sh_degree, cam)
+        t_pre = (time.perf_counter() - t0) * N / max(npre, 1)
+        t0 = time.perf_counter()
+        OR.render_ref(g, scene.opacity_logits, scene.sh, scene.sh_degree, cam, tiles_subset=tiles, pre=pre, bins=bins)
+        t_blend = (time.perf_counter() - t0) * (gx * gy) / len(tiles)
     frame_s = t_def + t_pre + t_bin + t_blend
-    desc = (f"1 frame of {scene.name} on {P} host processes: oracle deform of {sub}/{N} Gaussians "
-            f"(x{N / max(sub, 1):.0f}), preprocess of all {N}, binning (serial), blend of {len(tiles)}/{gx * gy} "
-            f"random tiles (x{gx * gy / len(tiles):.1f}) of the canonical G; fp64 numpy, 1 BLAS thread per process")
-    return frame_s, t_def, desc, P
+    return {"frames_per_s": 1.0 / frame_s, "gaussians_deformed_per_s": N / t_def, "cores": 1,
+            "extrapolated": True,
+            "sample": f"1 process, 1 BLAS thread: deform of {nd}/{N} Gaussians, preprocess of {npre}/{N}, "
+                      f"binning of the full frame, blend of {len(tiles)}/{gx * gy} random tiles, each scaled "
+                      f"to the full frame"}
 
 
 def run_reference(args, scene, rank):
+    """The reference arm for this tier: the fp64 oracle, as it stands, on the host cores.  A step is ONE
+    FULL frame of the workload (frames cycled through the batch), not a sample: value = frames / s."""
     if rank != 0:
         return
     P = oracle_procs()
-    n_tiles = 24 * P
-    for w in range(args.warmup):
-        oracle_sample(scene, w % scene.n_frames, n_tiles, rng_seed=w, procs=P)
-    frame_s = []
-    t_defs = []
-    for k in range(args.steps):
-        fs, td, desc, _ = oracle_sample(scene, k % scene.n_frames, n_tiles, rng_seed=100 + k, procs=P)
-        frame_s.append(fs)
-        t_defs.append(td)
     F = scene.n_frames
-    step_s = [F * s for s in frame_s]
-    total = sum(step_s)
-    value = F * args.steps / total
+    for w in range(args.warmup):
+        oracle_full_frame(scene, w % F, P)
+    secs, t_defs = [], []
+    for k in range(args.steps):
+        r = oracle_full_frame(scene, k % F, P)
+        secs.append(r["seconds"])
+        t_defs.append(r["stages_s"]["deform"])
+    total = sum(secs)
+    value = args.steps / total
+    sample = (f"1 full frame of {scene.name} per step (frames cycled through the {F}-frame batch): oracle deform "
+              f"of all {scene.n} Gaussians, preprocess of all, binning, blend of every tile; fp64 numpy on {P} "
+              f"host processes (1 BLAS thread each); not extrapolated")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_desc(scene), "frames_per_step": F, "parallelism": f"{P} host processes (oracle over Gaussian chunks and tiles)"},
+        "config": {"workload": workload_desc(scene), "frames_per_step": 1,
+                   "parallelism": f"{P} host processes (oracle over Gaussian chunks and tiles)"},
         "gaussians_deformed_per_s": scene.n * len(t_defs) / sum(t_defs),
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": P, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": P, "kind": "oracle", "sample": sample,
+                         "extrapolated": False, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------ GPU arm
-STAGE_KERNELS = {"deform": ["deform_tc3_kernel", "deform_tc2_kernel", "deform_tc_kernel"],
+STAGE_KERNELS = {"deform": ["deform_tc3_kernel"],
                  "preprocess": ["preprocess_kernel"], "blend": ["blend_kernel"],
                  "binning": ["tile_scan_kernel", "duplicate_kernel", "tile_sort_kernel",
                              "long_sort_kernel"]}
@@ -287,15 +357,23 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz, ste
     if t > 0:
         out["preprocess"] = {"bound": "hbm", "achieved": by_pre / t / 1e9, "peak": hbm, "unit": "GB/s",
                              "frac": by_pre / t / 1e9 / hbm, "traffic": None,
-                             "algorithmic": f"{44 + 12 * K + 72} B per Gaussian-frame"}
+                             "algorithmic": f"{44 + 12 * K + 72} B per Gaussian-frame",
+                             "limiter": "not HBM: the frame-minor grid serves the frame-invariant SH of all "
+                                        "but the first frame from L2 (ncu DRAM bytes ~0.3x the algorithmic "
+                                        "bytes); the kernel is issue-bound on L1 (l1tex ~75%), XU (~31%) and "
+                                        "FP64 (~27%) work (profiles/r02_ncu_summary.md)"}
     # blend: 9 FP32 inst per evaluated pair + 4 per contributing pair
     E, C = counts.get("evaluated_per_frame"), counts.get("contrib_per_frame")
     t = avg_launch_s("blend")
     if t > 0 and E:
         work = (9 * E + 4 * C) * F / 1e12
+        # C basis: the algorithmic minimum, as if only the contributing pairs were evaluated
+        work_c = 13 * C * F / 1e12
         out["blend"] = {"bound": "alu", "achieved": work / t, "peak": fp32_peak, "unit": "Tinst/s",
                         "frac": work / t / fp32_peak, "traffic": None,
-                        "algorithmic": f"9 inst x {E:.3g} evaluated + 4 x {C:.3g} contributing pairs per frame"}
+                        "algorithmic": f"9 inst x {E:.3g} evaluated + 4 x {C:.3g} contributing pairs per frame",
+                        "achieved_C": work_c / t, "frac_C": work_c / t / fp32_peak,
+                        "algorithmic_C": f"13 inst x {C:.3g} contributing pairs per frame (C basis)"}
     M = counts.get("instances_per_frame")
     t_sort = stage_ms.get("tile_scan", 0) + stage_ms.get("duplicate", 0) + stage_ms.get("tile_sort", 0)
     if t_sort > 0 and M:
@@ -311,40 +389,117 @@ def roofline_objects(scene, stage_ms, stage_launches, peaks, counts, sm_mhz, ste
     return out
 
 
+def _debug_render(fgs, ds, cam, dstruct, cap, dev, W, H):
+    """One untimed fgs_render_debug of a frame with every debug output (work counts, parity summary)."""
+    import torch
+    n = ds.n
+    gx, gy = (W + 15) // 16, (H + 15) // 16
+    t = {"radii": torch.zeros(n, dtype=torch.int32, device=dev), "rect": torch.zeros((n, 4), dtype=torch.int32, device=dev),
+         "depth_key": torch.zeros(n, dtype=torch.int32, device=dev),
+         "tiles_touched": torch.zeros(n, dtype=torch.int32, device=dev),
+         "n_instances": torch.zeros(1, dtype=torch.int32, device=dev),
+         "sorted_gid": torch.zeros(cap, dtype=torch.int32, device=dev),
+         "ranges": torch.zeros((gx * gy, 2), dtype=torch.int32, device=dev),
+         "final_T": torch.zeros((H, W), dtype=torch.float32, device=dev),
+         "n_contrib": torch.zeros((H, W), dtype=torch.int32, device=dev),
+         "n_evaluated": torch.zeros((H, W), dtype=torch.int32, device=dev),
+         "blend_work": torch.zeros(2, dtype=torch.int64, device=dev)}
+    aux = fgs.fgs_render_aux(**{k: v.data_ptr() for k, v in t.items()})
+    ws1 = ds.alloc_workspace(1, cap)
+    im = torch.empty((3, H, W), device=dev)
+    fgs.fgs_render_debug(cam, dstruct, im, ws1, aux)
+    fgs.fgs_render_status(ws1, 1)
+    out = {k: v.cpu().numpy() for k, v in t.items()}
+    out["image"] = im.cpu().numpy()
+    return out
+
+
+def parity_summary(scene, frame, g_gpu, dbg, orc):
+    """SURVEY 8(c.5) protocol on one whole frame, GPU vs the fp64 oracle (untimed; reported in the line):
+    deform max |err| over all N (oracle's own deform vs the GPU's G'); integer work bit-exact outside
+    boundary Gaussians — radii, rects, tiles_touched, depth keys of all N, the ordered list of every tile —
+    with the oracle fed the GPU's fp32 G' (P3); pixels over every pixel: PSNR, max |err| on pixels the
+    oracle does not flag, and the flagged count."""
+    import numpy as np
+    pre = orc["pre"]
+    n = scene.n
+    derr = max(float(np.max(np.abs(g_gpu[k].astype(np.float64) - orc["deformed"][k]))) for k in orc["deformed"])
+    keep = ~pre["boundary"]
+    mism = {
+        "radii": int(np.sum((dbg["radii"][:n] != pre["radius"]) & keep)),
+        "rect": int(np.sum(np.any(dbg["rect"][:n] != pre["rect"], axis=1) & keep)),
+        "tiles_touched": int(np.sum((dbg["tiles_touched"][:n] != pre["tiles_touched"]) & keep)),
+        "depth_key": int(np.sum((dbg["depth_key"][:n].view(np.uint32) != pre["depth_key"]) & keep)),
+    }
+    _, o_gids, o_ranges = orc["bins"]
+    bad = 0
+    for tile in range(o_ranges.shape[0]):
+        a = o_gids[o_ranges[tile, 0]:o_ranges[tile, 1]]
+        b = dbg["sorted_gid"][dbg["ranges"][tile, 0]:dbg["ranges"][tile, 1]].astype(np.int64)
+        if not np.array_equal(a[keep[a]], b[keep[b]]):
+            bad += 1
+    mism["tile_lists"] = bad
+    img, ref, flag = dbg["image"].astype(np.float64), orc["image"], orc["flagged"]
+    d = np.abs(img - ref)
+    mse = float(np.mean(d ** 2))
+    psnr = float("inf") if mse == 0 else 10 * math.log10(1.0 / mse)
+    return {"frame": frame, "deform_max_abs_err": derr, "deform_tol": 1e-4, "integer_mismatches": mism,
+            "boundary_gaussians": int(pre["boundary"].sum()), "pixels": int(flag.size), "psnr_db": psnr,
+            "psnr_min_db": 60.0, "max_abs_err_unflagged": float(d[:, ~flag].max()), "pixel_tol": 2e-3,
+            "max_abs_err_all": float(d.max()), "flagged_pixels": int(flag.sum()),
+            "final_T_max_abs_err": float(np.nanmax(np.abs(dbg["final_T"] - orc["final_T"]))),
+            "n_contrib_mismatch_unflagged": int(np.sum((dbg["n_contrib"] != orc["n_contrib"]) & ~flag)),
+            "pass": bool(derr <= 1e-4 and all(v == 0 for v in mism.values()) and psnr >= 60.0
+                         and float(d[:, ~flag].max()) <= 2e-3)}
+
+
 def run_fgs(args, scene, rank, world, local_rank):
+    import dataclasses
+
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2310_08528_b200 import build, fgs
+    from paper_2310_08528_b200.sharding import frame_split, gather_frames
 
     build.build()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    F_all = scene.n_frames
+    # (e1) frame-batch split: the config's batch is cut across ranks (strong scaling); --weak gives every
+    # rank its own copy of the whole batch instead
+    split = not args.weak
+    mine = frame_split(F_all, rank, world) if split else list(range(F_all))
+    full_scene = scene
+    scene = dataclasses.replace(scene, cameras=[scene.cameras[f] for f in mine],
+                                times=np.asarray([scene.times[f] for f in mine], np.float32))
     ds = fgs.DeviceScene(scene, dev)
     F = scene.n_frames
-    W, H = scene.cameras[0].width, scene.cameras[0].height
-    outs, outs_t = ds.alloc_deformed(F)     # keep the tensors alive (structs hold raw pointers)
+    W, H = full_scene.cameras[0].width, full_scene.cameras[0].height
+    outs, outs_t = ds.alloc_deformed(max(F, 1))     # keep the tensors alive (structs hold raw pointers)
     images = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in range(F)]
     cap = 16 * scene.n
-    ws = ds.alloc_workspace(F, cap)
+    ws = ds.alloc_workspace(max(F, 1), cap)
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)   # 512 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step_eager():
-        fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, images, ws)
+        if F:
+            fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs[:F], images, ws)
 
     for _ in range(args.warmup):
         step_eager()
-    fgs.fgs_render_status(ws, F)
+    if F:
+        fgs.fgs_render_status(ws, F)
     graph = None
     launches_per_step = None
-    if not args.no_graph:
+    if not args.no_graph and F:
         # one step captured in a CUDA graph: the timed steps replay it (same kernels, no launch gaps)
         graph = torch.cuda.CUDAGraph()
         l0 = fgs.fgs_launch_count()
         with torch.cuda.graph(graph):
-            fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, images, ws,
+            fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs[:F], images, ws,
                            stream=torch.cuda.current_stream())
         launches_per_step = fgs.fgs_launch_count() - l0
         torch.cuda.synchronize()
@@ -352,27 +507,21 @@ def run_fgs(args, scene, rank, world, local_rank):
             graph.replay()
         torch.cuda.synchronize()
 
-    # work counts of this workload (deterministic; one debug render per frame, untimed)
+    # work counts of this rank's frames (deterministic; one debug render per frame, untimed)
     counts = {"sms": torch.cuda.get_device_properties(dev).multi_processor_count}
-    if rank == 0:
+    dbg0 = None
+    if rank == 0 and F:
         Ev, Cv, Mv, Wv, Tv = [], [], [], [], []
         for fi in range(F):
-            ne = torch.zeros((H, W), dtype=torch.int32, device=dev)
-            nc = torch.zeros((H, W), dtype=torch.int32, device=dev)
-            ni = torch.zeros(1, dtype=torch.int32, device=dev)
-            bw = torch.zeros(2, dtype=torch.int64, device=dev)
-            aux = fgs.fgs_render_aux(n_evaluated=ne.data_ptr(), n_contrib=nc.data_ptr(), n_instances=ni.data_ptr(),
-                                     blend_work=bw.data_ptr())
-            ws1 = ds.alloc_workspace(1, cap)
-            im = torch.empty((3, H, W), device=dev)
-            fgs.fgs_render_debug(ds.cams[fi], outs[fi], im, ws1, aux)
-            torch.cuda.synchronize()
-            Ev.append(int(ne.sum()))
-            Cv.append(int(nc.sum()))
-            Mv.append(int(ni[0]))
-            Wv.append(int(bw[0]) * 32)
-            Tv.append(int(bw[1]))
-            del ws1
+            dbg = _debug_render(fgs, ds, ds.cams[fi], outs[fi] if _first_of_time(scene, fi) == fi
+                                else outs[_first_of_time(scene, fi)], cap, dev, W, H)
+            if fi == 0:
+                dbg0 = dbg
+            Ev.append(int(dbg["n_evaluated"].sum()))
+            Cv.append(int(dbg["n_contrib"].sum()))
+            Mv.append(int(dbg["n_instances"][0]))
+            Wv.append(int(dbg["blend_work"][0]) * 32)
+            Tv.append(int(dbg["blend_work"][1]))
         counts.update(evaluated_per_frame=float(np.mean(Ev)), contrib_per_frame=float(np.mean(Cv)),
                       instances_per_frame=float(np.mean(Mv)), blend_pixel_evals_per_frame=float(np.mean(Wv)),
                       blend_warp_tests_per_frame=float(np.mean(Tv)))
@@ -404,7 +553,8 @@ def run_fgs(args, scene, rank, world, local_rank):
         if profile:
             st = fgs.fgs_profile_read()
             fgs.fgs_profile_enable(False)
-        fgs.fgs_render_status(ws, F)
+        if F:
+            fgs.fgs_render_status(ws, F)
         per = [a.elapsed_time(b) for a, b in evs]
         timed.per_step = per
         t_ms = sum(per)
@@ -424,13 +574,14 @@ def run_fgs(args, scene, rank, world, local_rank):
         t_max, _, _ = timed(graph.replay, False)
         launches = launches_per_step * args.steps
     else:
-        t_max, launches = t_eager, launches_eager
+        t_max, launches = timed(step_eager, False)[:2]
     per_step = sorted(timed.per_step)
     step_stats = {"median": statistics.median(per_step), "p10": per_step[int(0.1 * (len(per_step) - 1))],
                   "p90": per_step[int(round(0.9 * (len(per_step) - 1)))], "unit": "ms (this rank)"}
     clk = clocks.stop()
-    value = F * args.steps * world / (t_max / 1e3)
-    value_eager = F * args.steps * world / (t_eager / 1e3)
+    frames_per_step = F_all if split else F_all * world
+    value = frames_per_step * args.steps / (t_max / 1e3)
+    value_eager = frames_per_step * args.steps / (t_eager / 1e3)
     deform_ms = stages["deform"][0]
 
     # ---- e2e through the C ABI with host (pinned) buffers ----
@@ -438,11 +589,12 @@ def run_fgs(args, scene, rank, world, local_rank):
     if not args.no_e2e:
         hs = fgs.HostScene(scene)
         himgs = [torch.empty((3, H, W), dtype=torch.float32).pin_memory() for _ in range(F)]
-        nbytes = fgs.fgs_frames_host_workspace_bytes(hs.g, hs.field, hs.mlp, F, W, H, cap)
+        nbytes = fgs.fgs_frames_host_workspace_bytes(hs.g, hs.field, hs.mlp, max(F, 1), W, H, cap)
         dws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
 
         def step_host():
-            fgs.fgs_frames_host(hs.g, hs.field, hs.mlp, hs.times, hs.cams, himgs, dws)
+            if F:
+                fgs.fgs_frames_host(hs.g, hs.field, hs.mlp, hs.times, hs.cams, himgs, dws)
 
         for _ in range(max(1, args.warmup)):
             step_host()
@@ -460,16 +612,33 @@ def run_fgs(args, scene, rank, world, local_rank):
             eev.append((a, b))
         torch.cuda.synchronize()
         e_ms = sum(a.elapsed_time(b) for a, b in eev)
+        if F:
+            fgs.fgs_frames_host_status(hs.g, hs.field, hs.mlp, hs.cams, dws)   # no capacity overflow
         if world > 1:
             tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
         # parity of the host path against the device path (same inputs -> same images)
         same = all(torch.equal(himgs[i], images[i].cpu()) for i in range(F))
-        e2e = {"value": F * args.steps * world / (e_ms / 1e3), "unit": "frames/s",
+        e2e = {"value": frames_per_step * args.steps / (e_ms / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": hs.h2d_bytes() + F * 4, "d2h_bytes_per_step": F * 3 * H * W * 4,
                "api": "fgs_frames_host (pinned host model in, host images out)", "matches_device_path": same}
         del dws
+
+    # ---- (e1) untimed: the ranks' images gathered to rank 0 == a single-GPU render of the whole batch ----
+    split_check = None
+    if world > 1 and split:
+        got = gather_frames(images, F_all, rank, world)
+        if rank == 0:
+            fds = fgs.DeviceScene(full_scene, dev)
+            fo, _ = fds.alloc_deformed(F_all)
+            fimgs = [torch.empty((3, H, W), dtype=torch.float32, device=dev) for _ in range(F_all)]
+            fws = fds.alloc_workspace(F_all, cap)
+            fgs.fgs_frames(fds.g, fds.field, fds.mlp, fds.times, fds.cams, fo, fimgs, fws)
+            fgs.fgs_render_status(fws, F_all)
+            split_check = {"frames_gathered": len(got),
+                           "bit_identical_to_one_gpu_batch": all(torch.equal(a, b) for a, b in zip(got, fimgs))}
+            del fws
 
     if rank != 0:
         return
@@ -482,20 +651,24 @@ def run_fgs(args, scene, rank, world, local_rank):
     dom = max(roof, key=lambda k: stage_ms.get(k, 0.0) if k != "binning" else 0.0) if roof else None
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": t_max / steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_max / steps, "higher_is_better": True,
+        "scaling": "strong" if split else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_desc(scene), "frames_per_step": F, "n_gaussians": scene.n,
-                   "image": f"{W}x{H}", "l2": "flushed between steps (512 MiB write outside the events)",
-                   "parallelism": f"frame-split x{world} (each rank its own {F}-frame batch)",
+        "config": {"workload": workload_desc(full_scene), "frames_per_step": frames_per_step,
+                   "n_gaussians": scene.n, "image": f"{W}x{H}",
+                   "l2": "flushed between steps (512 MiB write outside the events)",
+                   "parallelism": (f"frame-batch split x{world}: rank r renders frames {{frame_split(F, r, {world})}} "
+                                   f"of the {F_all}-frame batch (rank 0: {len(mine)})") if split else
+                                  f"replicated x{world} (--weak: each rank its own {F_all}-frame batch)",
                    "max_instances_per_frame": cap,
                    "timed": "CUDA-graph replay of one fgs_frames step" if graph is not None else "eager fgs_frames"},
         "value_eager": value_eager,
         "step_ms": step_stats,
-        "gaussians_deformed_per_s": scene.n * F * steps * world / (t_max / 1e3),
+        "gaussians_deformed_per_s": scene.n * frames_per_step * steps / (t_max / 1e3),
         "gaussians_deformed_per_s_deform_stage": scene.n * F * steps / (deform_ms / 1e3) if deform_ms else None,
         "stages_ms_per_step": {k: v / steps for k, v in stage_ms.items()},
-        "stages_note": "per-stage library CUDA events over the eager timed steps (value_eager); the graph "
-                       "replays the same kernels",
+        "stages_note": "rank 0's per-stage library CUDA events over the eager timed steps (value_eager); the "
+                       "graph replays the same kernels",
         "work_per_frame": {k: v for k, v in counts.items() if k != "sms"},
         "roofline": dict(roof[dom], kernel=dom) if dom else None,
         "roofline_stages": roof,
@@ -506,12 +679,33 @@ def run_fgs(args, scene, rank, world, local_rank):
         "clocks": clk,
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline and world >= 1:
+    if split_check is not None:
+        line["frame_split_check"] = split_check
+    if not args.no_cpu_baseline and F:
+        # the oracle on one FULL frame (rank 0's first frame), rendering the GPU's fp32 G' (protocol P3) so
+        # the same run gives the whole-frame parity summary; its own deform output gives the deform error
         P = oracle_procs()
-        fs, td, desc, P = oracle_sample(scene, 0, n_tiles=24 * P, procs=P)
-        line["cpu_baseline"] = {"value": 1.0 / fs, "unit": "frames/s", "cores": P, "kind": "oracle",
-                                "sample": desc, "gaussians_deformed_per_s": scene.n / td}
+        g_gpu = {k: v.cpu().numpy() for k, v in outs_t[0].items()}
+        orc = oracle_full_frame(scene, 0, P, g_render=g_gpu)
+        line["parity"] = parity_summary(scene, 0, g_gpu, dbg0, orc)
+        single = oracle_single_process(scene, 0, g_gpu, orc["pre"], orc["bins"], orc["stages_s"]["binning"])
+        line["cpu_baseline"] = {
+            "value": 1.0 / orc["seconds"], "unit": "frames/s", "cores": P, "kind": "oracle",
+            "sample": (f"1 full frame of {scene.name} (frame {mine[0]} of the batch): oracle deform of all "
+                       f"{scene.n} Gaussians, preprocess of all, binning, blend of every tile; fp64 numpy on "
+                       f"{P} host processes (1 BLAS thread each)"),
+            "extrapolated": False, "stages_s": orc["stages_s"],
+            "gaussians_deformed_per_s": scene.n / orc["stages_s"]["deform"],
+            "single_process": single, "cpu_model": cpu_model()}
     print(json.dumps(line), flush=True)
+
+
+def _first_of_time(scene, f):
+    """Index of the first frame of `scene` with frame f's time (fgs_frames deforms each time once and
+    the frames sharing it render from that frame's G')."""
+    import numpy as np
+    tb = np.float32(scene.times[f]).tobytes()
+    return next(i for i in range(scene.n_frames) if np.float32(scene.times[i]).tobytes() == tb)
 
 
 def run_shard(args, scene, rank, world, local_rank):
@@ -625,6 +819,9 @@ def main():
     ap.add_argument("--n", type=int, default=None,
                     help="override the number of Gaussians (SURVEY 8(f) N-sweep: same distributions)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="frames mode under torchrun: every rank renders its own copy of the whole batch (weak "
+                         "scaling) instead of its frame_split chunk of it (strong scaling, the default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="frames", choices=["frames", "shard"],
                     help="frames: every rank renders its own frame batch (e1); shard: multi-view batch, views "

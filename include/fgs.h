@@ -20,13 +20,15 @@
  *    except fgs_render_status synchronises.  All calls are CUDA-graph capturable.
  *  - Errors: an int code, never an exception.  FGS_E_INVALID for bad arguments (null pointers,
  *    n < 0, sh_degree outside [0,3], width/height <= 0, res/t_res < 2, n_scales outside [1,4],
- *    feat not in {4,8,...,32}, in_dim != feat*n_scales, in_dim > 64, width not in {32,64,128},
+ *    feat not in {8,16,32}, in_dim != feat*n_scales, in_dim > 64, width not in {32,64,128},
  *    t not finite or outside [0,1], misaligned pointers, begin/end out of range, workspace too
  *    small).  FGS_E_CUDA when a launch fails (message in fgs_last_error()).  Instance-capacity
  *    overflow is data dependent and reported by fgs_render_status as FGS_E_CAPACITY.
  *  - Data-dependent degeneracies are not validated: NaN or zero quaternions make a Gaussian
  *    culled (its projected determinant is NaN), never a crash.
- *  - Reentrant for distinct workspaces; the only global state is one-time kernel attribute setup.
+ *  - Reentrant for distinct workspaces, from any number of host threads; the only global state is the
+ *    tuning knobs below, the profiler, and fgs_frames_host's pool of copy streams / events (each call
+ *    holds its own set while it enqueues).
  */
 #ifndef FGS_H
 #define FGS_H
@@ -66,7 +68,7 @@ typedef struct {
  * u = clamp((X - bmin)/(bmax - bmin), 0, 1); knot k of an axis of n knots sits at u = k/(n-1). */
 typedef struct {
   int32_t n_scales;             /* L, 1..4                                                        */
-  int32_t feat;                 /* h, multiple of 4, <= 32                                        */
+  int32_t feat;                 /* h: 8, 16 or 32                                                 */
   int32_t t_res;                /* temporal knots, >= 2                                           */
   int32_t res[FGS_MAX_SCALES];  /* spatial knots per scale, >= 2                                  */
   float bmin[3], bmax[3];       /* world AABB of the field (bmax > bmin)                          */
@@ -131,6 +133,9 @@ typedef struct {
   uint64_t* blend_work;         /* [2] (accumulated, caller zeroes): [0] (warp, Gaussian) pairs the
                                  * blend evaluated after its per-warp cull, [1] pairs it tested; a warp
                                  * covers 64 pixels, so [0] * 64 bounds the pixel evaluations           */
+  uint32_t* binning_direct;     /* [2]          CTAs of the per-tile counting [0] and of the key
+                                 * duplication [1] whose Gaussians' rect union exceeded the shared
+                                 * aggregation box (FGS_TUNE_AGG_TILES) and went to direct global atomics */
 } fgs_render_aux;
 
 /* ---- deformation field F --------------------------------------------------
@@ -199,6 +204,12 @@ size_t fgs_frames_host_workspace_bytes(const fgs_gaussians* g_host, const fgs_he
 int fgs_frames_host(const fgs_gaussians* g_host, const fgs_hexplanes* field_host, const fgs_mlp* mlp_host,
                     const float* ts, const fgs_camera* cams, int32_t n_frames, float* const* images_host,
                     void* dev_ws, size_t dev_ws_bytes, fgs_stream_t stream);
+/* The instance-capacity check of a fgs_frames_host call (its renders live inside dev_ws): pass the same
+ * g_host / field_host / mlp_host / cams / n_frames / dev_ws / dev_ws_bytes.  Synchronises `stream`;
+ * FGS_E_CAPACITY if any frame overflowed (its host image is then invalid), else FGS_OK. */
+int fgs_frames_host_status(const fgs_gaussians* g_host, const fgs_hexplanes* field_host, const fgs_mlp* mlp_host,
+                           const fgs_camera* cams, int32_t n_frames, const void* dev_ws, size_t dev_ws_bytes,
+                           fgs_stream_t stream);
 
 /* ---- profiling -------------------------------------------------------------------------------
  * When enabled, the library records a CUDA event pair around every stage it launches, on the
@@ -226,11 +237,16 @@ int64_t fgs_launch_count(void);
  * Range [1, 1024], default 1024.  Results are identical for every value (tests lower it to exercise
  * the long-list path).  fgs_set_tuning returns FGS_E_INVALID for an unknown key or a value out of
  * range; fgs_get_tuning returns -1 for an unknown key.
- * FGS_TUNE_DEFORM_KERNEL: 0 = automatic choice (default), 1 = SIMT fp32 (deform.cu), 2 = tcgen05 v1
- * (deform_tc.cu), 3 = TMEM-resident v2 (deform_tc2.cu), 4 = warp-specialised v3 (deform_tc3.cu); a kernel
- * that cannot run a given field falls back to the automatic choice.  All give the same results within
- * the 1e-4 deformation tolerance (tests compare every kernel with the oracle). */
-enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_DEFORM_KERNEL = 1 };
+ * FGS_TUNE_BLEND_CULL: 1 (default) = the blend skips, per warp, the Gaussians whose alpha is below
+ * 1/255 on a whole 8x4 pixel sub-box (conservative ellipse-vs-box bound); 0 = every list entry is
+ * evaluated on every live pixel.  Images, final T and contributor counts are identical (tests check it
+ * on whole full-size frames).
+ * FGS_TUNE_AGG_TILES: the per-tile counting and key duplication aggregate a CTA's per-tile atomics in
+ * shared memory when the CTA's rect union holds at most this many tiles, else use direct global
+ * atomics.  Range [1, 4096], default 4096.  Results are identical for every value (tests lower it to
+ * force the direct path; fgs_render_aux.binning_direct counts the CTAs that took it).
+ * (Key 1 is retired: there is a single deformation kernel.) */
+enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_BLEND_CULL = 2, FGS_TUNE_AGG_TILES = 3 };
 int fgs_set_tuning(int32_t key, int64_t value);
 int64_t fgs_get_tuning(int32_t key);
 

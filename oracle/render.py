@@ -313,7 +313,8 @@ def _tile_pixels(tile, gx, W, H):
     return px.ravel(), py.ravel()
 
 
-def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, pre=None, full_bins=True):
+def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, pre=None, full_bins=True,
+               bins=None):
     """I = S(M, G'): preprocess, bin/sort, per-tile blend (tiled oracle).
 
     deformed: dict with means, log_scales, quats (raw, as written by deform).
@@ -323,13 +324,17 @@ def render_ref(deformed, opacity_logits, sh, sh_degree, cam, tiles_subset=None, 
     boundary Gaussian), plus the preprocess dict and (tiles, gids, ranges).
     full_bins=False (with tiles_subset): per-tile lists from tile_list_ref only, for configs where
     building every instance is too slow; (tiles, gids, ranges) are then None.
+    bins: (tiles, gids, ranges) of bin_ref(pre, cam) computed earlier (several processes blending the
+    tiles of one frame share one binning); same values as computing them here.
     """
     W, H = cam.width, cam.height
     gx, gy = tile_grid(W, H)
     if pre is None:
         pre = preprocess_ref(deformed["means"], deformed["log_scales"], deformed["quats"],
                              opacity_logits, sh, sh_degree, cam)
-    if full_bins or tiles_subset is None:
+    if bins is not None:
+        tiles, gids, ranges = bins
+    elif full_bins or tiles_subset is None:
         tiles, gids, ranges = bin_ref(pre, cam)
     else:
         tiles = gids = ranges = None

@@ -51,7 +51,7 @@ int check_gaussians(const fgs_gaussians* g) {
 int check_field(const fgs_hexplanes* h, const fgs_mlp* m) {
   FGS_CHECK(h && m, "hexplanes/mlp is NULL");
   FGS_CHECK(h->n_scales >= 1 && h->n_scales <= FGS_MAX_SCALES, "n_scales must be in [1,4]");
-  FGS_CHECK(h->feat == 4 || h->feat == 8 || h->feat == 16 || h->feat == 32, "feat must be 4, 8, 16 or 32");
+  FGS_CHECK(h->feat == 8 || h->feat == 16 || h->feat == 32, "feat must be 8, 16 or 32");
   FGS_CHECK(h->t_res >= 2, "t_res must be >= 2");
   for (int l = 0; l < h->n_scales; ++l) {
     FGS_CHECK(h->res[l] >= 2 && h->res[l] <= 4096, "res[l] must be in [2,4096]");
@@ -110,38 +110,6 @@ void fill_deform(DeformBatch& p, const fgs_gaussians* g, const fgs_hexplanes* h,
   p.n_peer = 1;                          // one replica at offset 0 (memset)
 }
 
-// Deform kernel selection: FGS_TUNE_DEFORM_KERNEL (or env FGS_DEFORM = simt | tc1 | tc2 | tc3 at load)
-// forces one (A/B comparison and cross-checks); 0 = auto: tc3 (warp-specialised pipeline) when the
-// field fits its line buffer and TMEM plan, else tc2, else tc1.  A forced kernel that cannot run the
-// field falls back to auto.
-std::atomic<int> g_deform_kernel{-1};
-int deform_choice() {
-  int c = g_deform_kernel.load(std::memory_order_relaxed);
-  if (c < 0) {
-    c = 0;
-    if (const char* e = getenv("FGS_DEFORM")) {
-      if (strcmp(e, "simt") == 0) c = 1;
-      if (strcmp(e, "tc1") == 0) c = 2;
-      if (strcmp(e, "tc2") == 0) c = 3;
-      if (strcmp(e, "tc3") == 0) c = 4;
-    }
-    g_deform_kernel.store(c);
-  }
-  return c;
-}
-
-cudaError_t launch_deform_any(const DeformBatch& p, cudaStream_t s) {
-  if (p.w_c || p.w_a) return launch_deform_tc3(p, s);   // the only kernel with the P:1232 decoders
-  switch (deform_choice()) {
-    case 1: return launch_deform(p, s);
-    case 2: return launch_deform_tc(p, s);
-    case 3: if (deform_tc2_supported(p)) return launch_deform_tc2(p, s); break;
-    case 4: if (deform_tc3_supported(p)) return launch_deform_tc3(p, s); break;
-    default: break;
-  }
-  if (deform_tc3_supported(p)) return launch_deform_tc3(p, s);
-  return deform_tc2_supported(p) ? launch_deform_tc2(p, s) : launch_deform_tc(p, s);
-}
 
 int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, const float* ts, int n_t,
                 int64_t begin, int64_t end, fgs_deformed* outs, cudaStream_t s, const int64_t* peer_off = nullptr,
@@ -166,12 +134,11 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
   DeformBatch p;
   fill_deform(p, g, h, m);
   p.begin = begin; p.end = end;
-  if ((heads_c || heads_a) && !deform_tc3_supported(p))
-    return fail(FGS_E_NOTIMPL, "colour/opacity decoders need the warp-specialised deform (field too large)");
+  // every field check_field accepts fits the warp-specialised kernel (feat 8..32, in_dim <= 64, W <= 128)
+  if (!deform_tc3_supported(p)) return fail(FGS_E_NOTIMPL, "field does not fit the deform kernel's TMEM plan");
   if (peer_off) {
     FGS_CHECK(n_peers >= 1 && n_peers <= kMaxPeers, "n_peers must be in [1, 8]");
     FGS_CHECK(!heads_c && !heads_a, "peer replicas: only means / log_scales / quats (no phi_C / phi_alpha)");
-    FGS_CHECK(deform_tc3_supported(p), "peer replicas need the warp-specialised deform (field too large)");
     for (int q = 0; q < n_peers; ++q) FGS_CHECK(peer_off[q] % 4 == 0, "peer offsets must be multiples of 4 bytes");
     p.n_peer = n_peers;
     for (int q = 0; q < n_peers; ++q) p.peer_off[q] = peer_off[q];
@@ -186,7 +153,7 @@ int deform_impl(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m
       p.out_sh[f] = outs[f0 + f].sh;
       p.out_opacity[f] = outs[f0 + f].opacity_logits;
     }
-    cudaError_t e = peer_off ? launch_deform_tc3(p, s) : launch_deform_any(p, s);
+    cudaError_t e = launch_deform_tc3(p, s);
     if (e != cudaSuccess) return cuda_fail(e, "deform launch");
   }
   return FGS_OK;
@@ -244,6 +211,8 @@ int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* 
   local.width = W; local.height = H;
   local.gx = local.L.gx; local.gy = local.L.gy; local.ntiles = local.L.ntiles;
   local.sort_cap = tile_sort_cap();
+  local.cull = blend_cull();
+  local.agg_tiles = agg_tiles();
   local.debug = aux != nullptr;
   local.blend_work = aux ? (unsigned long long*)aux->blend_work : nullptr;
   local.ws_stride = per;
@@ -353,8 +322,12 @@ int64_t capacity_for(int64_t n, int width, int height, size_t bytes) {
 
 namespace {
 std::atomic<int> g_tile_sort_cap{kBlendSortMax};
+std::atomic<int> g_blend_cull{1};
+std::atomic<int> g_agg_tiles{kAggTilesMax};
 }
 int tile_sort_cap() { return g_tile_sort_cap.load(std::memory_order_relaxed); }
+int blend_cull() { return g_blend_cull.load(std::memory_order_relaxed); }
+int agg_tiles() { return g_agg_tiles.load(std::memory_order_relaxed); }
 
 }  // namespace fgs
 
@@ -497,10 +470,13 @@ int fgs_set_tuning(int32_t key, int64_t value) {
       FGS_CHECK(value >= 1 && value <= kBlendSortMax, "tile sort cap must be in [1, 1024]");
       g_tile_sort_cap.store((int)value);
       return FGS_OK;
-    case FGS_TUNE_DEFORM_KERNEL:
-      FGS_CHECK(value >= 0 && value <= 4, "deform kernel must be 0 (auto) .. 4");
-      deform_choice();                 // settle the env default first
-      g_deform_kernel.store((int)value);
+    case FGS_TUNE_BLEND_CULL:
+      FGS_CHECK(value == 0 || value == 1, "blend cull must be 0 or 1");
+      g_blend_cull.store((int)value);
+      return FGS_OK;
+    case FGS_TUNE_AGG_TILES:
+      FGS_CHECK(value >= 1 && value <= kAggTilesMax, "aggregation limit must be in [1, 4096]");
+      g_agg_tiles.store((int)value);
       return FGS_OK;
     default:
       return fail(FGS_E_INVALID, "unknown tuning key");
@@ -509,7 +485,8 @@ int fgs_set_tuning(int32_t key, int64_t value) {
 
 int64_t fgs_get_tuning(int32_t key) {
   if (key == FGS_TUNE_TILE_SORT_CAP) return tile_sort_cap();
-  if (key == FGS_TUNE_DEFORM_KERNEL) return deform_choice();
+  if (key == FGS_TUNE_BLEND_CULL) return blend_cull();
+  if (key == FGS_TUNE_AGG_TILES) return agg_tiles();
   return -1;
 }
 
@@ -555,46 +532,67 @@ HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs
 
 namespace {
 constexpr int kHostChunkFrames = 4;
-// Side stream + events of fgs_frames_host (one set per process and device, created on first use).
-struct CopyStreams {
-  bool ok = false;
-  cudaError_t err = cudaSuccess;
+// Side stream + events of ONE fgs_frames_host call.  Calls take a set from a per-device free list for
+// the duration of their enqueue and give it back before returning, so concurrent calls (distinct
+// workspaces, any threads) never share a stream or an event while enqueueing.  Re-recording an event
+// after the set is returned does not affect the waits already enqueued on it (a wait captures the
+// event's state at enqueue time), so a set is reusable as soon as its call has returned.
+struct CopySet {
+  int dev = -1;
   cudaStream_t copy = nullptr;
   cudaEvent_t done = nullptr, fork = nullptr, sh_done = nullptr;
   std::vector<cudaEvent_t> evs;
-  std::mutex mu;
-  std::mutex call_mu;   // one fgs_frames_host enqueue at a time per device (events are shared)
-  cudaEvent_t event(int i) {
-    std::lock_guard<std::mutex> lk(mu);
+  cudaError_t event(int i, cudaEvent_t* out) {
     while ((int)evs.size() <= i) {
       cudaEvent_t e = nullptr;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      const cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      if (r != cudaSuccess) return r;
       evs.push_back(e);
     }
-    return evs[i];
+    *out = evs[i];
+    return cudaSuccess;
   }
 };
-constexpr int kMaxDevices = 64;
-CopyStreams& copy_streams() {
-  static CopyStreams cs[kMaxDevices];
-  static std::once_flag once[kMaxDevices];
-  static CopyStreams unsupported;   // ok = false: device ordinal beyond kMaxDevices
+struct CopyPool {
+  std::mutex mu;
+  std::vector<CopySet*> free;    // sets of any device; a call takes one of its current device
+};
+CopyPool& copy_pool() { static CopyPool p; return p; }   // sets live for the process (never freed)
+
+cudaError_t acquire_copy_set(CopySet** out) {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= kMaxDevices) {
-    unsupported.err = cudaErrorInvalidDevice;
-    return unsupported;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  CopyPool& P = copy_pool();
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (size_t i = 0; i < P.free.size(); ++i)
+      if (P.free[i]->dev == dev) {
+        *out = P.free[i];
+        P.free.erase(P.free.begin() + (ptrdiff_t)i);
+        return cudaSuccess;
+      }
   }
-  std::call_once(once[dev], [&] {
-    CopyStreams& c = cs[dev];
-    c.err = cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking);
-    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming);
-    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming);
-    if (c.err == cudaSuccess) c.err = cudaEventCreateWithFlags(&c.sh_done, cudaEventDisableTiming);
-    c.ok = c.err == cudaSuccess;
-  });
-  return cs[dev];
+  CopySet* c = new CopySet();
+  c->dev = dev;
+  e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->sh_done, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;   // (leaks the partial set; only on a failing device)
+  *out = c;
+  return cudaSuccess;
 }
+void release_copy_set(CopySet* c) {
+  CopyPool& P = copy_pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.free.push_back(c);
+}
+// RAII: the set goes back to the pool on every return path of fgs_frames_host
+struct CopySetLease {
+  CopySet* c = nullptr;
+  ~CopySetLease() { if (c) release_copy_set(c); }
+};
 }  // namespace
 
 size_t fgs_frames_host_workspace_bytes(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp,
@@ -623,9 +621,12 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   const HostLayout L = host_layout(gh, hh, mh, F, W, H, cap);
   char* d = (char*)dev_ws;
   const size_t n = (size_t)gh->n, K = (size_t)(gh->sh_degree + 1) * (gh->sh_degree + 1);
-  CopyStreams& cs = copy_streams();
-  if (!cs.ok) return cuda_fail(cs.err, "copy stream setup");
-  std::lock_guard<std::mutex> call_lock(cs.call_mu);
+  CopySetLease lease;
+  {
+    const cudaError_t ce = acquire_copy_set(&lease.c);
+    if (ce != cudaSuccess) return cuda_fail(ce, "copy stream setup");
+  }
+  CopySet& cs = *lease.c;
   auto h2d = [&](size_t off, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(d + off, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
   };
@@ -695,7 +696,8 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
     rc = render_impl(cams + f0, rdefs.data() + f0, imgs.data() + f0, nf, d + L.render + (size_t)f0 * L.per_render,
                      L.per_render * (size_t)nf, nullptr, s);
     if (rc != FGS_OK) return rc;
-    cudaEvent_t ev = cs.event(ci);
+    cudaEvent_t ev = nullptr;
+    if ((e = cs.event(ci, &ev)) != cudaSuccess) return cuda_fail(e, "event create");
     if ((e = cudaEventRecord(ev, s)) != cudaSuccess) return cuda_fail(e, "event record");
     if ((e = cudaStreamWaitEvent(cs.copy, ev, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     for (int f = f0; f < f0 + nf; ++f) {
@@ -706,6 +708,34 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   // the caller's stream covers the copies: it waits for the side stream's last copy
   if ((e = cudaEventRecord(cs.done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
   if ((e = cudaStreamWaitEvent(s, cs.done, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+  return FGS_OK;
+}
+
+int fgs_frames_host_status(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_mlp* mh,
+                           const fgs_camera* cams, int32_t F, const void* dev_ws, size_t dev_ws_bytes,
+                           fgs_stream_t stream) {
+  FGS_CHECK(gh && hh && mh && cams && dev_ws && F > 0, "null argument");
+  int rc;
+  if ((rc = check_gaussians(gh)) != FGS_OK) return rc;
+  if ((rc = check_field(hh, mh)) != FGS_OK) return rc;
+  if ((rc = check_camera(&cams[0])) != FGS_OK) return rc;
+  const int W = cams[0].width, H = cams[0].height;
+  // the same layout fgs_frames_host derived from these arguments
+  const HostLayout L0 = host_layout(gh, hh, mh, F, W, H, 1);
+  FGS_CHECK(dev_ws_bytes >= L0.total, "device workspace too small");
+  const size_t fixed = L0.total - L0.per_render * (size_t)F;
+  const int64_t cap = capacity_for(gh->n, W, H, ((dev_ws_bytes - fixed) / (size_t)F) & ~(size_t)255);
+  FGS_CHECK(cap > 0, "device workspace too small");
+  const HostLayout L = host_layout(gh, hh, mh, F, W, H, cap);
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  if (gh->n == 0) return FGS_OK;
+  for (int f = 0; f < F; ++f) {
+    uint32_t flag = 0;
+    e = cudaMemcpy(&flag, (const char*)dev_ws + L.render + (size_t)f * L.per_render + 8, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "status read");
+    if (flag) return fail(FGS_E_CAPACITY, "instance capacity overflow in frame " + std::to_string(f));
+  }
   return FGS_OK;
 }
 

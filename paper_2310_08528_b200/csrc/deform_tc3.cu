@@ -125,6 +125,7 @@ __device__ __forceinline__ float4 lerp_line(const float* line, int off, int R, f
   const float g = u * (float)(R - 1);
   const int i0 = min((int)floorf(g), R - 2);
   const float fa = g - (float)i0;
+  FGS_DCHECK(i0 >= 0 && off + i0 * FEAT >= 0 && off + (i0 + 2) * FEAT <= kLineBufFloats);
   const float4 a = reinterpret_cast<const float4*>(line + off + i0 * FEAT)[swz<FEAT>(i0, c4)];
   const float4 b = reinterpret_cast<const float4*>(line + off + (i0 + 1) * FEAT)[swz<FEAT>(i0 + 1, c4)];
   return lerp4(a, b, fa);
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   const int KP = (IN + 7) & ~7;
   const uint32_t colA_hi = 2 * DW, colA_lo = 2 * DW + KP, colS = 2 * DW + 2 * KP;
   const int G = min(SM::GMAX, (kTmemCols - (int)colS) / IN);
+  FGS_DCHECK(G >= 1 && (int)colS + G * IN <= kTmemCols && NS <= MAXS && IN == NS * FEAT);
 
   extern __shared__ __align__(128) unsigned char smem[];
   float* line = reinterpret_cast<float*>(smem + SM::OFF_LINE);
@@ -341,9 +343,14 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
       // (1) grid coordinates u (smem U) and knot windows: thread (quarter, part) takes the tiles
       //     gt = part mod NP of the group
       for (int gt = part; gt < ng; gt += RL::NP) {
-        const int64_t g = p.begin + (int64_t)(gstart + gt) * kM + row;
+        // rows past the end of the range (ragged last tile) take the coordinates of the tile's row 0,
+        // which always exists: their line reads then stay inside the group's knot windows (a padding
+        // row at u = 0 could fall outside them and read below the staged segment — found by the checked
+        // build).  Their S is 0 and their outputs are never stored.
+        int64_t g = p.begin + (int64_t)(gstart + gt) * kM + row;
+        if (g >= p.end) g = p.begin + (int64_t)(gstart + gt) * kM;
         float u[3] = {0.f, 0.f, 0.f};
-        if (g < p.end) {
+        {
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const float m = __ldg(p.means + g * 3 + a);
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             }
           }
         }
+        FGS_DCHECK(gt < SM::GMAX);
         float* Ur = U + (gt * kM + row) * 4;
         Ur[0] = u[0]; Ur[1] = u[1]; Ur[2] = u[2];
       }
@@ -424,6 +432,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             }
           }
           __syncwarp();
+          FGS_DCHECK((int)colS + gt * IN + (l + 1) * FEAT <= kTmemCols);
           float sv[FEAT];
 #pragma unroll
           for (int c = 0; c < FEAT; ++c) sv[c] = T[lane * FEAT + (c ^ (lane & (FEAT - 1)))];
@@ -476,6 +485,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
               for (int q = tid; q < n_items; q += kProdThreads) {
                 const int rem = lo * (FEAT / 4) + q;
                 const int i = rem / (FEAT / 4), c4 = rem - i * (FEAT / 4);
+                FGS_DCHECK(segoff[sg] + i * FEAT >= 0 && segoff[sg] + (i + 1) * FEAT <= kLineBufFloats && i < R);
                 dst[i * (FEAT / 4) + swz<FEAT>(i, c4)] = lerp4(__ldg(P0 + rem), __ldg(P1 + rem), ft);
               }
             }
@@ -637,6 +647,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
+                FGS_DCHECK((c0 + i) * NOUTP + 12 * pass + 12 <= NOUTP * WIDTH);
                 const float4* w4 = reinterpret_cast<const float4*>(Wh + (c0 + i) * NOUTP + 12 * pass);
                 const float4 wa = w4[0], wb = w4[1], wc = w4[2];
                 const float2 fd2 = make_float2(fd, fd);

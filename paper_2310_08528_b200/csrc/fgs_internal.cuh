@@ -5,6 +5,25 @@
 
 #include "../../include/fgs.h"
 
+// Checked build (libfgs_checked.so, build.py --checked): device-side bounds / invariant assertions on
+// the shared-memory, TMEM and workspace indices of every kernel, and a watchdog on every mbarrier wait.
+// A failed check prints its condition and traps (the launch fails with an error the tests see).  The
+// normal build compiles every FGS_DCHECK to nothing.  (compute-sanitizer is closed on the GPU pool this
+// was developed on; this is its stand-in — DESIGN.md §6.)
+#ifdef FGS_CHECKED
+#include <stdio.h>
+#define FGS_DCHECK(cond)                                                                               \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("FGS_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x,   \
+             (int)threadIdx.x, #cond);                                                                 \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define FGS_DCHECK(cond) ((void)0)
+#endif
+
 namespace fgs {
 
 constexpr int kTile = FGS_TILE;              // 16x16 pixel tiles ([3dgs] rasterizer, reading R8)
@@ -20,7 +39,8 @@ struct WsLayout {
   int64_t n = 0, cap = 0;
   int width = 0, height = 0, gx = 0, gy = 0, ntiles = 0;
   size_t cnt = 0;            // uint32[16]: 0 n, 1 M clamped to cap, 2 overflow flag, 3 M raw, 4 long lists,
-                             // 5 (frame 0) long-list claim counter of the batch
+                             // 5 (frame 0) long-list claim counter of the batch, 6 / 7 CTAs of
+                             // preprocess / duplicate that took the direct-atomics binning path
   size_t keys = 0;           // uint32[n] depth key (IEEE bits of fp32 view depth), gid order
   size_t tt = 0;             // uint32[n] tiles_touched
   size_t rect = 0;           // uint2[n]  (x0 | y0<<16, x1 | y1<<16)
@@ -53,6 +73,8 @@ struct RenderBatch {
   int width, height, gx, gy, ntiles;
   int sort_cap;              // lists longer than this are sorted by the global-memory path
   int debug;                 // 1: blend writes each tile's sorted list back (fgs_render_debug)
+  int cull;                  // 1: per-warp ellipse cull in the blend (FGS_TUNE_BLEND_CULL), 0: none
+  int agg_tiles;             // CTA binning aggregation limit in tiles (FGS_TUNE_AGG_TILES, <= 4096)
   char* ws;                  // frame f slice = ws + f * ws_stride
   size_t ws_stride;
   WsLayout L;
@@ -99,10 +121,6 @@ struct DeformBatch {
 };
 
 // Kernel launchers (return cudaError_t of the launch).
-cudaError_t launch_deform(const DeformBatch& p, cudaStream_t s);      // SIMT FP32 (deform.cu)
-cudaError_t launch_deform_tc(const DeformBatch& p, cudaStream_t s);   // tcgen05 3xTF32 (deform_tc.cu)
-cudaError_t launch_deform_tc2(const DeformBatch& p, cudaStream_t s);  // TMEM-resident v2 (deform_tc2.cu)
-bool deform_tc2_supported(const DeformBatch& p);
 cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s);  // warp-specialised v3 (deform_tc3.cu)
 bool deform_tc3_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
@@ -110,6 +128,9 @@ cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, c
 
 // Tuning knobs (api.cu, fgs_set_tuning).
 int tile_sort_cap();
+int blend_cull();
+int agg_tiles();
+constexpr int kAggTilesMax = 4096;           // shared histogram of the CTA binning aggregation
 
 // Profiling / launch accounting (api.cu).
 void prof_mark(int stage, bool begin, cudaStream_t s);

@@ -109,10 +109,9 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ sh, float X,
 }
 
 // CTA-level aggregation of per-tile atomics.  The CTA's kept Gaussians are bounded by the tile box
-// [bx0,bx1) x [by0,by1); when it holds at most kAggTiles tiles (spatially ordered models: a CTA's
+// [bx0,bx1) x [by0,by1); when it holds at most b.agg_tiles (<= kAggTilesMax) tiles (spatially ordered models: a CTA's
 // Gaussians are neighbours), per-tile sums are formed in shared memory and each touched tile gets one
 // global atomic; otherwise every instance goes to global memory directly.
-constexpr int kAggTiles = 4096;
 struct AggBox {
   int x0, y0, x1, y1;
 };
@@ -130,8 +129,9 @@ __device__ __forceinline__ AggBox cta_rect_union(bool kept, int x0, int y0, int 
   return r;
 }
 
-__device__ __forceinline__ bool agg_fits(const AggBox& r) {
-  return r.x1 > r.x0 && (int64_t)(r.x1 - r.x0) * (r.y1 - r.y0) <= kAggTiles;
+// `limit` = b.agg_tiles (<= kAggTilesMax; FGS_TUNE_AGG_TILES lowers it so tests can force the direct path)
+__device__ __forceinline__ bool agg_fits(const AggBox& r, int limit) {
+  return r.x1 > r.x0 && (int64_t)(r.x1 - r.x0) * (r.y1 - r.y0) <= limit;
 }
 
 template <int DEG>
@@ -224,10 +224,11 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
   keep = keep && valid;
   // ---- instance counts per tile (the bucket sizes of the duplication) ----
   __shared__ int sbox[4];
-  __shared__ uint32_t scount[kAggTiles];
+  __shared__ uint32_t scount[kAggTilesMax];
   const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
-  if (agg_fits(box)) {
+  if (agg_fits(box, b.agg_tiles)) {
     const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= b.gx && box.y1 <= b.gy);
     for (int q = threadIdx.x; q < area; q += blockDim.x) scount[q] = 0;
     __syncthreads();
     if (keep)
@@ -236,9 +237,13 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
     __syncthreads();
     for (int q = threadIdx.x; q < area; q += blockDim.x)
       if (scount[q]) atomicAdd(tile_count + (box.y0 + q / bw) * b.gx + box.x0 + q % bw, scount[q]);
-  } else if (keep) {
-    for (int ty = y0; ty < y1; ++ty)
-      for (int tx = x0; tx < x1; ++tx) atomicAdd(tile_count + ty * b.gx + tx, 1u);
+  } else {
+    // direct global atomics (the CTA's rect union exceeds the shared histogram); cnt[6] counts the
+    // CTAs that took this path (debug evidence, fgs_render_aux.binning_direct[0])
+    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt_ptr(b, f) + 6, 1u);
+    if (keep)
+      for (int ty = y0; ty < y1; ++ty)
+        for (int tx = x0; tx < x1; ++tx) atomicAdd(tile_count + ty * b.gx + tx, 1u);
   }
   if (!valid) return;
   if (!keep) {
@@ -362,6 +367,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_co
   for (int t = beg; t < end; ++t) {
     const uint32_t len = tc[t];
     const uint32_t pos = atomicAdd(hist + (kOrderBuckets - 1 - (int)min(len, (uint32_t)(kOrderBuckets - 1))), 1u);
+    FGS_DCHECK(pos < (uint32_t)nt);
     order[pos] = (uint32_t)t;
   }
 }
@@ -385,11 +391,12 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ 
   const uint64_t cap = (uint64_t)b.L.cap;
   const unsigned long long v = ((unsigned long long)key << 32) | (uint32_t)i;
   __shared__ int sbox[4];
-  __shared__ uint32_t sbase[kAggTiles];
+  __shared__ uint32_t sbase[kAggTilesMax];
   const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
-  if (agg_fits(box)) {
+  if (agg_fits(box, b.agg_tiles)) {
     // one global cursor claim per touched tile for the whole CTA, slots handed out in smem
     const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= b.gx && box.y1 <= b.gy);
     for (int q = threadIdx.x; q < area; q += blockDim.x) sbase[q] = 0;
     __syncthreads();
     if (keep)
@@ -405,12 +412,14 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ 
           const uint32_t pos = atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
           if (pos < cap) inst[pos] = v;
         }
-  } else if (keep) {
-    for (int ty = y0; ty < y1; ++ty)
-      for (int tx = x0; tx < x1; ++tx) {
-        const uint32_t pos = atomicAdd(cursor + ty * b.gx + tx, 1u);
-        if (pos < cap) inst[pos] = v;
-      }
+  } else {
+    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt_ptr(b, f) + 7, 1u);   // binning_direct[1]
+    if (keep)
+      for (int ty = y0; ty < y1; ++ty)
+        for (int tx = x0; tx < x1; ++tx) {
+          const uint32_t pos = atomicAdd(cursor + ty * b.gx + tx, 1u);
+          if (pos < cap) inst[pos] = v;
+        }
   }
 }
 
@@ -490,6 +499,7 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
                                             int lane) {
   constexpr int N2 = 32 * R;
   constexpr int LB = R == 1 ? 5 : R == 2 ? 6 : R == 4 ? 7 : R == 8 ? 8 : 9;   // log2(N2)
+  FGS_DCHECK(L >= 1 && L <= N2);
   static_assert((1 << LB) == N2, "slot bits");
   uint32_t hk[R];
   uint32_t mn = 0xFFFFFFFFu, mx = 0u;
@@ -517,6 +527,7 @@ __device__ __noinline__ void warp_sort_tile(const unsigned long long* src, unsig
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = R * lane + r;
+    FGS_DCHECK(e >= L || (int)(v[r] & (uint32_t)(N2 - 1)) < L);
     out[r] = e < L ? src[v[r] & (uint32_t)(N2 - 1)] : 0ull;
     const uint32_t nx = r + 1 < R ? v[r + 1 < R ? r + 1 : r] : next0;
     if (e + 1 < L && (v[r] >> LB) == (nx >> LB)) tie = true;
@@ -593,8 +604,10 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
   const int rank = (int)(blockIdx.x / (unsigned)b.n_frames) * kTileSortWarps + warp;
   if (rank >= b.ntiles) return;                 // no CTA-wide barriers below
   const int tile = (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.order)[rank];
+  FGS_DCHECK(tile >= 0 && tile < b.ntiles);
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
+  FGS_DCHECK(rg.x <= rg.y && (int64_t)rg.y <= b.L.cap);
   if (L <= 1) return;
   if (L > b.sort_cap) {
     if (lane == 0) {
@@ -612,6 +625,7 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
   // each by the smallest network that holds it), one merge-path merge into the list
   __shared__ unsigned long long buf[kTileSortWarps][kBlendSortMax];
   unsigned long long* A = buf[warp];
+  FGS_DCHECK(L <= kBlendSortMax);
   const int h = L <= 512 ? 256 : 512;
   if (h == 256) warp_sort_upto256(inst, A, 256, lane);
   else warp_sort_tile<16>(inst, A, 512, lane);
@@ -663,6 +677,7 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   constexpr int NT = kLargeSortThreads, NW = NT / 32;
   uint32_t* wA = reinterpret_cast<uint32_t*>(sm);
   uint32_t* wB = wA + kCtaSortMax;
+  FGS_DCHECK(L >= 1 && L <= kCtaSortMax);
   unsigned long long* stage = sm + kCtaSortMax;
   __shared__ uint32_t s_mn, s_mx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -709,6 +724,7 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   }
   bool tie = false;
   for (int q = threadIdx.x; q < L; q += NT) {
+    FGS_DCHECK((int)(A[q] & ((1u << SB) - 1u)) < L);
     stage[q] = src[A[q] & ((1u << SB) - 1u)];
     if (q + 1 < L && (A[q] >> SB) == (A[q + 1] >> SB)) tie = true;
   }
@@ -739,6 +755,7 @@ __device__ void cta_sort_keys(const unsigned long long* src, unsigned long long*
                          unsigned long long* sB) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kLargeSortThreads / 32;
+  FGS_DCHECK(L >= 1 && L <= kCtaSortMax);
   for (int r0 = warp * 256; r0 < L; r0 += NW * 256)
     warp_sort_upto256(src + r0, sA + r0, min(256, L - r0), lane);
   __syncthreads();
@@ -816,6 +833,7 @@ __global__ void __launch_bounds__(kLargeSortThreads) long_sort_kernel(const __gr
       w -= n_long;
     }
     if (f == b.n_frames) return;                    // CTA-uniform
+    FGS_DCHECK(w < (uint32_t)b.ntiles);
     long_sort_one(b, f, (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.long_list)[w], long_sm);
     __syncthreads();
   }
@@ -960,6 +978,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
       const int idx = start + threadIdx.x + NT * k;
       if (idx < L) {
         const uint32_t g = (uint32_t)inst[idx];
+        FGS_DCHECK((int64_t)g < b.n && (int64_t)rg.x + idx < b.L.cap);
         float4 a = rec[3 * g + 0];
         const float4 c = rec[3 * g + 2];
         a.x = (a.x - tx0) + c.y;      // tile-relative mean: exact hi difference + lo part
@@ -982,7 +1001,10 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
       uint32_t need = 0;
       if (jt < cnt) {
         const float4 a = srec[jt].a;
-        need = subboxes_may_reach(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live;
+        // b.cull = 0 (FGS_TUNE_BLEND_CULL): every Gaussian on every live sub-box — the unculled Eq. 4
+        // loop, which the culled one must equal bit for bit
+        need = b.cull ? subboxes_may_reach(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live
+                      : live;
       }
       uint32_t mk[kBlendPix];
 #pragma unroll
@@ -1138,6 +1160,10 @@ __global__ void debug_copy_kernel(const __grid_constant__ RenderBatch b, fgs_ren
       for (uint32_t p = r.x; p < r.y; ++p) aux.sorted_tile[p] = (uint32_t)i;
   }
   if (i == 0 && aux.n_instances) aux.n_instances[0] = cnt[3];
+  if (i == 0 && aux.binning_direct) {
+    aux.binning_direct[0] = cnt[6];
+    aux.binning_direct[1] = cnt[7];
+  }
 }
 
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s) {

@@ -1,6 +1,9 @@
 // Thin inline-PTX wrappers for the sm_100a tensor-core path (tcgen05 / TMEM / mbarrier).
 #pragma once
 #include <stdint.h>
+#ifdef FGS_CHECKED
+#include <stdio.h>
+#endif
 
 namespace fgs {
 namespace tc {
@@ -19,6 +22,36 @@ __device__ __forceinline__ void fence_mbar_init() {
 // try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit (up to the hint) instead
 // of re-issuing try_wait in a tight loop, which takes issue slots from the warps doing the work
 constexpr uint32_t kMbarSuspendNs = 0x989680;
+#ifdef FGS_CHECKED
+// checked build: the same wait, one try_wait per iteration, with a watchdog (a pipeline that waits on a
+// phase nobody will complete — a role-schedule mismatch — traps instead of hanging the GPU)
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(kMbarSuspendNs)
+        : "memory");
+    if (ok) return;
+    if (globaltimer_ns() - t0 > 2000000000ull) {   // 2 s: no kernel phase of this library takes that long
+      printf("FGS_DCHECK mbarrier wait timeout: block %d thread %d parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -30,6 +63,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(kMbarSuspendNs)
       : "memory");
 }
+#endif
 
 // ---- warpgroup register re-split (all warps of the warpgroup execute the same instruction) ----------
 template <int N>

@@ -15,7 +15,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfgs.so")
+# FGS_LIB=checked loads the checked build (device-side assertions, build.py --checked) — same ABI
+LIB_PATH = os.path.join(HERE, "libfgs_checked.so" if os.environ.get("FGS_LIB", "") == "checked" else "libfgs.so")
 
 FGS_OK, FGS_E_INVALID, FGS_E_CUDA, FGS_E_CAPACITY, FGS_E_NOTIMPL = 0, -1, -2, -3, -4
 MAX_SCALES, PLANES, TILE = 4, 6, 16
@@ -59,18 +60,19 @@ class fgs_camera(ctypes.Structure):
 class fgs_render_aux(ctypes.Structure):
     _fields_ = [(k, c_void_p) for k in ("radii", "rect", "mean2d", "depth_key", "tiles_touched",
                                         "n_instances", "sorted_tile", "sorted_gid", "ranges",
-                                        "final_T", "n_contrib", "n_evaluated", "blend_work")]
+                                        "final_T", "n_contrib", "n_evaluated", "blend_work",
+                                        "binning_direct")]
 
 
 _LIB = None
 EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_range_peers", "fgs_deform_batch", "fgs_render_workspace_bytes",
            "fgs_render", "fgs_render_batch", "fgs_render_debug", "fgs_render_status", "fgs_frames",
-           "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_profile_enable", "fgs_profile_read",
+           "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_frames_host_status", "fgs_profile_enable", "fgs_profile_read",
            "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version")
 STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend")
 FGS_TUNE_TILE_SORT_CAP = 0
-FGS_TUNE_DEFORM_KERNEL = 1
-DEFORM_KERNELS = {"auto": 0, "simt": 1, "tc1": 2, "tc2": 3, "tc3": 4}
+FGS_TUNE_BLEND_CULL = 2
+FGS_TUNE_AGG_TILES = 3
 
 
 def lib():
@@ -103,6 +105,8 @@ def lib():
         L.fgs_frames_host_workspace_bytes.restype = c_size_t
         L.fgs_frames_host.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(c_float), P(fgs_camera),
                                       c_int32, P(c_void_p), c_void_p, c_size_t, c_void_p]
+        L.fgs_frames_host_status.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(fgs_camera),
+                                             c_int32, c_void_p, c_size_t, c_void_p]
         L.fgs_profile_enable.argtypes = [c_int]
         L.fgs_profile_read.argtypes = [P(ctypes.c_double), P(c_int64)]
         L.fgs_launch_count.restype = c_int64
@@ -214,6 +218,31 @@ def fgs_frames_host(g_host, field_host, mlp_host, ts, cams, images_host, dev_ws,
     iarr = (c_void_p * max(F, 1))(*[im.data_ptr() for im in images_host])
     return _check(lib().fgs_frames_host(ctypes.byref(g_host), ctypes.byref(field_host), ctypes.byref(mlp_host),
                                         tarr, carr, F, iarr, _ptr(dev_ws), dev_ws.numel(), _stream(stream)))
+
+
+def fgs_frames_host_status(g_host, field_host, mlp_host, cams, dev_ws, stream=None):
+    """FGS_E_CAPACITY (raised) if a frame of the last fgs_frames_host call into dev_ws overflowed."""
+    F = len(cams)
+    carr = (fgs_camera * max(F, 1))(*cams)
+    return _check(lib().fgs_frames_host_status(ctypes.byref(g_host), ctypes.byref(field_host),
+                                               ctypes.byref(mlp_host), carr, F, _ptr(dev_ws), dev_ws.numel(),
+                                               _stream(stream)))
+
+
+class tuning:
+    """Context manager: set a tuning knob for the block, restore it after (tests, tools)."""
+
+    def __init__(self, key, value):
+        self.key, self.value = key, value
+
+    def __enter__(self):
+        self.old = fgs_get_tuning(self.key)
+        fgs_set_tuning(self.key, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        fgs_set_tuning(self.key, self.old)
+        return False
 
 
 def fgs_profile_enable(enable=True):

@@ -52,6 +52,41 @@ def frame_split(n_frames: int, rank: int, world: int) -> List[int]:
     return list(range(begin, begin + base + (1 if rank < extra else 0)))
 
 
+def gather_frames(images: Sequence, n_frames: int, rank: int, world: int, group=None):
+    """(e1) untimed validation step: every rank's images of its frame_split chunk -> the whole batch in
+    frame order on rank 0 (other ranks get None).  One all_gather of the chunks padded to the largest
+    chunk (all_gather works on NCCL and gloo alike); images are same-shape tensors on the rank's device."""
+    import torch
+    import torch.distributed as dist
+    mine = frame_split(n_frames, rank, world)
+    if len(images) != len(mine):
+        raise ValueError(f"rank {rank} holds {len(images)} images for {len(mine)} frames")
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return list(images)
+    per = -(-n_frames // world)
+    ref = images[0] if images else None
+    shape = tuple(ref.shape) if ref is not None else None
+    # every rank must agree on shape/dtype/device: take them from rank 0's first image
+    meta = [shape, None if ref is None else str(ref.dtype)]
+    objs = [None] * world
+    dist.all_gather_object(objs, meta, group=group)
+    shape, dtype = next((tuple(o[0]), o[1]) for o in objs if o[0] is not None)
+    dt = getattr(torch, dtype.replace("torch.", ""))
+    dev = ref.device if ref is not None else (torch.device("cuda", torch.cuda.current_device())
+                                              if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    buf = torch.zeros((per,) + shape, dtype=dt, device=dev)
+    for i, im in enumerate(images):
+        buf[i].copy_(im)
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    if rank != 0:
+        return None
+    frames = []
+    for r in range(world):
+        frames.extend(out[r][:len(frame_split(n_frames, r, world))].unbind(0))
+    return frames
+
+
 def views_of_times(n_times: int, n_views: int, rank: int, world: int) -> List[Tuple[int, int]]:
     """(e2) multi-view batch: frames (time k, view v), frame id k * n_views + v.  Views are split across
     ranks (each rank renders its views at EVERY time), so all ranks need G'(t_k) for every k — the case
@@ -109,7 +144,17 @@ class ShardedDeform:
 
     def deform(self, slot: int, t: float, deform_fn: Callable[..., None]) -> None:
         """deform_fn(slot, t, begin, end, bufs) — with fused=True also the peer offsets of the slot's
-        replicas: deform_fn(slot, t, begin, end, bufs, offsets)."""
+        replicas: deform_fn(slot, t, begin, end, bufs, offsets).
+
+        fused: this rank's deform writes into EVERY rank's copy of the slot, so before it starts, every
+        rank must have finished reading the slot's previous contents (its render of the time the slot
+        held before).  A stream-ordered barrier over the group on channel 2 + slot does that: each rank
+        enqueues it after its earlier render of the slot (the render was issued before this call), so
+        when the barrier completes on this rank's stream, all peers' streams have passed that render.
+        (The NCCL path needs none: each rank's all-gather writes only its own buffer, in its stream
+        order, after its own render.)"""
+        if self.fused:
+            self.handles[slot].barrier(channel=2 + slot)
         if self.end > self.begin:
             if self.fused:
                 deform_fn(slot, t, self.begin, self.end, self.bufs[slot], self.offsets[slot])

@@ -74,7 +74,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(fgs.fgs_gaussians) == 8 + 8 + 5 * 8
     assert ctypes.sizeof(fgs.fgs_camera) == 4 * (9 + 3 + 4 + 2 + 3)
     assert fgs.fgs_hexplanes.planes.offset == 56
-    assert ctypes.sizeof(fgs.fgs_render_aux) == 13 * 8
+    assert ctypes.sizeof(fgs.fgs_render_aux) == 14 * 8
     assert ctypes.sizeof(fgs.fgs_mlp) == 8 + 12 * 8
 
 
@@ -88,11 +88,18 @@ def test_tuning_knob_host_only(L):
     assert L.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 4096) == fgs.FGS_E_INVALID
     assert L.fgs_set_tuning(99, 1) == fgs.FGS_E_INVALID
     assert fgs.fgs_get_tuning(99) == -1
-    k0 = fgs.fgs_get_tuning(fgs.FGS_TUNE_DEFORM_KERNEL)
-    fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, 2)
-    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_DEFORM_KERNEL) == 2
-    fgs.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, k0)
-    assert L.fgs_set_tuning(fgs.FGS_TUNE_DEFORM_KERNEL, 9) == fgs.FGS_E_INVALID
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_BLEND_CULL) == 1
+    with fgs.tuning(fgs.FGS_TUNE_BLEND_CULL, 0):
+        assert fgs.fgs_get_tuning(fgs.FGS_TUNE_BLEND_CULL) == 0
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_BLEND_CULL) == 1
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_BLEND_CULL, 2) == fgs.FGS_E_INVALID
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_AGG_TILES) == 4096
+    with fgs.tuning(fgs.FGS_TUNE_AGG_TILES, 1):
+        assert fgs.fgs_get_tuning(fgs.FGS_TUNE_AGG_TILES) == 1
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_AGG_TILES) == 4096
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_AGG_TILES, 0) == fgs.FGS_E_INVALID
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_AGG_TILES, 4097) == fgs.FGS_E_INVALID
+    assert L.fgs_set_tuning(1, 0) == fgs.FGS_E_INVALID          # retired key (single deform kernel)
 
 
 def test_stage_names_match_header():

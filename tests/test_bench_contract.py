@@ -58,3 +58,30 @@ def test_roofline_work_per_step_with_several_launches():
     work = (9 * 1e6 + 4 * 2e5) * s.n_frames / 1e12
     assert one["blend"]["achieved"] == pytest.approx(work / (1.5e-3 / steps))
     assert one["blend"]["peak"] == pytest.approx(148 * 128 * 2000e6 / 1e12)
+
+
+def test_blend_c_basis_fraction():
+    """roofline.frac_C: 13 instructions per contributing pair (SURVEY 8(d) C basis) over the same time."""
+    s = make_scene("dnerf", n=1000, n_frames=2)
+    counts = {"sms": 148, "evaluated_per_frame": 1e6, "contrib_per_frame": 2e5, "instances_per_frame": 5e3}
+    r = bench.roofline_objects(s, {"blend": 1.0}, {"blend": 1}, {"hbm_gbs": 6000.0}, counts, 2000.0, 1)
+    assert r["blend"]["achieved_C"] == pytest.approx(13 * 2e5 * 2 / 1e12 / 1e-3)
+    assert r["blend"]["frac_C"] == pytest.approx(r["blend"]["achieved_C"] / r["blend"]["peak"])
+    assert r["blend"]["frac_C"] < r["blend"]["frac"]
+
+
+def test_oracle_full_frame_is_complete_and_matches_render_ref():
+    """The oracle arm times a FULL frame (every Gaussian, every tile, no extrapolation): its pooled
+    deform / preprocess / blend equal the single-process oracle exactly (tiny config, ragged tiles)."""
+    import numpy as np
+
+    import oracle
+    s = make_scene("tiny", n=700, width=70, height=50)
+    r = bench.oracle_full_frame(s, 0, 3)
+    d = oracle.deform_ref(s, float(s.times[0]))
+    for k in d:      # chunked vs whole-array matmul: equal up to BLAS summation order
+        assert np.allclose(r["deformed"][k], d[k], rtol=0, atol=1e-13)
+    ref = oracle.render_ref(r["deformed"], s.opacity_logits, s.sh, s.sh_degree, s.cameras[0])
+    assert np.array_equal(r["image"], ref["image"])
+    assert np.array_equal(r["n_contrib"], ref["n_contrib"]) and np.array_equal(r["flagged"], ref["flagged"])
+    assert set(r["stages_s"]) == {"deform", "preprocess", "binning", "blend"}

@@ -99,3 +99,25 @@ def test_fullsize_batch_parity(name, frames, n):
                             full_bins=False)
         pix = compare_pixels(imgs[f].cpu().numpy(), ref["image"], ref["flagged"])
         assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, (name, f, pix)
+
+
+@pytest.mark.parametrize("name", ["dnerf", "scaling"])
+def test_blend_cull_exact_on_whole_fullsize_frames(name):
+    """The blend's per-warp ellipse cull (Eq. 4 evaluations skipped when alpha < 1/255 on a whole 8x4
+    sub-box) must not change any pixel: two full-size frames (D: all 2,500 tiles; S: all 8,160 tiles of
+    1920x1080 with 2M Gaussians), image / final T / contributor counts bit-identical with the cull on
+    and off (FGS_TUNE_BLEND_CULL)."""
+    s = make_scene(name, n_frames=2)
+    ds, outs, tens, imgs = _run_frames(s)
+    for f in range(2):
+        # frames sharing a time render from the first such frame's G' (fgs_frames deforms each t once)
+        f0 = next(i for i in range(2) if np.float32(s.times[i]).tobytes() == np.float32(s.times[f]).tobytes())
+        on = gpu_render_debug(ds, s.cameras[f], outs[f0])
+        with fgs.tuning(fgs.FGS_TUNE_BLEND_CULL, 0):
+            off = gpu_render_debug(ds, s.cameras[f], outs[f0])
+        assert on["status"] == off["status"] == fgs.FGS_OK
+        for k in ("image", "final_T", "n_contrib"):
+            assert np.array_equal(on[k], off[k]), (name, f, k, int(np.sum(on[k] != off[k])))
+        assert np.array_equal(imgs[f].cpu().numpy(), on["image"])
+        # the cull really skipped work: fewer (warp, Gaussian) evaluations than the unculled loop
+        assert on["blend_work"][0] < off["blend_work"][0]

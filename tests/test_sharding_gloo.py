@@ -156,6 +156,75 @@ def test_sharded_deform_fused_host_logic(monkeypatch):
     assert b["means"].data_ptr() - b["quats"].data_ptr() == rows * 4 * 4
     assert b["log_scales"].data_ptr() - b["means"].data_ptr() == rows * 3 * 4
     seen = []
-    sd.deform(1, 0.25, lambda slot, t, lo, hi, bufs, offsets: seen.append((slot, t, lo, hi, offsets)))
-    assert seen == [(1, 0.25) + shard_range(n, rank, world) + ([-4096, 0, 8192],)]
-    assert sd.gather(1) == [] and calls["barrier"] == [1]
+    sd.deform(1, 0.25, lambda slot, t, lo, hi, bufs, offsets: seen.append((slot, t, lo, hi, offsets,
+                                                                           list(calls["barrier"]))))
+    # the slot-free barrier (channel 2 + slot) is enqueued BEFORE the deform writes into the peers' copies
+    # of the slot (a peer may still be rendering the slot's previous time)
+    assert seen == [(1, 0.25) + shard_range(n, rank, world) + ([-4096, 0, 8192], [3])]
+    assert sd.gather(1) == [] and calls["barrier"] == [3, 1]
+    # a rank with an empty shard still joins the slot-free barrier (every rank must reach it)
+    sd.begin = sd.end
+    sd.deform(0, 0.5, lambda *a: seen.append(a))
+    assert len(seen) == 1 and calls["barrier"] == [3, 1, 2]
+
+
+def _frames_worker(rank, world, port, W, H, q):
+    """(e1) frame-batch split on gloo: each rank renders (here: the oracle renders) only its frame_split
+    chunk of a reduced D batch; gather_frames assembles the batch on rank 0 in frame order."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from oracle import render as OR
+    from paper_2310_08528_b200.inputs import make_scene
+    from paper_2310_08528_b200.sharding import gather_frames
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = make_scene("dnerf", n=400, width=W, height=H, n_frames=5)
+        mine = frame_split(s.n_frames, rank, world)
+        imgs = []
+        for f in mine:
+            d = oracle.deform_ref(s, float(s.times[f]))
+            out = OR.render_ref(d, s.opacity_logits, s.sh, s.sh_degree, s.cameras[f])
+            imgs.append(torch.from_numpy(out["image"].astype(np.float32)))
+        got = gather_frames(imgs, s.n_frames, rank, world)
+        q.put((rank, mine, None if got is None else [g.numpy() for g in got]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_frame_split_gather_gloo(world):
+    """bench.py --gpus N frames mode: the config's batch is split (not replicated) across ranks and the
+    rank-0 gather reproduces the single-process batch image for image (5 frames: ragged split)."""
+    import multiprocessing as mp
+
+    import oracle
+    from oracle import render as OR
+    from paper_2310_08528_b200.inputs import make_scene
+
+    W, H = 40, 24
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_frames_worker, args=(r, world, port, W, H, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, mine, got = q.get(timeout=240)
+        res[rank] = (mine, got)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum((res[r][0] for r in range(world)), []) == list(range(5))
+    assert all(res[r][1] is None for r in range(1, world))
+    s = make_scene("dnerf", n=400, width=W, height=H, n_frames=5)
+    got = res[0][1]
+    assert len(got) == 5
+    for f in range(5):
+        d = oracle.deform_ref(s, float(s.times[f]))
+        want = OR.render_ref(d, s.opacity_logits, s.sh, s.sh_degree, s.cameras[f])["image"].astype(np.float32)
+        assert np.array_equal(got[f], want), f

@@ -2,7 +2,7 @@
 # ncu --set full captures of the top kernels (one launch each) of the default bench workload.
 # Usage: bash tools/gpu_ncu_full.sh TAG "kernel:skip kernel:skip ..."
 TAG=${1:-r1}
-LIST=${2:-"blend_kernel:2 deform_tc2_kernel:2 radix_scatter_kernel:10 preprocess_kernel:2"}
+LIST=${2:-"blend_kernel:2 deform_tc3_kernel:2 tile_sort_kernel:2 preprocess_kernel:2"}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1
 for KS in $LIST; do
