@@ -15,6 +15,9 @@ Citations: `P:n` = /root/reference/PAPER.md line n (later, camera-ready version
 P:611-1251 is authoritative); readings D*/R* are listed in DESIGN.md §3 and
 SURVEY.md §8(c.3).
 
+`oracle.backward` (imported explicitly; it needs torch) restates the forward in PyTorch CPU float64
+ops and differentiates it with autograd: the gradients of the training loss of PAPER.md §4.3.
+
 Pinned by `tests/test_oracle_*.py` (-m "not gpu") against closed forms, worked
 examples (tests/golden/), library routines (scipy SH) and brute force.  The
 only unpinned item is end-to-end image parity with the paper's figures (no
