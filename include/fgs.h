@@ -211,6 +211,52 @@ int fgs_frames_host_status(const fgs_gaussians* g_host, const fgs_hexplanes* fie
                            const fgs_camera* cams, int32_t n_frames, const void* dev_ws, size_t dev_ws_bytes,
                            fgs_stream_t stream);
 
+/* ---- training side: loss and gradients (§4.3 P:828-833 "L = |I^ - I| + L_tv") ----------
+ * The backward of the frame: L1 image loss and grid total variation, then dL/dI^ back through the
+ * splatting (the [3dgs] "differentiable" rasterizer) to the deformed Gaussians, and back through
+ * the deformation field (Eq. 7, phi_d, heads) to the canonical Gaussians, the planes and the MLP.
+ * Discontinuous decisions (culls, tile lists, depth order, alpha skip / stop, 0.99 clamp, colour
+ * clamp, ReLU, AABB clamp, knot indices) are held fixed, as in [3dgs].  Gradients are accumulated in
+ * 2^-40 fixed point with integer atomics: every result is bit-identical from run to run.
+ * Readings B1-B4: L1 = mean over 3 H W of |I^ - I|; L_tv = pooled mean of squared
+ * differences of adjacent entries of all planes, channels and both grid directions; L = L1 + w L_tv. */
+enum { FGS_LOSS_PARTIALS = 1024 };  /* fp64 scratch entries of a loss call (one per block)            */
+typedef struct {                    /* dL/d per-Gaussian arrays (device, fp32, layouts as fgs_gaussians) */
+  float* means;                     /* [n][3] */
+  float* log_scales;                /* [n][3] */
+  float* quats;                     /* [n][4] */
+  float* opacity_logits;            /* [n]    */
+  float* sh;                        /* [n][K][3] */
+} fgs_gaussian_grads;
+typedef struct {                    /* dL/d field + MLP (device, fp32, layouts as fgs_hexplanes / fgs_mlp) */
+  float* planes[FGS_MAX_SCALES][FGS_PLANES];
+  float *w_d, *b_d, *w_x, *b_x, *w_r, *b_r, *w_s, *b_s;
+} fgs_field_grads;
+/* loss[0] = mean |image - target| over [3][H][W] (B2); dL_dimage (may be NULL) = sign(image - target) /
+ * (3 H W), 0 where equal.  partials: device double[FGS_LOSS_PARTIALS] scratch. */
+int fgs_l1_loss(const float* image, const float* target, int32_t width, int32_t height, float* dL_dimage,
+                double* partials, float* loss, fgs_stream_t stream);
+/* loss[0] = weight * L_tv(field) (B1); grads->planes[l][p] (if grads != NULL) += weight * dL_tv/dplane. */
+int fgs_tv_loss(const fgs_hexplanes* field, float weight, fgs_field_grads* grads, double* partials, float* loss,
+                fgs_stream_t stream);
+/* Splat backward for ONE frame: cam, g and the workspace ws must be those of the fgs_render call that
+ * produced `image` (the sorted lists and records are read from ws, which must be unchanged since).
+ * Writes (overwrites) dg->means, log_scales, quats (raw), opacity_logits and sh for all n Gaussians
+ * (0 for culled ones).  scratch: device memory of fgs_render_backward_scratch_bytes(n) bytes. */
+size_t fgs_render_backward_scratch_bytes(int64_t n);
+int fgs_render_backward(const fgs_camera* cam, const fgs_deformed* g, const float* image, const float* dL_dimage,
+                        const void* ws, size_t ws_bytes, void* scratch, size_t scratch_bytes,
+                        const fgs_gaussian_grads* dg, fgs_stream_t stream);
+/* Deformation backward at time t: given dL/dG' (d_deformed: means, log_scales, quats), writes dL/dG for
+ * the canonical means (additive path + the query-position path u(X)), log_scales and quats into
+ * d_canonical (opacity_logits / sh untouched: they are not deformed), and ADDS dL/d planes and MLP
+ * weights into d_field.  Not with the P:1232 decoders (FGS_E_NOTIMPL).  scratch: device memory of
+ * fgs_deform_backward_scratch_bytes(field, mlp) bytes. */
+size_t fgs_deform_backward_scratch_bytes(const fgs_hexplanes* field, const fgs_mlp* mlp);
+int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
+                        const fgs_gaussian_grads* d_deformed, const fgs_gaussian_grads* d_canonical,
+                        const fgs_field_grads* d_field, void* scratch, size_t scratch_bytes, fgs_stream_t stream);
+
 /* ---- profiling -------------------------------------------------------------------------------
  * When enabled, the library records a CUDA event pair around every stage it launches, on the
  * stream of the call.  fgs_profile_read synchronises those events and writes the accumulated

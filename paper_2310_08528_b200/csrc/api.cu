@@ -739,6 +739,119 @@ int fgs_frames_host_status(const fgs_gaussians* gh, const fgs_hexplanes* hh, con
   return FGS_OK;
 }
 
+// ---- training side ----------------------------------------------------------------------------
+int fgs_l1_loss(const float* image, const float* target, int32_t width, int32_t height, float* dL_dimage,
+                double* partials, float* loss, fgs_stream_t stream) {
+  FGS_CHECK(image && target && partials && loss, "null argument");
+  FGS_CHECK(width > 0 && height > 0, "bad image size");
+  const cudaError_t e = launch_l1(image, target, (int64_t)3 * width * height, dL_dimage, partials, loss,
+                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? FGS_OK : cuda_fail(e, "l1 loss");
+}
+
+int fgs_tv_loss(const fgs_hexplanes* h, float weight, fgs_field_grads* grads, double* partials, float* loss,
+                fgs_stream_t stream) {
+  FGS_CHECK(h && partials && loss, "null argument");
+  FGS_CHECK(h->n_scales >= 1 && h->n_scales <= FGS_MAX_SCALES, "n_scales must be in [1,4]");
+  FGS_CHECK(h->feat >= 1 && h->t_res >= 2 && isfinite(weight), "bad field / weight");
+  TvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.feat = h->feat;
+  a.weight = weight;
+  a.partials = partials;
+  a.loss = loss;
+  for (int l = 0; l < h->n_scales; ++l) {
+    FGS_CHECK(h->res[l] >= 2, "res[l] must be >= 2");
+    for (int q = 0; q < FGS_PLANES; ++q) {
+      FGS_CHECK(h->planes[l][q], "null plane");
+      const int k = a.n_planes++;
+      a.planes[k] = h->planes[l][q];
+      a.na[k] = h->res[l];
+      a.nb[k] = q < 3 ? h->res[l] : h->t_res;
+      a.grads[k] = grads ? grads->planes[l][q] : nullptr;
+    }
+  }
+  const cudaError_t e = launch_tv(a, (cudaStream_t)stream);
+  return e == cudaSuccess ? FGS_OK : cuda_fail(e, "tv loss");
+}
+
+size_t fgs_render_backward_scratch_bytes(int64_t n) {
+  return n < 0 ? 0 : (size_t)std::max<int64_t>(n, 1) * 9 * sizeof(unsigned long long);
+}
+
+int fgs_render_backward(const fgs_camera* cam, const fgs_deformed* g, const float* image, const float* dL_dimage,
+                        const void* ws, size_t ws_bytes, void* scratch, size_t scratch_bytes,
+                        const fgs_gaussian_grads* dg, fgs_stream_t stream) {
+  int rc;
+  if ((rc = check_camera(cam)) != FGS_OK) return rc;
+  if ((rc = check_deformed(g, g ? g->n : 0, g ? g->sh_degree : 0, false)) != FGS_OK) return rc;
+  FGS_CHECK(g->n >= 0 && g->n < ((int64_t)1 << 31) && g->sh_degree >= 0 && g->sh_degree <= 3, "bad deformed set");
+  FGS_CHECK(image && dL_dimage && ws && scratch && dg, "null argument");
+  FGS_CHECK(scratch_bytes >= fgs_render_backward_scratch_bytes(g->n), "scratch too small");
+  const int64_t n = g->n;
+  if (n == 0) return FGS_OK;
+  FGS_CHECK(dg->means && dg->log_scales && dg->quats && dg->opacity_logits && dg->sh, "null gradient array");
+  const int W = cam->width, H = cam->height;
+  const size_t per = ws_bytes & ~(size_t)255;
+  const int64_t cap = capacity_for(n, W, H, per);
+  FGS_CHECK(cap > 0, "workspace too small (see fgs_render_workspace_bytes)");
+  RenderBatch b;
+  memset(&b, 0, sizeof(b));
+  b.L = make_layout(n, W, H, cap);
+  b.n = n; b.n_frames = 1; b.sh_degree = g->sh_degree;
+  b.width = W; b.height = H; b.gx = b.L.gx; b.gy = b.L.gy; b.ntiles = b.L.ntiles;
+  b.ws = (char*)const_cast<void*>(ws); b.ws_stride = per;
+  FrameCam& fc = b.cam[0];
+  memcpy(fc.R, cam->R, sizeof(fc.R)); memcpy(fc.t, cam->t, sizeof(fc.t));
+  fc.fx = cam->fx; fc.fy = cam->fy; fc.cx = cam->cx; fc.cy = cam->cy;
+  memcpy(fc.bg, cam->bg, sizeof(fc.bg));
+  b.means[0] = g->means; b.log_scales[0] = g->log_scales; b.quats[0] = g->quats;
+  b.opacity[0] = g->opacity_logits; b.sh[0] = g->sh;
+  const cudaError_t e = launch_render_backward(b, image, dL_dimage, (unsigned long long*)scratch, dg->means,
+                                               dg->log_scales, dg->quats, dg->opacity_logits, dg->sh,
+                                               (cudaStream_t)stream);
+  return e == cudaSuccess ? FGS_OK : cuda_fail(e, "render backward");
+}
+
+size_t fgs_deform_backward_scratch_bytes(const fgs_hexplanes* field, const fgs_mlp* mlp) {
+  if (!field || !mlp || field->n_scales < 1 || field->n_scales > FGS_MAX_SCALES) return 0;
+  DeformBatch p;
+  memset(&p, 0, sizeof(p));
+  p.n_scales = field->n_scales; p.feat = field->feat; p.t_res = field->t_res;
+  for (int l = 0; l < field->n_scales; ++l) p.res[l] = field->res[l];
+  p.width = mlp->width; p.in_dim = mlp->in_dim;
+  return deform_backward_acc_elems(p) * sizeof(unsigned long long);
+}
+
+int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs_mlp* m, float t,
+                        const fgs_gaussian_grads* dd, const fgs_gaussian_grads* dc, const fgs_field_grads* df,
+                        void* scratch, size_t scratch_bytes, fgs_stream_t stream) {
+  int rc;
+  if ((rc = check_gaussians(g)) != FGS_OK) return rc;
+  if ((rc = check_field(h, m)) != FGS_OK) return rc;
+  FGS_CHECK(isfinite(t) && t >= 0.f && t <= 1.f, "t must be finite and in [0,1]");
+  FGS_CHECK(dd && dc && df && scratch, "null argument");
+  if (m->w_c || m->w_a) return fail(FGS_E_NOTIMPL, "backward of the P:1232 colour / opacity decoders");
+  FGS_CHECK(scratch_bytes >= fgs_deform_backward_scratch_bytes(h, m), "scratch too small");
+  for (int l = 0; l < h->n_scales; ++l)
+    for (int q = 0; q < FGS_PLANES; ++q) FGS_CHECK(df->planes[l][q], "null plane gradient");
+  FGS_CHECK(df->w_d && df->b_d && df->w_x && df->b_x && df->w_r && df->b_r && df->w_s && df->b_s,
+            "null MLP gradient");
+  if (g->n > 0)
+    FGS_CHECK(dd->means && dd->log_scales && dd->quats && dc->means && dc->log_scales && dc->quats,
+              "null per-Gaussian gradient");
+  DeformBatch p;
+  fill_deform(p, g, h, m);
+  p.begin = 0; p.end = g->n; p.n_t = 1; p.t[0] = t;
+  float* pg[FGS_MAX_SCALES * FGS_PLANES] = {};
+  for (int l = 0; l < h->n_scales; ++l)
+    for (int q = 0; q < FGS_PLANES; ++q) pg[l * FGS_PLANES + q] = df->planes[l][q];
+  float* mg[8] = {df->w_d, df->b_d, df->w_x, df->b_x, df->w_r, df->b_r, df->w_s, df->b_s};
+  const cudaError_t e = launch_deform_backward(p, dd->means, dd->log_scales, dd->quats, dc->means, dc->log_scales,
+                                               dc->quats, (unsigned long long*)scratch, pg, mg, (cudaStream_t)stream);
+  return e == cudaSuccess ? FGS_OK : cuda_fail(e, "deform backward");
+}
+
 const char* fgs_last_error(void) { return g_err.c_str(); }
 
 

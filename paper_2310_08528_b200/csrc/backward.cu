@@ -1,0 +1,788 @@
+// Training side of the 4D-GS frame on sm_100a — PAPER.md §4.3 "L = |I^ - I| + L_tv", its
+// gradients back through the splatting (the [3dgs] "differentiable" rasterizer, Eq. 1-4)
+// and the deformation field (Eq. 7, phi_d P:791, heads P:797-802).  SURVEY §8(f) rank 4.
+// Readings B1-B4 (loss definitions, what is a parameter) in DESIGN.md §3.
+//
+// Kernels:
+//   l1_kernel / tv_kernel      loss value (block partials in fp64, summed in a fixed order by
+//                              loss_finish_kernel) and its gradient, elementwise (B1, B2).
+//   blend_backward_kernel      one CTA per 16x16 tile: every pixel re-walks its list front to back with
+//                              the forward's own fp32 arithmetic (same e, alpha, T, hence the same skip /
+//                              stop decisions), and for each contributing Gaussian forms the 9 partials
+//                              dL/d(mean2d, log2-domain conic, log2 opacity, rgb); warp butterflies and a
+//                              fixed-order sum over the CTA's warps reduce them per (tile, Gaussian), and
+//                              one fixed-point atomic per component adds them into the Gaussian's
+//                              accumulator.  Integer (2^-40) accumulation is associative: the result is
+//                              bit-identical for every launch order (SPEC S:173 determinism).
+//   preprocess_backward_kernel per Gaussian, fp64: the chain rule through the log2-domain conic, the
+//                              inverse of Sigma2 + 0.3 I, Sigma2 = J W Sigma W^T J^T (J with the 1.3 tan
+//                              clamp), mean2d, Sigma = R S S^T R^T, the quaternion normalisation, the
+//                              sigmoid opacity and the SH colour (clamped at 0) with its view direction.
+//   deform_backward_kernel     per Gaussian: recompute f_h and phi_d, back through the heads, the ReLU,
+//                              W_d and the Hadamard products to the bilinear plane samples; plane
+//                              gradients scattered with fixed-point atomics, MLP weight gradients reduced
+//                              per CTA in a fixed order, dX through both the additive path and the query
+//                              position u(X).
+//   fixed_to_float_kernel      int64 fixed-point accumulators -> fp32 gradients (added to the caller's).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "fgs_internal.cuh"
+
+namespace fgs {
+
+namespace {
+
+constexpr double kFixScale = 1099511627776.0;   // 2^40: fixed-point step 9.1e-13, range +-8.4e6
+constexpr double kLn2 = 0.69314718055994531;
+constexpr float kAlphaMinB = 1.0f / 255.0f;
+constexpr float kTMinB = 1e-4f;
+constexpr float kAlphaMaxB = 0.99f;
+constexpr float kLog2AlphaMinB = -7.9943534368588578f;   // log2(1/255), as the forward blend
+
+__device__ __forceinline__ void fix_add(unsigned long long* acc, double v) {
+  if (v != 0.0) atomicAdd(acc, (unsigned long long)__double2ll_rn(v * kFixScale));
+}
+
+__device__ __forceinline__ float ex2_approx_b(float x) {   // the forward's ex2.approx.ftz
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ------------------------------------------------------------------ losses
+// Block partial of a per-element value, summed in a fixed order (thread-strided, then a fixed tree).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  sm[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = NT / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sm[0];
+  __syncthreads();
+  return r;
+}
+
+constexpr int kLossThreads = 256;
+
+// B2: L1 = mean |I^ - I| over 3 H W values; dL/dI^ = sign(I^ - I) / (3 H W) (0 at equality).
+__global__ void __launch_bounds__(kLossThreads) l1_kernel(const float* __restrict__ img, const float* __restrict__ tgt,
+                                                          int64_t count, float* __restrict__ grad,
+                                                          double* __restrict__ partials) {
+  __shared__ double sm[kLossThreads];
+  const float inv = (float)(1.0 / (double)count);
+  float acc = 0.f;                          // a thread's few elements in fp32, the block sum in fp64
+  for (int64_t i = (int64_t)blockIdx.x * kLossThreads + threadIdx.x; i < count; i += (int64_t)gridDim.x * kLossThreads) {
+    const float d = img[i] - tgt[i];
+    acc += fabsf(d);
+    if (grad) grad[i] = d > 0.f ? inv : (d < 0.f ? -inv : 0.f);
+  }
+  const double s = block_sum<kLossThreads>((double)acc, sm);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s / (double)count;
+}
+
+// B1: L_tv = pooled mean of squared differences of adjacent entries along both grid directions of every
+// plane; d/dP = 2 w / Nterms * (sum over the entry's neighbour pairs of (P - P_neighbour)).  One launch
+// over the concatenated elements of all planes (a.off[q] = first element of plane q).
+__global__ void __launch_bounds__(kLossThreads) tv_kernel(const __grid_constant__ TvArgs a, double inv_terms) {
+  __shared__ double sm[kLossThreads];
+  const int feat = a.feat;
+  const int64_t total = a.off[a.n_planes];
+  float acc = 0.f;
+  int q = 0;
+  for (int64_t e = (int64_t)blockIdx.x * kLossThreads + threadIdx.x; e < total; e += (int64_t)gridDim.x * kLossThreads) {
+    while (e >= a.off[q + 1]) ++q;                    // elements ascend per thread: the plane only advances
+    const int64_t el = e - a.off[q];
+    const int na = a.na[q], nb = a.nb[q];
+    const float* P = a.planes[q];
+    const int64_t ij = el / feat;
+    const int i = (int)(ij % na), j = (int)(ij / na);
+    const float v = P[el];
+    float g = 0.f;
+    if (i + 1 < na) {
+      const float d = P[el + feat] - v;
+      acc = fmaf(d, d, acc);                          // the pair (i, i+1) is counted by its left entry
+      g -= 2.f * d;
+    }
+    if (i > 0) g += 2.f * (v - P[el - feat]);
+    if (j + 1 < nb) {
+      const float d = P[el + (int64_t)na * feat] - v;
+      acc = fmaf(d, d, acc);
+      g -= 2.f * d;
+    }
+    if (j > 0) g += 2.f * (v - P[el - (int64_t)na * feat]);
+    if (a.grads[q]) a.grads[q][el] += (float)((double)a.weight * g * inv_terms);
+  }
+  const double s = block_sum<kLossThreads>((double)acc, sm);
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = s * inv_terms * a.weight;
+}
+
+// loss = sum of partials[0..n): one warp, lane-strided then a fixed butterfly (deterministic)
+__global__ void loss_finish_kernel(const double* __restrict__ partials, int n, float* __restrict__ loss) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) s += partials[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) *loss = (float)s;
+}
+
+// ------------------------------------------------------------------ splat backward
+constexpr int kBwdBatch = 32;
+constexpr int kBwdThreads = 256;
+constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kNPart = 9;   // d mean2d.x, .y, a2, b2, c2, log2 o, r, g, b
+
+struct BwdArgs {
+  RenderBatch b;                    // frame 0: the forward's layout and records
+  const float* image;               // [3][H][W] the forward's output
+  const float* dimg;                // [3][H][W] dL/dI^
+  unsigned long long* acc;          // [n][9] fixed-point accumulators
+};
+
+__global__ void __launch_bounds__(kBwdThreads) blend_backward_kernel(const __grid_constant__ BwdArgs A) {
+  const RenderBatch& b = A.b;
+  const int tile = blockIdx.x;
+  const int tx = tile % b.gx, ty = tile / b.gx;
+  const int lx = threadIdx.x & 15, ly16 = threadIdx.x >> 4;      // pixel (lx, ly16) of the tile
+  const int px = tx * kTile + lx, py = ty * kTile + ly16;
+  const bool inside = px < b.width && py < b.height;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.ranges)[tile];
+  const int L = (int)(rg.y - rg.x);
+  const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, 0, b.L.inst) + rg.x;
+  const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, 0, b.L.rec);
+  __shared__ float4 s_a[kBwdBatch], s_q[kBwdBatch];
+  __shared__ float s_c[kBwdBatch];
+  __shared__ uint32_t s_gid[kBwdBatch];
+  __shared__ float s_red[kBwdWarps][kBwdBatch][kNPart];
+  // the forward's per-pixel arithmetic: dx = mean_rel.x - x, dy = (mean_rel.y - (y & 3)) - 4 (y >> 2)
+  const float fx_ = (float)lx, fy_ = (float)(ly16 & 3), fk4 = 4.f * (float)(ly16 >> 2);
+  float T = 1.f, pc0 = 0.f, pc1 = 0.f, pc2 = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
+  bool done = !inside;
+  if (inside) {
+    const size_t hw = (size_t)b.width * b.height, pix = (size_t)py * b.width + px;
+    C0 = A.image[pix]; C1 = A.image[hw + pix]; C2 = A.image[2 * hw + pix];
+    g0 = A.dimg[pix]; g1 = A.dimg[hw + pix]; g2 = A.dimg[2 * hw + pix];
+  }
+  const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
+  for (int start = 0; start < L; start += kBwdBatch) {
+    if (__syncthreads_count(done) == kBwdThreads) break;
+    if (threadIdx.x < kBwdBatch && start + (int)threadIdx.x < L) {
+      const uint32_t g = (uint32_t)inst[start + threadIdx.x];
+      float4 a = rec[3 * g + 0];
+      const float4 c = rec[3 * g + 2];
+      a.x = (a.x - tx0) + c.y;        // tile-relative mean, exactly as the forward stages it
+      a.y = (a.y - ty0) + c.z;
+      s_a[threadIdx.x] = a;
+      s_q[threadIdx.x] = rec[3 * g + 1];
+      s_c[threadIdx.x] = c.x;
+      s_gid[threadIdx.x] = g;
+    }
+    __syncthreads();
+    const int cnt = min(kBwdBatch, L - start);
+    for (int j = 0; j < cnt; ++j) {
+      float part[kNPart];
+#pragma unroll
+      for (int k = 0; k < kNPart; ++k) part[k] = 0.f;
+      bool contrib = false;
+      if (!done) {
+        const float4 a = s_a[j], q = s_q[j];
+        const float bch = s_c[j];
+        const float dx = a.x - fx_;
+        const float bdx = a.w * dx;
+        const float base = fmaf(a.z * dx, dx, q.y);
+        const float dy = (a.y - fy_) - fk4;
+        const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
+        const float ex = ex2_approx_b(e);
+        const float alpha = fminf(kAlphaMaxB, ex);
+        if (e >= kLog2AlphaMinB) {
+          const float test_T = fmaf(-alpha, T, T);
+          if (test_T < kTMinB) {
+            done = true;
+          } else {
+            contrib = true;
+            const float w = alpha * T;
+            pc0 = fmaf(q.z, w, pc0);
+            pc1 = fmaf(q.w, w, pc1);
+            pc2 = fmaf(bch, w, pc2);
+            // suffix after this Gaussian: S = C_pixel - prefix (incl. this one); dC/dalpha = c T - S / (1 - alpha)
+            const float inv1ma = 1.f / (1.f - alpha);
+            const float dA = g0 * (q.z * T - (C0 - pc0) * inv1ma) + g1 * (q.w * T - (C1 - pc1) * inv1ma)
+                             + g2 * (bch * T - (C2 - pc2) * inv1ma);
+            part[6] = g0 * w;
+            part[7] = g1 * w;
+            part[8] = g2 * w;
+            if (ex < kAlphaMaxB) {          // alpha = 2^e unclamped: dalpha/de = alpha ln 2
+              const float dE = dA * alpha * (float)kLn2;
+              part[0] = dE * (2.f * a.z * dx + a.w * dy);       // de / d mean.x (dx = mean - pixel)
+              part[1] = dE * (a.w * dx + 2.f * q.x * dy);       // de / d mean.y
+              part[2] = dE * dx * dx;                           // de / d a2
+              part[3] = dE * dx * dy;                           // de / d b2
+              part[4] = dE * dy * dy;                           // de / d c2
+              part[5] = dE;                                     // de / d log2 o
+            }
+            T = test_T;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+        for (int k = 0; k < kNPart; ++k) {
+          float v = part[k];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          part[k] = v;
+        }
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < kNPart; ++k) s_red[warp][j][k] = part[k];
+      } else if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kNPart; ++k) s_red[warp][j][k] = 0.f;
+      }
+    }
+    __syncthreads();
+    // per (Gaussian, component): the CTA's warps summed in warp order, one fixed-point atomic
+    for (int idx = threadIdx.x; idx < cnt * kNPart; idx += kBwdThreads) {
+      const int j = idx / kNPart, k = idx - j * kNPart;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kBwdWarps; ++w) s += (double)s_red[w][j][k];
+      fix_add(A.acc + (size_t)s_gid[j] * kNPart + k, s);
+    }
+  }
+}
+
+// Real SH constants with the CS phase (reading R10), as the forward preprocess uses them.
+constexpr double B_C0 = 0.28209479177387814, B_C1 = 0.4886025119029199;
+constexpr double B_C2_0 = 1.0925484305920792, B_C2_1 = -1.0925484305920792, B_C2_2 = 0.31539156525252005,
+                 B_C2_3 = -1.0925484305920792, B_C2_4 = 0.5462742152960396;
+constexpr double B_C3_0 = -0.5900435899266435, B_C3_1 = 2.890611442640554, B_C3_2 = -0.4570457994644658,
+                 B_C3_3 = 0.3731763325901154, B_C3_4 = -0.4570457994644658, B_C3_5 = 1.445305721320277,
+                 B_C3_6 = -0.5900435899266435;
+
+// basis values Y_k(d) and their partials dY_k/d(x, y, z) of the forward's polynomial table
+__device__ __forceinline__ void sh_basis_grad(int deg, double x, double y, double z, double* Y, double (*dY)[3]) {
+  Y[0] = B_C0; dY[0][0] = dY[0][1] = dY[0][2] = 0.0;
+  if (deg >= 1) {
+    Y[1] = -B_C1 * y; dY[1][0] = 0; dY[1][1] = -B_C1; dY[1][2] = 0;
+    Y[2] = B_C1 * z;  dY[2][0] = 0; dY[2][1] = 0; dY[2][2] = B_C1;
+    Y[3] = -B_C1 * x; dY[3][0] = -B_C1; dY[3][1] = 0; dY[3][2] = 0;
+  }
+  if (deg >= 2) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = B_C2_0 * x * y;               dY[4][0] = B_C2_0 * y; dY[4][1] = B_C2_0 * x; dY[4][2] = 0;
+    Y[5] = B_C2_1 * y * z;               dY[5][0] = 0; dY[5][1] = B_C2_1 * z; dY[5][2] = B_C2_1 * y;
+    Y[6] = B_C2_2 * (2 * zz - xx - yy);  dY[6][0] = -2 * B_C2_2 * x; dY[6][1] = -2 * B_C2_2 * y; dY[6][2] = 4 * B_C2_2 * z;
+    Y[7] = B_C2_3 * x * z;               dY[7][0] = B_C2_3 * z; dY[7][1] = 0; dY[7][2] = B_C2_3 * x;
+    Y[8] = B_C2_4 * (xx - yy);           dY[8][0] = 2 * B_C2_4 * x; dY[8][1] = -2 * B_C2_4 * y; dY[8][2] = 0;
+    if (deg >= 3) {
+      Y[9] = B_C3_0 * y * (3 * xx - yy);
+      dY[9][0] = 6 * B_C3_0 * x * y; dY[9][1] = B_C3_0 * (3 * xx - 3 * yy); dY[9][2] = 0;
+      Y[10] = B_C3_1 * x * y * z;
+      dY[10][0] = B_C3_1 * y * z; dY[10][1] = B_C3_1 * x * z; dY[10][2] = B_C3_1 * x * y;
+      Y[11] = B_C3_2 * y * (4 * zz - xx - yy);
+      dY[11][0] = -2 * B_C3_2 * x * y; dY[11][1] = B_C3_2 * (4 * zz - xx - 3 * yy); dY[11][2] = 8 * B_C3_2 * y * z;
+      Y[12] = B_C3_3 * z * (2 * zz - 3 * xx - 3 * yy);
+      dY[12][0] = -6 * B_C3_3 * x * z; dY[12][1] = -6 * B_C3_3 * y * z; dY[12][2] = B_C3_3 * (6 * zz - 3 * xx - 3 * yy);
+      Y[13] = B_C3_4 * x * (4 * zz - xx - yy);
+      dY[13][0] = B_C3_4 * (4 * zz - 3 * xx - yy); dY[13][1] = -2 * B_C3_4 * x * y; dY[13][2] = 8 * B_C3_4 * x * z;
+      Y[14] = B_C3_5 * z * (xx - yy);
+      dY[14][0] = 2 * B_C3_5 * x * z; dY[14][1] = -2 * B_C3_5 * y * z; dY[14][2] = B_C3_5 * (xx - yy);
+      Y[15] = B_C3_6 * x * (xx - 3 * yy);
+      dY[15][0] = B_C3_6 * (3 * xx - 3 * yy); dY[15][1] = -6 * B_C3_6 * x * y; dY[15][2] = 0;
+    }
+  }
+}
+
+struct PreBwdArgs {
+  RenderBatch b;
+  const unsigned long long* acc;   // [n][9]
+  float *d_means, *d_log_scales, *d_quats, *d_opacity, *d_sh;
+};
+
+__global__ void __launch_bounds__(128) preprocess_backward_kernel(const __grid_constant__ PreBwdArgs A) {
+  const RenderBatch& b = A.b;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n) return;
+  const int deg = b.sh_degree, K = (deg + 1) * (deg + 1);
+  const uint32_t tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, 0, b.L.tt)[i];
+  double G[kNPart];
+  for (int k = 0; k < kNPart; ++k) G[k] = (double)(long long)A.acc[i * kNPart + k] / kFixScale;
+  if (tt == 0) {                       // culled: no gradient
+    for (int c = 0; c < 3; ++c) { A.d_means[3 * i + c] = 0.f; A.d_log_scales[3 * i + c] = 0.f; }
+    for (int c = 0; c < 4; ++c) A.d_quats[4 * i + c] = 0.f;
+    A.d_opacity[i] = 0.f;
+    for (int k = 0; k < 3 * K; ++k) A.d_sh[(size_t)i * 3 * K + k] = 0.f;
+    return;
+  }
+  const FrameCam& c = b.cam[0];
+  // ---- recompute the forward (preprocess_kernel's fp64 formulas) ----
+  const float* Xp = b.means[0] + 3 * i;
+  const double x = Xp[0], y = Xp[1], z = Xp[2];
+  double Wm[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) Wm[r][k] = c.R[3 * r + k];
+  const double px = (((Wm[0][0] * x) + Wm[0][1] * y) + Wm[0][2] * z) + (double)c.t[0];
+  const double py = (((Wm[1][0] * x) + Wm[1][1] * y) + Wm[1][2] * z) + (double)c.t[1];
+  const double pz = (((Wm[2][0] * x) + Wm[2][1] * y) + Wm[2][2] * z) + (double)c.t[2];
+  const float* ls = b.log_scales[0] + 3 * i;
+  const double s[3] = {exp((double)ls[0]), exp((double)ls[1]), exp((double)ls[2])};
+  const float* qp = b.quats[0] + 4 * i;
+  const double qr[4] = {qp[0], qp[1], qp[2], qp[3]};
+  const double qn = sqrt(qr[0] * qr[0] + qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
+  const double qw = qr[0] / qn, qx = qr[1] / qn, qy = qr[2] / qn, qz = qr[3] / qn;
+  double R[3][3] = {{1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy)},
+                    {2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx)},
+                    {2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)}};
+  double M[3][3], Sg[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) M[r][k] = R[r][k] * s[k];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) Sg[r][k] = M[r][0] * M[k][0] + M[r][1] * M[k][1] + M[r][2] * M[k][2];
+  const double fx = c.fx, fy = c.fy;
+  const double limx = 1.3 * ((double)b.width / (2.0 * fx)), limy = 1.3 * ((double)b.height / (2.0 * fy));
+  const double rx = px / pz, ry = py / pz;
+  const bool clx = rx < -limx || rx > limx, cly = ry < -limy || ry > limy;
+  const double xt = fmin(limx, fmax(-limx, rx)) * pz, yt = fmin(limy, fmax(-limy, ry)) * pz;
+  const double J[2][3] = {{fx / pz, 0.0, -fx * xt / (pz * pz)}, {0.0, fy / pz, -fy * yt / (pz * pz)}};
+  double Tm[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k) Tm[r][k] = J[r][0] * Wm[0][k] + J[r][1] * Wm[1][k] + J[r][2] * Wm[2][k];
+  double TS[2][3];   // T Sigma
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k) TS[r][k] = Tm[r][0] * Sg[0][k] + Tm[r][1] * Sg[1][k] + Tm[r][2] * Sg[2][k];
+  const double a = TS[0][0] * Tm[0][0] + TS[0][1] * Tm[0][1] + TS[0][2] * Tm[0][2] + 0.3;
+  const double bb = TS[0][0] * Tm[1][0] + TS[0][1] * Tm[1][1] + TS[0][2] * Tm[1][2];
+  const double cc = TS[1][0] * Tm[1][0] + TS[1][1] * Tm[1][1] + TS[1][2] * Tm[1][2] + 0.3;
+  const double det = a * cc - bb * bb;
+  // ---- log2-domain conic (a2, b2, c2) = k (-A/2, -B, -C/2), M^-1 = [[A, B], [B, C]] ----
+  const double kk = 1.4426950408889634;
+  const double dA_ = -0.5 * kk * G[2], dB_ = -kk * G[3], dC_ = -0.5 * kk * G[4];
+  const double iA = cc / det, iB = -bb / det, iC = a / det;
+  // dL/dM = -M^-1 Gs M^-1 with Gs = [[dA, dB/2], [dB/2, dC]] (symmetric)
+  const double g00 = dA_, g01 = 0.5 * dB_, g11 = dC_;
+  const double t00 = iA * g00 + iB * g01, t01 = iA * g01 + iB * g11;
+  const double t10 = iB * g00 + iC * g01, t11 = iB * g01 + iC * g11;
+  const double dM00 = -(t00 * iA + t01 * iB), dM01 = -(t00 * iB + t01 * iC), dM11 = -(t10 * iB + t11 * iC);
+  // G2 = dL/dSigma2 as a symmetric matrix: [[dM00, dM01], [dM01, dM11]]
+  const double G2[2][2] = {{dM00, dM01}, {dM01, dM11}};
+  // dSigma = T^T G2 T ; dT = 2 G2 T Sigma
+  double GT[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k) GT[r][k] = G2[r][0] * Tm[0][k] + G2[r][1] * Tm[1][k];
+  double dS[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) dS[r][k] = Tm[0][r] * GT[0][k] + Tm[1][r] * GT[1][k];
+  double dT[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k)
+      dT[r][k] = 2.0 * (G2[r][0] * TS[0][k] + G2[r][1] * TS[1][k]);
+  // dJ = dT W^T
+  double dJ[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 3; ++k) dJ[r][k] = dT[r][0] * Wm[k][0] + dT[r][1] * Wm[k][1] + dT[r][2] * Wm[k][2];
+  // ---- camera-space point: J, mean2d ----
+  double dpx = 0.0, dpy = 0.0, dpz = 0.0;
+  const double iz = 1.0 / pz, iz2 = iz * iz, iz3 = iz2 * iz;
+  dpz += dJ[0][0] * (-fx * iz2) + dJ[1][1] * (-fy * iz2);
+  if (!clx) { dpx += dJ[0][2] * (-fx * iz2); dpz += dJ[0][2] * (2.0 * fx * px * iz3); }
+  else      { dpz += dJ[0][2] * (fx * (rx > 0 ? limx : -limx) * iz2); }
+  if (!cly) { dpy += dJ[1][2] * (-fy * iz2); dpz += dJ[1][2] * (2.0 * fy * py * iz3); }
+  else      { dpz += dJ[1][2] * (fy * (ry > 0 ? limy : -limy) * iz2); }
+  dpx += G[0] * fx * iz;
+  dpz += -G[0] * fx * px * iz2;
+  dpy += G[1] * fy * iz;
+  dpz += -G[1] * fy * py * iz2;
+  double dX[3];
+  for (int k = 0; k < 3; ++k) dX[k] = Wm[0][k] * dpx + Wm[1][k] * dpy + Wm[2][k] * dpz;
+  // ---- Sigma = M M^T, M = R diag(s): dM = 2 dSigma M ----
+  double dMm[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) dMm[r][k] = 2.0 * (dS[r][0] * M[0][k] + dS[r][1] * M[1][k] + dS[r][2] * M[2][k]);
+  double dR[3][3];
+  for (int k = 0; k < 3; ++k) {
+    double ds = 0.0;
+    for (int r = 0; r < 3; ++r) { ds += dMm[r][k] * R[r][k]; dR[r][k] = dMm[r][k] * s[k]; }
+    A.d_log_scales[3 * i + k] = (float)(ds * s[k]);
+  }
+  // dR -> d qhat (w, x, y, z)
+  double dq[4];
+  dq[0] = 2 * (-qz * dR[0][1] + qy * dR[0][2] + qz * dR[1][0] - qx * dR[1][2] - qy * dR[2][0] + qx * dR[2][1]);
+  dq[1] = 2 * (qy * dR[0][1] + qz * dR[0][2] + qy * dR[1][0] - 2 * qx * dR[1][1] - qw * dR[1][2] + qz * dR[2][0]
+               + qw * dR[2][1] - 2 * qx * dR[2][2]);
+  dq[2] = 2 * (-2 * qy * dR[0][0] + qx * dR[0][1] + qw * dR[0][2] + qx * dR[1][0] + qz * dR[1][2] - qw * dR[2][0]
+               + qz * dR[2][1] - 2 * qy * dR[2][2]);
+  dq[3] = 2 * (-2 * qz * dR[0][0] - qw * dR[0][1] + qx * dR[0][2] + qw * dR[1][0] - 2 * qz * dR[1][1] + qy * dR[1][2]
+               + qx * dR[2][0] + qy * dR[2][1]);
+  const double qh[4] = {qw, qx, qy, qz};
+  const double dot = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+  for (int k = 0; k < 4; ++k) A.d_quats[4 * i + k] = (float)((dq[k] - qh[k] * dot) / qn);
+  // ---- opacity: log2 o = log2 sigmoid(logit): d/dlogit = (1 - o) / ln 2 ----
+  const double lg = b.opacity[0][i];
+  const double o = 1.0 / (1.0 + exp(-lg));
+  A.d_opacity[i] = (float)(G[5] * (1.0 - o) / kLn2);
+  // ---- SH colour: rgb = max(0, sum Y_k C_k + 0.5) at d = normalize(X - campos) ----
+  const double cxw = -(Wm[0][0] * c.t[0] + Wm[1][0] * c.t[1] + Wm[2][0] * c.t[2]);
+  const double cyw = -(Wm[0][1] * c.t[0] + Wm[1][1] * c.t[1] + Wm[2][1] * c.t[2]);
+  const double czw = -(Wm[0][2] * c.t[0] + Wm[1][2] * c.t[1] + Wm[2][2] * c.t[2]);
+  const double vx = x - cxw, vy = y - cyw, vz = z - czw;
+  const double vn = sqrt(vx * vx + vy * vy + vz * vz);
+  const double dx_ = vx / vn, dy_ = vy / vn, dz_ = vz / vn;
+  double Y[16], dY[16][3];
+  sh_basis_grad(deg, dx_, dy_, dz_, Y, dY);
+  const float* sh = b.sh[0] + (size_t)i * 3 * K;
+  double ddir[3] = {0.0, 0.0, 0.0};
+  for (int ch = 0; ch < 3; ++ch) {
+    double raw = 0.5;
+    for (int k = 0; k < K; ++k) raw += Y[k] * (double)sh[3 * k + ch];
+    const double gch = raw > 0.0 ? G[6 + ch] : 0.0;      // clamp at 0 (R10)
+    for (int k = 0; k < K; ++k) {
+      A.d_sh[(size_t)i * 3 * K + 3 * k + ch] = (float)(Y[k] * gch);
+      for (int a3 = 0; a3 < 3; ++a3) ddir[a3] += gch * (double)sh[3 * k + ch] * dY[k][a3];
+    }
+  }
+  const double ddot = dx_ * ddir[0] + dy_ * ddir[1] + dz_ * ddir[2];
+  dX[0] += (ddir[0] - dx_ * ddot) / vn;
+  dX[1] += (ddir[1] - dy_ * ddot) / vn;
+  dX[2] += (ddir[2] - dz_ * ddot) / vn;
+  for (int k = 0; k < 3; ++k) A.d_means[3 * i + k] = (float)dX[k];
+}
+
+// ------------------------------------------------------------------ deform backward
+// One warp per Gaussian at a time, LANES OVER FEATURES (feature k = lane + 32 r of f_h, i.e. scale
+// k / FEAT, channel k % FEAT): every plane corner read is one coalesced row and every plane-gradient
+// atomic of a warp hits consecutive addresses; phi_d and its transpose run lane-parallel over the hidden
+// units with the other operand broadcast by shuffles.  A CTA (8 warps) takes 64 consecutive Gaussians and
+// keeps their f_h, dz, f_d and dOut rows in shared memory for the fixed-order MLP weight reduction.
+constexpr int kDbWarps = 8;
+constexpr int kDbThreads = 32 * kDbWarps;
+constexpr int kDbRows = 64;
+
+struct DefBwdArgs {
+  DeformBatch p;                    // n_t = 1, t[0]
+  const float *d_means, *d_log_scales, *d_quats;     // dL/dG' [n][3|3|4]
+  float *o_means, *o_log_scales, *o_quats;           // dL/dG (canonical), written
+  unsigned long long* acc_planes[FGS_MAX_SCALES][FGS_PLANES];   // fixed-point, same layout as planes
+  unsigned long long *acc_wd, *acc_bd, *acc_wh, *acc_bh;         // [W][IN], [W], [10][W], [10]
+};
+
+template <int W, int IN>
+__global__ void __launch_bounds__(kDbThreads) deform_backward_kernel(const __grid_constant__ DefBwdArgs A) {
+  constexpr int KS = (IN + 31) / 32;       // feature slots per lane
+  constexpr int WS = W / 32;               // hidden-unit slots per lane
+  const DeformBatch& p = A.p;
+  extern __shared__ __align__(16) float dsm[];
+  float* sWd = dsm;                        // [W][IN]   row-major (k contiguous)
+  float* sWdT = sWd + W * IN;              // [IN][W]   transposed (cw contiguous)
+  float* sBd = sWdT + W * IN;              // [W]
+  float* sWh = sBd + W;                    // [10][W] : rows x(3), r(4), s(3)
+  float* sFh = sWh + 10 * W;               // [kDbRows][IN]
+  float* sDz = sFh + kDbRows * IN;         // [kDbRows][W]
+  float* sFd = sDz + kDbRows * W;          // [kDbRows][W]
+  float* sDo = sFd + kDbRows * W;          // [kDbRows][10]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < W * IN; e += kDbThreads) {
+    const float v = p.w_d[e];
+    sWd[e] = v;
+    sWdT[(e % IN) * W + e / IN] = v;
+  }
+  for (int e = tid; e < W; e += kDbThreads) sBd[e] = p.b_d[e];
+  for (int e = tid; e < 10 * W; e += kDbThreads) {
+    const int o = e / W, c = e - o * W;
+    sWh[e] = o < 3 ? p.w_x[o * W + c] : (o < 7 ? p.w_r[(o - 3) * W + c] : p.w_s[(o - 7) * W + c]);
+  }
+  __syncthreads();
+  const int FEAT = p.feat;
+  const int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {1, 2, 2, 3, 3, 3};
+  const int64_t row0 = p.begin + (int64_t)blockIdx.x * kDbRows;
+  const int nrow = (int)(p.end - row0 < (int64_t)kDbRows ? p.end - row0 : (int64_t)kDbRows);
+  const float ut = p.t[0];
+  for (int r = warp; r < kDbRows; r += kDbWarps) {
+    float* fh = sFh + r * IN;
+    float* dz = sDz + r * W;
+    float* fd = sFd + r * W;
+    float* dO = sDo + r * 10;
+    if (r >= nrow) {                          // rows past the range: zero rows for the reduction
+      for (int k = lane; k < IN; k += 32) fh[k] = 0.f;
+      for (int c = lane; c < W; c += 32) { dz[c] = 0.f; fd[c] = 0.f; }
+      if (lane < 10) dO[lane] = 0.f;
+      continue;
+    }
+    const int64_t g = row0 + r;
+    float u[4];
+    bool inb[3];
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3) {
+      const float v = (p.means[g * 3 + a3] - p.bmin[a3]) / p.ext[a3];
+      inb[a3] = v >= 0.f && v <= 1.f;
+      u[a3] = fminf(fmaxf(v, 0.f), 1.f);
+    }
+    u[3] = ut;
+    // ---- forward: f_h[k] = prod over the 6 planes of the bilinear sample (feature k of lane slot) ----
+    float fhv[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = lane + 32 * ks;
+      float f = 0.f;
+      if (k < IN) {
+        const int l = k / FEAT, c = k - l * FEAT;
+        f = 1.f;
+#pragma unroll
+        for (int pl = 0; pl < 6; ++pl) {
+          const int na = PA[pl] < 3 ? p.res[l] : p.t_res, nb = PB[pl] < 3 ? p.res[l] : p.t_res;
+          const float ga = u[PA[pl]] * (float)(na - 1), gb = u[PB[pl]] * (float)(nb - 1);
+          const int i0 = min((int)floorf(ga), na - 2), j0 = min((int)floorf(gb), nb - 2);
+          const float fa = ga - (float)i0, fb = gb - (float)j0;
+          const float* P = p.planes[l][pl] + ((size_t)j0 * na + i0) * FEAT + c;
+          const float v00 = __ldg(P), v01 = __ldg(P + FEAT);
+          const float v10 = __ldg(P + (size_t)na * FEAT), v11 = __ldg(P + (size_t)na * FEAT + FEAT);
+          f *= (1.f - fa) * (1.f - fb) * v00 + fa * (1.f - fb) * v01 + (1.f - fa) * fb * v10 + fa * fb * v11;
+        }
+        fh[k] = f;
+      }
+      fhv[ks] = f;
+    }
+    if (lane < 10) dO[lane] = lane < 3 ? A.d_means[g * 3 + lane] : (lane < 7 ? A.d_quats[g * 4 + lane - 3]
+                                                                             : A.d_log_scales[g * 3 + lane - 7]);
+    __syncwarp();
+    // ---- z = W_d f_h + b_d (hidden unit cw = lane + 32 w), dz = (W_h^T dOut) [z > 0] ----
+    float zz[WS];
+#pragma unroll
+    for (int w = 0; w < WS; ++w) zz[w] = sBd[lane + 32 * w];
+    for (int k = 0; k < IN; ++k) {
+      const float fk = __shfl_sync(0xffffffffu, fhv[k >> 5], k & 31);
+#pragma unroll
+      for (int w = 0; w < WS; ++w) zz[w] = fmaf(sWdT[k * W + lane + 32 * w], fk, zz[w]);
+    }
+    float dzv[WS];
+#pragma unroll
+    for (int w = 0; w < WS; ++w) {
+      const int cw = lane + 32 * w;
+      float dfd = 0.f;
+#pragma unroll
+      for (int o = 0; o < 10; ++o) dfd = fmaf(sWh[o * W + cw], dO[o], dfd);
+      dzv[w] = zz[w] > 0.f ? dfd : 0.f;
+      fd[cw] = fmaxf(zz[w], 0.f);
+      dz[cw] = dzv[w];
+    }
+    // ---- d f_h[k] = sum_cw W_d[cw][k] dz[cw] ----
+    float dfh[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dfh[ks] = 0.f;
+    for (int cw = 0; cw < W; ++cw) {
+      const float d = __shfl_sync(0xffffffffu, dzv[cw >> 5], cw & 31);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = lane + 32 * ks;
+        if (k < IN) dfh[ks] = fmaf(sWd[cw * IN + k], d, dfh[ks]);
+      }
+    }
+    // ---- planes: dv_p = dfh * prod_{q != p} v_q, scattered to the 4 corners; du from dv/du ----
+    float du[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = lane + 32 * ks;
+      if (k >= IN || dfh[ks] == 0.f) continue;
+      const int l = k / FEAT, c = k - l * FEAT;
+      float v[6], w00[6], w01[6], w10[6], w11[6], dva[6], dvb[6];
+      size_t base[6];
+      int rowb[6];
+#pragma unroll
+      for (int pl = 0; pl < 6; ++pl) {
+        const int na = PA[pl] < 3 ? p.res[l] : p.t_res, nb = PB[pl] < 3 ? p.res[l] : p.t_res;
+        const float ga = u[PA[pl]] * (float)(na - 1), gb = u[PB[pl]] * (float)(nb - 1);
+        const int i0 = min((int)floorf(ga), na - 2), j0 = min((int)floorf(gb), nb - 2);
+        const float fa = ga - (float)i0, fb = gb - (float)j0;
+        base[pl] = ((size_t)j0 * na + i0) * FEAT + c;
+        rowb[pl] = na * FEAT;
+        const float* P = p.planes[l][pl] + base[pl];
+        const float v00 = __ldg(P), v01 = __ldg(P + FEAT), v10 = __ldg(P + rowb[pl]), v11 = __ldg(P + rowb[pl] + FEAT);
+        w00[pl] = (1.f - fa) * (1.f - fb); w01[pl] = fa * (1.f - fb);
+        w10[pl] = (1.f - fa) * fb;         w11[pl] = fa * fb;
+        v[pl] = w00[pl] * v00 + w01[pl] * v01 + w10[pl] * v10 + w11[pl] * v11;
+        dva[pl] = ((1.f - fb) * (v01 - v00) + fb * (v11 - v10)) * (float)(na - 1);   // dv / du_a
+        dvb[pl] = ((1.f - fa) * (v10 - v00) + fa * (v11 - v01)) * (float)(nb - 1);   // dv / du_b
+      }
+#pragma unroll
+      for (int pl = 0; pl < 6; ++pl) {
+        float others = 1.f;
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          if (q != pl) others *= v[q];
+        const float dv = dfh[ks] * others;
+        unsigned long long* Ag = A.acc_planes[l][pl] + base[pl];
+        fix_add(Ag, (double)dv * w00[pl]);
+        fix_add(Ag + FEAT, (double)dv * w01[pl]);
+        fix_add(Ag + rowb[pl], (double)dv * w10[pl]);
+        fix_add(Ag + rowb[pl] + FEAT, (double)dv * w11[pl]);
+        if (PA[pl] < 3) du[PA[pl]] += dv * dva[pl];
+        if (PB[pl] < 3) du[PB[pl]] += dv * dvb[pl];
+      }
+    }
+    // du summed over the lanes by a fixed butterfly (deterministic)
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) du[a3] += __shfl_xor_sync(0xffffffffu, du[a3], o);
+    if (lane < 3) {
+      const float dux = inb[lane] ? du[lane] / p.ext[lane] : 0.f;
+      A.o_means[g * 3 + lane] = A.d_means[g * 3 + lane] + dux;
+      A.o_log_scales[g * 3 + lane] = A.d_log_scales[g * 3 + lane];
+    }
+    if (lane < 4) A.o_quats[g * 4 + lane] = A.d_quats[g * 4 + lane];
+  }
+  __syncthreads();
+  // ---- MLP weight gradients: the CTA's rows summed in row order, one fixed-point atomic each ----
+  for (int e = tid; e < W * IN; e += kDbThreads) {
+    const int cw = e / IN, k = e - cw * IN;
+    double sacc = 0.0;
+    for (int r = 0; r < nrow; ++r) sacc += (double)sDz[r * W + cw] * sFh[r * IN + k];
+    fix_add(A.acc_wd + e, sacc);
+  }
+  for (int cw = tid; cw < W; cw += kDbThreads) {
+    double sacc = 0.0;
+    for (int r = 0; r < nrow; ++r) sacc += sDz[r * W + cw];
+    fix_add(A.acc_bd + cw, sacc);
+  }
+  for (int e = tid; e < 10 * W; e += kDbThreads) {
+    const int o = e / W, cw = e - o * W;
+    double sacc = 0.0;
+    for (int r = 0; r < nrow; ++r) sacc += (double)sDo[r * 10 + o] * sFd[r * W + cw];
+    fix_add(A.acc_wh + e, sacc);
+  }
+  if (tid < 10) {
+    double sacc = 0.0;
+    for (int r = 0; r < nrow; ++r) sacc += sDo[r * 10 + tid];
+    fix_add(A.acc_bh + tid, sacc);
+  }
+}
+
+// dst[i] += acc[i] * 2^-40 (fp32); acc zeroed for the next call
+__global__ void fixed_to_float_kernel(unsigned long long* __restrict__ acc, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    dst[i] += (float)((double)(long long)acc[i] / kFixScale);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers (api.cu calls these)
+cudaError_t launch_l1(const float* img, const float* tgt, int64_t count, float* grad, double* partials, float* loss,
+                      cudaStream_t s) {
+  l1_kernel<<<kLossPartials, kLossThreads, 0, s>>>(img, tgt, count, grad, partials);
+  loss_finish_kernel<<<1, 32, 0, s>>>(partials, kLossPartials, loss);
+  note_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tv(const TvArgs& a0, cudaStream_t s) {
+  // pooled mean: count every adjacent pair of every plane (B1)
+  TvArgs a = a0;
+  double terms = 0.0;
+  a.off[0] = 0;
+  for (int q = 0; q < a.n_planes; ++q) {
+    terms += (double)a.feat * ((double)(a.na[q] - 1) * a.nb[q] + (double)a.na[q] * (a.nb[q] - 1));
+    a.off[q + 1] = a.off[q] + (int64_t)a.na[q] * a.nb[q] * a.feat;
+  }
+  tv_kernel<<<kLossPartials, kLossThreads, 0, s>>>(a, 1.0 / terms);
+  loss_finish_kernel<<<1, 32, 0, s>>>(a.partials, kLossPartials, a.loss);
+  note_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_render_backward(const RenderBatch& b, const float* image, const float* dimg,
+                                   unsigned long long* acc, float* d_means, float* d_log_scales, float* d_quats,
+                                   float* d_opacity, float* d_sh, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(acc, 0, (size_t)b.n * kNPart * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  BwdArgs A;
+  A.b = b; A.image = image; A.dimg = dimg; A.acc = acc;
+  blend_backward_kernel<<<(unsigned)b.ntiles, kBwdThreads, 0, s>>>(A);
+  PreBwdArgs P;
+  P.b = b; P.acc = acc; P.d_means = d_means; P.d_log_scales = d_log_scales; P.d_quats = d_quats;
+  P.d_opacity = d_opacity; P.d_sh = d_sh;
+  preprocess_backward_kernel<<<(unsigned)((b.n + 127) / 128), 128, 0, s>>>(P);
+  note_launches(2);
+  return cudaGetLastError();
+}
+
+size_t deform_backward_acc_elems(const DeformBatch& p) {
+  size_t n = 0;
+  for (int l = 0; l < p.n_scales; ++l)
+    for (int q = 0; q < FGS_PLANES; ++q)
+      n += (size_t)(q < 3 ? p.res[l] : p.t_res) * p.res[l] * p.feat;
+  return n + (size_t)p.width * p.in_dim + p.width + 10 * (size_t)p.width + 10;
+}
+
+template <int W, int IN>
+cudaError_t launch_def_bwd_t(const DefBwdArgs& A, unsigned grid, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + 10 * W + (size_t)kDbRows * (IN + 2 * W + 10));
+  cudaError_t e = cudaFuncSetAttribute(deform_backward_kernel<W, IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  deform_backward_kernel<W, IN><<<grid, kDbThreads, smem, s>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const float* dls, const float* dq,
+                                   float* om, float* ols, float* oq, unsigned long long* acc, float* const* plane_grads,
+                                   float* const* mlp_grads, cudaStream_t s) {
+  const size_t total = deform_backward_acc_elems(p);
+  cudaError_t e = cudaMemsetAsync(acc, 0, total * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  DefBwdArgs A;
+  memset(&A, 0, sizeof(A));
+  A.p = p;
+  A.d_means = dm; A.d_log_scales = dls; A.d_quats = dq;
+  A.o_means = om; A.o_log_scales = ols; A.o_quats = oq;
+  size_t off = 0;
+  for (int l = 0; l < p.n_scales; ++l)
+    for (int q = 0; q < FGS_PLANES; ++q) {
+      A.acc_planes[l][q] = acc + off;
+      off += (size_t)(q < 3 ? p.res[l] : p.t_res) * p.res[l] * p.feat;
+    }
+  A.acc_wd = acc + off; off += (size_t)p.width * p.in_dim;
+  A.acc_bd = acc + off; off += p.width;
+  A.acc_wh = acc + off; off += 10 * (size_t)p.width;
+  A.acc_bh = acc + off; off += 10;
+  const unsigned grid = (unsigned)((p.end - p.begin + kDbRows - 1) / kDbRows);
+  if (grid > 0) {
+#define FGS_DB(WW, II) if (p.width == WW && p.in_dim == II) e = launch_def_bwd_t<WW, II>(A, grid, s); else
+    FGS_DB(32, 16) FGS_DB(32, 32) FGS_DB(32, 64) FGS_DB(64, 16) FGS_DB(64, 32) FGS_DB(64, 64)
+    FGS_DB(128, 16) FGS_DB(128, 32) FGS_DB(128, 64) FGS_DB(32, 8) FGS_DB(64, 8) FGS_DB(128, 8)
+    FGS_DB(32, 24) FGS_DB(64, 24) FGS_DB(128, 24) FGS_DB(32, 48) FGS_DB(64, 48) FGS_DB(128, 48)
+    e = cudaErrorInvalidValue;
+#undef FGS_DB
+    if (e != cudaSuccess) return e;
+    note_launches(1);
+  }
+  // fixed point -> fp32, added to the caller's gradients (planes, then the MLP tensors in acc order)
+  off = 0;
+  for (int l = 0; l < p.n_scales; ++l)
+    for (int q = 0; q < FGS_PLANES; ++q) {
+      const size_t n = (size_t)(q < 3 ? p.res[l] : p.t_res) * p.res[l] * p.feat;
+      fixed_to_float_kernel<<<(unsigned)std::min<size_t>(1024, (n + 255) / 256), 256, 0, s>>>(
+          acc + off, plane_grads[l * FGS_PLANES + q], (int64_t)n);
+      off += n;
+    }
+  const size_t W = p.width, IN = p.in_dim;
+  const size_t sizes[8] = {W * IN, W, 3 * W, 3, 4 * W, 4, 3 * W, 3};
+  // acc order: wd | bd | wh (x 3W, r 4W, s 3W) | bh (x 3, r 4, s 3); mlp_grads order w_d b_d w_x b_x w_r b_r w_s b_s
+  const size_t wh0 = off + W * IN + W, bh0 = wh0 + 10 * W;
+  const size_t src[8] = {off, off + W * IN, wh0, bh0, wh0 + 3 * W, bh0 + 3, wh0 + 7 * W, bh0 + 7};
+  for (int k = 0; k < 8; ++k)
+    fixed_to_float_kernel<<<(unsigned)std::min<size_t>(64, (sizes[k] + 255) / 256), 256, 0, s>>>(
+        acc + src[k], mlp_grads[k], (int64_t)sizes[k]);
+  note_launches(p.n_scales * FGS_PLANES + 8);
+  return cudaGetLastError();
+}
+
+}  // namespace fgs

@@ -126,6 +126,30 @@ bool deform_tc3_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
 
+// Training side (backward.cu): losses and gradients (§4.3).
+constexpr int kLossPartials = FGS_LOSS_PARTIALS;  // fp64 block partials of a loss (caller scratch)
+constexpr int kMaxTvPlanes = FGS_MAX_SCALES * FGS_PLANES;
+struct TvArgs {
+  int n_planes, feat;
+  const float* planes[kMaxTvPlanes];
+  int na[kMaxTvPlanes], nb[kMaxTvPlanes];
+  int64_t off[kMaxTvPlanes + 1];   // element offsets of the planes in the concatenated index (launch_tv)
+  float* grads[kMaxTvPlanes];      // may be NULL (loss only)
+  float weight;
+  double* partials;
+  float* loss;
+};
+cudaError_t launch_l1(const float* img, const float* tgt, int64_t count, float* grad, double* partials, float* loss,
+                      cudaStream_t s);
+cudaError_t launch_tv(const TvArgs& a, cudaStream_t s);
+cudaError_t launch_render_backward(const RenderBatch& b, const float* image, const float* dimg,
+                                   unsigned long long* acc, float* d_means, float* d_log_scales, float* d_quats,
+                                   float* d_opacity, float* d_sh, cudaStream_t s);
+size_t deform_backward_acc_elems(const DeformBatch& p);
+cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const float* dls, const float* dq,
+                                   float* om, float* ols, float* oq, unsigned long long* acc, float* const* plane_grads,
+                                   float* const* mlp_grads, cudaStream_t s);
+
 // Tuning knobs (api.cu, fgs_set_tuning).
 int tile_sort_cap();
 int blend_cull();

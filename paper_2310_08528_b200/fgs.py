@@ -64,11 +64,25 @@ class fgs_render_aux(ctypes.Structure):
                                         "binning_direct")]
 
 
+class fgs_gaussian_grads(ctypes.Structure):
+    _fields_ = [(k, c_void_p) for k in ("means", "log_scales", "quats", "opacity_logits", "sh")]
+
+
+class fgs_field_grads(ctypes.Structure):
+    _fields_ = [("planes", (c_void_p * PLANES) * MAX_SCALES)] + [(k, c_void_p) for k in MLP_ARRAYS[:8]]
+
+
+FGS_LOSS_PARTIALS = 1024
+
 _LIB = None
 EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_range_peers", "fgs_deform_batch", "fgs_render_workspace_bytes",
            "fgs_render", "fgs_render_batch", "fgs_render_debug", "fgs_render_status", "fgs_frames",
            "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_frames_host_status", "fgs_profile_enable", "fgs_profile_read",
-           "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version")
+           "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version",
+           "fgs_l1_loss", "fgs_tv_loss", "fgs_render_backward_scratch_bytes", "fgs_render_backward",
+           "fgs_deform_backward_scratch_bytes", "fgs_deform_backward")
+SIZE_EXPORTS = ("fgs_render_workspace_bytes", "fgs_frames_host_workspace_bytes", "fgs_render_backward_scratch_bytes",
+                "fgs_deform_backward_scratch_bytes")
 STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend")
 FGS_TUNE_TILE_SORT_CAP = 0
 FGS_TUNE_BLEND_CULL = 2
@@ -107,6 +121,17 @@ def lib():
                                       c_int32, P(c_void_p), c_void_p, c_size_t, c_void_p]
         L.fgs_frames_host_status.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), P(fgs_camera),
                                              c_int32, c_void_p, c_size_t, c_void_p]
+        L.fgs_l1_loss.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.fgs_tv_loss.argtypes = [P(fgs_hexplanes), c_float, P(fgs_field_grads), c_void_p, c_void_p, c_void_p]
+        L.fgs_render_backward_scratch_bytes.argtypes = [c_int64]
+        L.fgs_render_backward_scratch_bytes.restype = c_size_t
+        L.fgs_render_backward.argtypes = [P(fgs_camera), P(fgs_deformed), c_void_p, c_void_p, c_void_p, c_size_t,
+                                          c_void_p, c_size_t, P(fgs_gaussian_grads), c_void_p]
+        L.fgs_deform_backward_scratch_bytes.argtypes = [P(fgs_hexplanes), P(fgs_mlp)]
+        L.fgs_deform_backward_scratch_bytes.restype = c_size_t
+        L.fgs_deform_backward.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float,
+                                          P(fgs_gaussian_grads), P(fgs_gaussian_grads), P(fgs_field_grads), c_void_p,
+                                          c_size_t, c_void_p]
         L.fgs_profile_enable.argtypes = [c_int]
         L.fgs_profile_read.argtypes = [P(ctypes.c_double), P(c_int64)]
         L.fgs_launch_count.restype = c_int64
@@ -116,8 +141,7 @@ def lib():
         L.fgs_last_error.restype = c_char_p
         L.fgs_version.restype = c_char_p
         for name in EXPORTS:
-            if name not in ("fgs_render_workspace_bytes", "fgs_frames_host_workspace_bytes", "fgs_launch_count",
-                            "fgs_get_tuning", "fgs_last_error", "fgs_version"):
+            if name not in SIZE_EXPORTS + ("fgs_launch_count", "fgs_get_tuning", "fgs_last_error", "fgs_version"):
                 getattr(L, name).restype = c_int
         _LIB = L
     return _LIB
@@ -243,6 +267,38 @@ class tuning:
     def __exit__(self, *exc):
         fgs_set_tuning(self.key, self.old)
         return False
+
+
+def fgs_l1_loss(image, target, dL_dimage, partials, loss, stream=None):
+    """loss[0] = mean |image - target|; dL_dimage = sign / (3HW) (device tensors; partials float64[1024])."""
+    H, W = image.shape[-2], image.shape[-1]
+    return _check(lib().fgs_l1_loss(_ptr(image), _ptr(target), W, H, _ptr(dL_dimage), _ptr(partials), _ptr(loss),
+                                    _stream(stream)))
+
+
+def fgs_tv_loss(field, weight, grads, partials, loss, stream=None):
+    return _check(lib().fgs_tv_loss(ctypes.byref(field), c_float(weight), None if grads is None else ctypes.byref(grads),
+                                    _ptr(partials), _ptr(loss), _stream(stream)))
+
+
+def fgs_render_backward_scratch_bytes(n):
+    return int(lib().fgs_render_backward_scratch_bytes(n))
+
+
+def fgs_render_backward(cam, g, image, dL_dimage, ws, scratch, dg, stream=None):
+    return _check(lib().fgs_render_backward(ctypes.byref(cam), ctypes.byref(g), _ptr(image), _ptr(dL_dimage),
+                                            _ptr(ws), ws.numel(), _ptr(scratch), scratch.numel(), ctypes.byref(dg),
+                                            _stream(stream)))
+
+
+def fgs_deform_backward_scratch_bytes(field, mlp):
+    return int(lib().fgs_deform_backward_scratch_bytes(ctypes.byref(field), ctypes.byref(mlp)))
+
+
+def fgs_deform_backward(g, field, mlp, t, d_deformed, d_canonical, d_field, scratch, stream=None):
+    return _check(lib().fgs_deform_backward(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
+                                            ctypes.byref(d_deformed), ctypes.byref(d_canonical), ctypes.byref(d_field),
+                                            _ptr(scratch), scratch.numel(), _stream(stream)))
 
 
 def fgs_profile_enable(enable=True):
@@ -412,6 +468,29 @@ class DeviceScene:
     def canonical_struct(self) -> fgs_deformed:
         """G itself as an fgs_deformed (render the undeformed scene, e.g. the warm-up / static case)."""
         return self.deformed_struct(self.means, self.log_scales, self.quats)
+
+    def alloc_gaussian_grads(self):
+        """Zeroed device gradient buffers shaped like the Gaussian arrays; returns (struct, tensors)."""
+        import torch
+        t = {k: torch.zeros_like(getattr(self, k)) for k in ("means", "log_scales", "quats", "opacity_logits", "sh")}
+        st = fgs_gaussian_grads(*[t[k].data_ptr() for k in ("means", "log_scales", "quats", "opacity_logits", "sh")])
+        st._keep = t
+        return st, t
+
+    def alloc_field_grads(self):
+        """Zeroed device gradient buffers shaped like the planes and the MLP; returns (struct, tensors)."""
+        import torch
+        t = {}
+        st = fgs_field_grads()
+        for l, ps in enumerate(self.planes):
+            for p, P in enumerate(ps):
+                t[f"plane{l}_{p}"] = torch.zeros_like(P)
+                st.planes[l][p] = t[f"plane{l}_{p}"].data_ptr()
+        for k in MLP_ARRAYS[:8]:
+            t[k] = torch.zeros_like(self.mlp_t[k])
+            setattr(st, k, t[k].data_ptr())
+        st._keep = t
+        return st, t
 
     def alloc_workspace(self, n_frames=1, max_instances=None, width=None, height=None):
         import torch

@@ -1,0 +1,218 @@
+"""GPU parity of the training side (§4.3) against the autograd
+oracle (oracle/backward.py, itself pinned by finite differences in tests/test_oracle_backward.py).
+
+Protocol (reading B5): both sides are fed the same fp32 inputs — for the splat backward
+the GPU's own fp32 G' (as the forward parity protocol P3); gradients are compared per tensor as
+max |g_gpu - g_ref| <= tol * max |g_ref| (tol 1e-4: fp32 arithmetic with ex2.approx and per-pixel
+sums with cancellation against the fp64 oracle; each gradient's scale is its tensor's largest entry).
+Discontinuous decisions are held fixed on both sides; scenes are chosen with no pixel in the oracle's
+decision band so the two sides hold the same decisions.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from paper_2310_08528_b200 import fgs
+from paper_2310_08528_b200.inputs import make_scene, with_heads
+
+from gpu_util import ensure_lib
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    ensure_lib()
+
+
+def _scene(n=40, W=48, H=40, deg=1, seed=0, log_scale=-2.6, heads=0.3, feat=None):
+    s = make_scene("dnerf", n=n, width=W, height=H, n_frames=2, seed=seed)
+    rng = np.random.default_rng(200 + seed)
+    K = (deg + 1) ** 2
+    f32 = np.float32
+    s = dataclasses.replace(s, means=(s.means * 0.6).astype(f32),
+                            log_scales=(log_scale + 0.3 * rng.normal(size=(n, 3))).astype(f32),
+                            sh=np.ascontiguousarray(s.sh[:, :K, :]).astype(f32), sh_degree=deg)
+    if heads:
+        s = with_heads(s, heads, seed=5 + seed, bias_sigma=0.05)
+    return s
+
+
+def _rel(a, b):
+    m = float(np.max(np.abs(b)))
+    return float(np.max(np.abs(a - b))) / m if m > 0 else float(np.max(np.abs(a)))
+
+
+def _forward(ds, s, frame):
+    import torch
+    outs, tens = ds.alloc_deformed(1)
+    fgs.fgs_deform(ds.g, ds.field, ds.mlp, float(s.times[frame]), outs[0])
+    cam = s.cameras[frame]
+    ws = ds.alloc_workspace(1)
+    img = torch.empty((3, cam.height, cam.width), device="cuda")
+    fgs.fgs_render(ds.cams[frame], outs[0], img, ws)
+    fgs.fgs_render_status(ws)
+    return outs[0], tens[0], img, ws
+
+
+@pytest.mark.parametrize("deg,seed", [(0, 0), (1, 1), (3, 2)])
+def test_render_backward_matches_oracle(deg, seed):
+    import torch
+
+    from oracle import backward as B
+    from oracle import render as R
+    s = _scene(deg=deg, seed=seed)
+    ds = fgs.DeviceScene(s)
+    d, tens, img, ws = _forward(ds, s, 0)
+    cam = s.cameras[0]
+    w = np.random.default_rng(7 + seed).normal(size=(3, cam.height, cam.width)).astype(np.float32)
+    wt = torch.from_numpy(w).cuda()
+    dg, gt = ds.alloc_gaussian_grads()
+    scratch = torch.empty(fgs.fgs_render_backward_scratch_bytes(s.n), dtype=torch.uint8, device="cuda")
+    fgs.fgs_render_backward(ds.cams[0], d, img, wt, ws, scratch, dg)
+    torch.cuda.synchronize()
+    G = {k: v.cpu().numpy() for k, v in tens.items()}
+    ref, ref_img = B.render_grads_ref(G, s.opacity_logits, s.sh, s.sh_degree, cam, w)
+    out = R.render_ref(G, s.opacity_logits, s.sh, s.sh_degree, cam)
+    assert not out["flagged"].any()
+    assert np.max(np.abs(img.cpu().numpy() - ref_img)) < 2e-3
+    for k in ("means", "log_scales", "quats", "opacity_logits", "sh"):
+        assert np.any(ref[k] != 0), k
+        err = _rel(gt[k].cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+
+
+def test_deform_backward_matches_oracle():
+    import torch
+
+    from oracle import backward as B
+    s = _scene(n=500, seed=3, heads=0.5)
+    ds = fgs.DeviceScene(s)
+    t = float(s.times[1])
+    rng = np.random.default_rng(9)
+    up = {"means": rng.normal(size=(s.n, 3)), "log_scales": rng.normal(size=(s.n, 3)),
+          "quats": rng.normal(size=(s.n, 4))}
+    up = {k: v.astype(np.float32) for k, v in up.items()}
+    dd, dt = ds.alloc_gaussian_grads()
+    for k, v in up.items():
+        dt[k].copy_(torch.from_numpy(v))
+    dc, ct = ds.alloc_gaussian_grads()
+    df, ft = ds.alloc_field_grads()
+    scratch = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device="cuda")
+    fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dd, dc, df, scratch)
+    torch.cuda.synchronize()
+    ref = B.deform_grads_ref(s, t, up)
+    for k in ("means", "log_scales", "quats"):
+        err = _rel(ct[k].cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+    for k, v in ft.items():
+        assert np.any(ref[k] != 0), k
+        err = _rel(v.cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+    # accumulation: a second call ADDS the field gradients
+    fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dd, dc, df, scratch)
+    torch.cuda.synchronize()
+    assert _rel(ft["w_d"].cpu().numpy(), 2 * ref["w_d"]) <= TOL
+
+
+def test_losses_match_oracle():
+    """L1 value and gradient (B2), TV value and plane gradients (B1) against the oracle."""
+    import torch
+
+    from oracle import backward as B
+    s = _scene(n=50)
+    ds = fgs.DeviceScene(s)
+    rng = np.random.default_rng(3)
+    a = rng.uniform(size=(3, 37, 53)).astype(np.float32)
+    b = rng.uniform(size=(3, 37, 53)).astype(np.float32)
+    b[0, :3, :3] = a[0, :3, :3]                         # exact equality: zero subgradient
+    at, bt = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    grad = torch.empty_like(at)
+    part = torch.empty(fgs.FGS_LOSS_PARTIALS, dtype=torch.float64, device="cuda")
+    loss = torch.empty(1, device="cuda")
+    fgs.fgs_l1_loss(at, bt, grad, part, loss)
+    A = torch.from_numpy(a.astype(np.float64)).requires_grad_(True)
+    L = B.l1_loss(A, b)
+    L.backward()
+    assert abs(float(loss.item()) - float(L.detach())) <= 1e-6 * float(L.detach())
+    assert np.array_equal(grad.cpu().numpy(), A.grad.numpy().astype(np.float32))
+    df, ft = ds.alloc_field_grads()
+    fgs.fgs_tv_loss(ds.field, 0.25, df, part, loss)
+    planes = [torch.from_numpy(np.asarray(P, np.float64)).requires_grad_(True) for ps in s.field.planes for P in ps]
+    Lt = 0.25 * B.tv_loss(planes)
+    Lt.backward()
+    assert abs(float(loss.item()) - float(Lt.detach())) <= 1e-6 * float(Lt.detach())
+    q = 0
+    for l, ps in enumerate(s.field.planes):
+        for p in range(6):
+            err = _rel(ft[f"plane{l}_{p}"].cpu().numpy(), planes[q].grad.numpy())
+            assert err <= 1e-5, (l, p, err)
+            q += 1
+
+
+def _train_frame(ds, s, frame, target_t, tvw):
+    """The whole training-side chain of one frame on the GPU; returns (loss, canonical grads, field grads)."""
+    import torch
+    d, tens, img, ws = _forward(ds, s, frame)
+    dimg = torch.empty_like(img)
+    part = torch.empty(fgs.FGS_LOSS_PARTIALS, dtype=torch.float64, device="cuda")
+    l1 = torch.empty(1, device="cuda")
+    tv = torch.empty(1, device="cuda")
+    fgs.fgs_l1_loss(img, target_t, dimg, part, l1)
+    dg, gt = ds.alloc_gaussian_grads()
+    rs = torch.empty(fgs.fgs_render_backward_scratch_bytes(s.n), dtype=torch.uint8, device="cuda")
+    fgs.fgs_render_backward(ds.cams[frame], d, img, dimg, ws, rs, dg)
+    df, ft = ds.alloc_field_grads()
+    fgs.fgs_tv_loss(ds.field, tvw, df, part, tv)
+    dc, ct = ds.alloc_gaussian_grads()
+    dsb = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device="cuda")
+    fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, float(s.times[frame]), dg, dc, df, dsb)
+    torch.cuda.synchronize()
+    canon = {k: ct[k].cpu().numpy() for k in ("means", "log_scales", "quats")}
+    canon["opacity_logits"] = gt["opacity_logits"].cpu().numpy()
+    canon["sh"] = gt["sh"].cpu().numpy()
+    return float(l1.item() + tv.item()), canon, {k: v.cpu().numpy() for k, v in ft.items()}
+
+
+def test_full_frame_gradients_match_oracle():
+    """L = L1 + w L_tv of one frame, every parameter's gradient (canonical Gaussians, planes, MLP) from
+    the GPU chain fgs_deform -> fgs_render -> fgs_l1_loss / fgs_tv_loss -> fgs_render_backward ->
+    fgs_deform_backward, against the autograd oracle of the same frame."""
+    import torch
+
+    from oracle import backward as B
+    s = _scene(n=60, W=40, H=32, deg=1, seed=4)
+    ds = fgs.DeviceScene(s)
+    frame = 1
+    cam = s.cameras[frame]
+    target = np.random.default_rng(2).uniform(size=(3, cam.height, cam.width)).astype(np.float32)
+    L, canon, field = _train_frame(ds, s, frame, torch.from_numpy(target).cuda(), 0.05)
+    ref, Lref, _ = B.grads_ref(s, frame, target, 0.05)
+    assert abs(L - Lref) <= 1e-4 * abs(Lref)
+    for k, v in canon.items():
+        err = _rel(v, ref[k])
+        assert err <= TOL, (k, err)
+    for k, v in field.items():
+        err = _rel(v, ref[k])
+        assert err <= TOL, (k, err)
+
+
+def test_backward_deterministic_full_size():
+    """The training chain on a full-size D frame (100k Gaussians, 800x800): finite gradients, and two runs
+    bit-identical (fixed-point accumulation: SPEC S:173)."""
+    import torch
+    s = make_scene("dnerf", n_frames=2)
+    ds = fgs.DeviceScene(s)
+    target = torch.rand((3, 800, 800), generator=torch.Generator().manual_seed(0)).cuda()
+    a = _train_frame(ds, s, 1, target, 0.01)
+    b = _train_frame(ds, s, 1, target, 0.01)
+    assert a[0] == b[0]
+    for x, y in ((a[1], b[1]), (a[2], b[2])):
+        for k in x:
+            assert np.all(np.isfinite(x[k])), k
+            assert np.array_equal(x[k], y[k]), k
+    assert np.abs(a[1]["means"]).max() > 0 and np.abs(a[2]["w_d"]).max() > 0
