@@ -466,6 +466,10 @@ def run_fgs(args, scene, rank, world, local_rank):
     build.build()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.radix is not None:
+        fgs.fgs_set_tuning(fgs.FGS_TUNE_RADIX, args.radix)
+    if args.radix_min_list is not None:
+        fgs.fgs_set_tuning(fgs.FGS_TUNE_RADIX_MIN_LIST, args.radix_min_list)
     F_all = scene.n_frames
     # (e1) frame-batch split: the config's batch is cut across ranks (strong scaling); --weak gives every
     # rank its own copy of the whole batch instead
@@ -818,6 +822,9 @@ def main():
                     help="P:1232 variant: add the colour / opacity decoders phi_C, phi_alpha (SURVEY 8(f) rank 2)")
     ap.add_argument("--n", type=int, default=None,
                     help="override the number of Gaussians (SURVEY 8(f) N-sweep: same distributions)")
+    ap.add_argument("--radix", type=int, default=None, choices=[0, 1, 2],
+                    help="FGS_TUNE_RADIX: 0 per-tile sorts, 1 auto (library default), 2 radix binning path")
+    ap.add_argument("--radix-min-list", type=int, default=None, help="FGS_TUNE_RADIX_MIN_LIST (auto threshold)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--weak", action="store_true",
                     help="frames mode under torchrun: every rank renders its own copy of the whole batch (weak "

@@ -291,8 +291,16 @@ int64_t fgs_launch_count(void);
  * shared memory when the CTA's rect union holds at most this many tiles, else use direct global
  * atomics.  Range [1, 4096], default 4096.  Results are identical for every value (tests lower it to
  * force the direct path; fgs_render_aux.binning_direct counts the CTAs that took it).
+ * FGS_TUNE_RADIX: how a frame's tile lists are put in (tile, depth, index) order.  0 (default) = per-tile sorts
+ * (the warp and long-list sorts above); 2 = the radix binning path for every frame: a stable LSD radix
+ * sort of the Gaussians by depth key, emission of the instances in that order, and stable radix passes on
+ * the tile id (images of up to 65536 tiles); 1 = the radix path for frames whose mean list length
+ * M / tiles reaches FGS_TUNE_RADIX_MIN_LIST (default 768; range [1, 2^20]), the per-tile sorts for the
+ * others.  Default 0 (the per-tile sorts were faster at every measured N).  The order, hence every image,
+ * is identical whichever path a frame takes.
  * (Key 1 is retired: there is a single deformation kernel.) */
-enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_BLEND_CULL = 2, FGS_TUNE_AGG_TILES = 3 };
+enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_BLEND_CULL = 2, FGS_TUNE_AGG_TILES = 3, FGS_TUNE_RADIX = 4,
+       FGS_TUNE_RADIX_MIN_LIST = 5 };
 int fgs_set_tuning(int32_t key, int64_t value);
 int64_t fgs_get_tuning(int32_t key);
 

@@ -213,6 +213,8 @@ int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* 
   local.sort_cap = tile_sort_cap();
   local.cull = blend_cull();
   local.agg_tiles = agg_tiles();
+  local.radix_mode = local.L.ntiles <= kRxMaxTiles ? radix_mode() : 0;
+  local.radix_min_list = radix_min_list();
   local.debug = aux != nullptr;
   local.blend_work = aux ? (unsigned long long*)aux->blend_work : nullptr;
   local.ws_stride = per;
@@ -305,6 +307,10 @@ WsLayout make_layout(int64_t n, int width, int height, int64_t cap) {
   L.order = take(4 * nt);
   L.inst = take(8 * cc);
   L.inst2 = take(8 * cc);
+  L.rx_blocks = (int)((std::max<int64_t>(std::max<int64_t>(n, cap), 1) + kRxItems - 1) / kRxItems);
+  L.rx_hist = take(4 * 256 * (size_t)L.rx_blocks);
+  L.rx_dtot = take(4 * 256);
+  L.rx_bsum = take(4 * (size_t)((std::max<int64_t>(n, 1) + kRxItems - 1) / kRxItems));
   L.total = o;
   return L;
 }
@@ -324,10 +330,14 @@ namespace {
 std::atomic<int> g_tile_sort_cap{kBlendSortMax};
 std::atomic<int> g_blend_cull{1};
 std::atomic<int> g_agg_tiles{kAggTilesMax};
+std::atomic<int> g_radix_mode{0};
+std::atomic<int> g_radix_min_list{kRadixMinListDefault};
 }
 int tile_sort_cap() { return g_tile_sort_cap.load(std::memory_order_relaxed); }
 int blend_cull() { return g_blend_cull.load(std::memory_order_relaxed); }
 int agg_tiles() { return g_agg_tiles.load(std::memory_order_relaxed); }
+int radix_mode() { return g_radix_mode.load(std::memory_order_relaxed); }
+int radix_min_list() { return g_radix_min_list.load(std::memory_order_relaxed); }
 
 }  // namespace fgs
 
@@ -478,6 +488,14 @@ int fgs_set_tuning(int32_t key, int64_t value) {
       FGS_CHECK(value >= 1 && value <= kAggTilesMax, "aggregation limit must be in [1, 4096]");
       g_agg_tiles.store((int)value);
       return FGS_OK;
+    case FGS_TUNE_RADIX:
+      FGS_CHECK(value >= 0 && value <= 2, "radix mode must be 0, 1 or 2");
+      g_radix_mode.store((int)value);
+      return FGS_OK;
+    case FGS_TUNE_RADIX_MIN_LIST:
+      FGS_CHECK(value >= 1 && value <= (1 << 20), "radix threshold must be in [1, 2^20]");
+      g_radix_min_list.store((int)value);
+      return FGS_OK;
     default:
       return fail(FGS_E_INVALID, "unknown tuning key");
   }
@@ -487,6 +505,8 @@ int64_t fgs_get_tuning(int32_t key) {
   if (key == FGS_TUNE_TILE_SORT_CAP) return tile_sort_cap();
   if (key == FGS_TUNE_BLEND_CULL) return blend_cull();
   if (key == FGS_TUNE_AGG_TILES) return agg_tiles();
+  if (key == FGS_TUNE_RADIX) return radix_mode();
+  if (key == FGS_TUNE_RADIX_MIN_LIST) return radix_min_list();
   return -1;
 }
 

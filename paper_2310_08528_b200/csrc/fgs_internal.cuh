@@ -33,6 +33,8 @@ constexpr int kScanThreads = 1024;           // tile-count scan CTA (one per fra
 constexpr int kBlendThreads = 128;           // blend CTA: 4 warps x 8x8 pixel boxes of a 16x16 tile
 constexpr int kBlendSortMax = 1024;          // longest tile list one warp sorts (tile_sort_kernel); longer: long_sort_kernel
 constexpr int kLargeSortThreads = 256;       // CTA sort of lists longer than the warp-sort cap
+constexpr int kRxItems = 4096;               // items per block of the radix binning passes (radix.cu)
+constexpr int kRxMaxTiles = 65536;           // tile ids the two 8-bit tile passes cover
 
 // Per-frame workspace layout (all offsets in bytes from the frame's slice, 256-B aligned).
 struct WsLayout {
@@ -40,7 +42,8 @@ struct WsLayout {
   int width = 0, height = 0, gx = 0, gy = 0, ntiles = 0;
   size_t cnt = 0;            // uint32[16]: 0 n, 1 M clamped to cap, 2 overflow flag, 3 M raw, 4 long lists,
                              // 5 (frame 0) long-list claim counter of the batch, 6 / 7 CTAs of
-                             // preprocess / duplicate that took the direct-atomics binning path
+                             // preprocess / duplicate that took the direct-atomics binning path,
+                             // 8 the frame takes the radix binning path (radix.cu)
   size_t keys = 0;           // uint32[n] depth key (IEEE bits of fp32 view depth), gid order
   size_t tt = 0;             // uint32[n] tiles_touched
   size_t rect = 0;           // uint2[n]  (x0 | y0<<16, x1 | y1<<16)
@@ -52,7 +55,11 @@ struct WsLayout {
   size_t long_list = 0;      // uint32[ntiles] tiles whose lists exceed the warp-sort cap (count in cnt[4])
   size_t order = 0;          // uint32[ntiles] tiles by descending list length (blend dispatch order)
   size_t inst = 0;           // uint64[cap] instances (depth_key << 32 | gid), bucketed by tile
-  size_t inst2 = 0;          // uint64[cap] scratch of the long-list sort
+  size_t inst2 = 0;          // uint64[cap] scratch of the long-list sort / the radix passes
+  int rx_blocks = 0;         // blocks of kRxItems over max(n, cap): the radix histogram stride
+  size_t rx_hist = 0;        // uint32[256][rx_blocks] per-block digit counts -> offsets (radix.cu)
+  size_t rx_dtot = 0;        // uint32[256] digit totals of a pass
+  size_t rx_bsum = 0;        // uint32[ceil(n / kRxItems)] tiles_touched sums of depth-ordered blocks
   size_t total = 0;
 };
 
@@ -75,6 +82,8 @@ struct RenderBatch {
   int debug;                 // 1: blend writes each tile's sorted list back (fgs_render_debug)
   int cull;                  // 1: per-warp ellipse cull in the blend (FGS_TUNE_BLEND_CULL), 0: none
   int agg_tiles;             // CTA binning aggregation limit in tiles (FGS_TUNE_AGG_TILES, <= 4096)
+  int radix_mode;            // FGS_TUNE_RADIX: 0 per-tile sorts only, 1 auto, 2 radix path for every frame
+  int radix_min_list;        // auto: a frame takes the radix path when M >= radix_min_list x tiles
   char* ws;                  // frame f slice = ws + f * ws_stride
   size_t ws_stride;
   WsLayout L;
@@ -124,6 +133,7 @@ struct DeformBatch {
 cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s);  // warp-specialised v3 (deform_tc3.cu)
 bool deform_tc3_supported(const DeformBatch& p);
 cudaError_t launch_render(const RenderBatch& b, cudaStream_t s);
+cudaError_t launch_radix_bin(const RenderBatch& b, cudaStream_t s);
 cudaError_t launch_debug_copy(const RenderBatch& b, const fgs_render_aux& aux, cudaStream_t s);
 
 // Training side (backward.cu): losses and gradients (§4.3).
@@ -154,7 +164,10 @@ cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const 
 int tile_sort_cap();
 int blend_cull();
 int agg_tiles();
+int radix_mode();
+int radix_min_list();
 constexpr int kAggTilesMax = 4096;           // shared histogram of the CTA binning aggregation
+constexpr int kRadixMinListDefault = 768;    // FGS_TUNE_RADIX_MIN_LIST default (mean list length)
 
 // Profiling / launch accounting (api.cu).
 void prof_mark(int stage, bool begin, cudaStream_t s);

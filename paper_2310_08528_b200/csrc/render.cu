@@ -343,6 +343,9 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_co
     cnt[3] = total;
     cnt[1] = (uint32_t)((uint64_t)total < cap ? (uint64_t)total : cap);
     cnt[2] = (uint64_t)total > cap ? 1u : 0u;
+    // binning path of this frame (radix.cu): the radix passes when the lists are long on average
+    cnt[8] = (b.radix_mode == 2 || (b.radix_mode == 1 && (uint64_t)total >= (uint64_t)b.radix_min_list * (uint64_t)nt))
+                 ? 1u : 0u;
   }
   // Blend dispatch order: the frame's tiles by descending list length (counting sort on the length,
   // capped), so the longest tiles start first and the grid does not end on a long tile — the blend
@@ -375,6 +378,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_co
 // ------------------------------------------------------------------------------ duplicate (a5)
 __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
+  if (cnt_ptr(b, f)[8]) return;                 // the radix path emits this frame's instances (radix.cu)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < b.n;
   const uint32_t* tt = ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.tt);
@@ -603,6 +607,7 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)(blockIdx.x / (unsigned)b.n_frames) * kTileSortWarps + warp;
   if (rank >= b.ntiles) return;                 // no CTA-wide barriers below
+  if (cnt_ptr(b, f)[8]) return;                 // radix path: the lists are already in order
   const int tile = (int)ws_ptr<uint32_t>(b.ws, b.ws_stride, f, b.L.order)[rank];
   FGS_DCHECK(tile >= 0 && tile < b.ntiles);
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
@@ -1097,6 +1102,14 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   note_launches(1);
   prof_mark(FGS_STAGE_DUPLICATE, false, s);
   prof_mark(FGS_STAGE_TILE_SORT, true, s);
+  // radix binning path (radix.cu) for the frames tile_scan selected (it emits their instances, so on
+  // those frames the stage holds the key duplication too); launched only when some frame may take it:
+  // always (mode 2), or in auto mode when there are at least 64 Gaussians per tile (a mean list of
+  // radix_min_list needs ~radix_min_list / 6 Gaussians per tile at the configs' ~6 tiles per Gaussian)
+  if (b.radix_mode == 2 || (b.radix_mode == 1 && b.n >= (int64_t)64 * b.ntiles)) {
+    const cudaError_t e = launch_radix_bin(b, s);
+    if (e != cudaSuccess) return e;
+  }
   tile_sort_kernel<<<(unsigned)(F * ((b.ntiles + kTileSortWarps - 1) / kTileSortWarps)), 32 * kTileSortWarps, 0, s>>>(b);
   // long lists: persistent CTAs (3 per SM over the batch) walk each frame's worklist (usually empty)
   // (per call: the attribute is per device, and the calling thread's current device may change)

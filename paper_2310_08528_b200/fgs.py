@@ -87,6 +87,8 @@ STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend"
 FGS_TUNE_TILE_SORT_CAP = 0
 FGS_TUNE_BLEND_CULL = 2
 FGS_TUNE_AGG_TILES = 3
+FGS_TUNE_RADIX = 4
+FGS_TUNE_RADIX_MIN_LIST = 5
 
 
 def lib():

@@ -100,6 +100,11 @@ def test_tuning_knob_host_only(L):
     assert L.fgs_set_tuning(fgs.FGS_TUNE_AGG_TILES, 0) == fgs.FGS_E_INVALID
     assert L.fgs_set_tuning(fgs.FGS_TUNE_AGG_TILES, 4097) == fgs.FGS_E_INVALID
     assert L.fgs_set_tuning(1, 0) == fgs.FGS_E_INVALID          # retired key (single deform kernel)
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_RADIX) == 0 and fgs.fgs_get_tuning(fgs.FGS_TUNE_RADIX_MIN_LIST) == 768
+    with fgs.tuning(fgs.FGS_TUNE_RADIX, 2):
+        assert fgs.fgs_get_tuning(fgs.FGS_TUNE_RADIX) == 2
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_RADIX, 3) == fgs.FGS_E_INVALID
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_RADIX_MIN_LIST, 0) == fgs.FGS_E_INVALID
 
 
 def test_stage_names_match_header():

@@ -205,6 +205,11 @@ def test_nan_and_degenerate_gaussians_are_culled():
 
 @pytest.mark.parametrize("cap", [1, 16, 100, 300, 700])
 def test_long_list_sort_path_matches(cap):
+    with fgs.tuning(fgs.FGS_TUNE_RADIX, 0):       # the per-tile sorts (the radix path is tested below)
+        _long_list_sort_path_matches(cap)
+
+
+def _long_list_sort_path_matches(cap):
     """Tile lists longer than the shared-memory sort cap go through long_sort_kernel (global-memory
     runs + merge-path merges): same lists, same image, bit for bit, as the in-smem bitonic path."""
     s = make_scene("tiny", width=70, height=50)
@@ -224,13 +229,14 @@ def test_long_list_sort_path_matches(cap):
         assert np.array_equal(out[k], base[k]), k
 
 
-@pytest.mark.parametrize("cap", [None, 100])
-def test_sort_exact_and_near_depth_ties(cap):
+@pytest.mark.parametrize("cap,radix", [(None, 0), (100, 0), (None, 2)])
+def test_sort_exact_and_near_depth_ties(cap, radix):
     """The tile sort's 32-bit prefix words (depth key relative to the list minimum, shifted right when
     the list's depth range does not fit beside the slot index): groups of Gaussians at bit-identical
     depths (exact ties, ordered by index) and Gaussians along view rays from depth 0.5 to 500 (wide
     ranges: shifted prefixes, near ties resolved on the full key) give the oracle's (tile, depth,
-    index) lists bit for bit, through the warp sorts and (cap 100) the long-list sort."""
+    index) lists bit for bit, through the warp sorts, (cap 100) the long-list sort and (radix 2) the radix
+    binning path (stable depth sort: exact ties keep index order)."""
     s = with_heads(make_scene("tiny", n=3000, width=64, height=64), 0.0)   # zero heads: means as given
     rng = np.random.default_rng(7)
     i = 0
@@ -248,7 +254,8 @@ def test_sort_exact_and_near_depth_ties(cap):
     if cap is not None:
         fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, cap)
     try:
-        out, ref, _, _ = _render_parity(s, check_tiles=True)
+        with fgs.tuning(fgs.FGS_TUNE_RADIX, radix):
+            out, ref, _, _ = _render_parity(s, check_tiles=True)
     finally:
         fgs.fgs_set_tuning(fgs.FGS_TUNE_TILE_SORT_CAP, old)
     tiles, gids = np.asarray(ref["tiles"]), np.asarray(ref["gids"])
@@ -260,11 +267,12 @@ def test_sort_exact_and_near_depth_ties(cap):
     assert spans.max() >= 1 << 25, "no list with a depth range wider than the prefix bits"
 
 
-@pytest.mark.parametrize("ties", [False, True])
-def test_long_lists_multi_run_merge(ties):
+@pytest.mark.parametrize("ties,radix", [(False, 0), (True, 0), (False, 2), (True, 2)])
+def test_long_lists_multi_run_merge(ties, radix):
     """A list longer than several 2048-entry runs (merge passes) sorted in global memory: many
     Gaussians piled on one tile (segments of 4096 on the 32-bit prefix-word CTA sort); with ties,
-    groups of bit-identical depths inside those segments (the word sort's tie fixup)."""
+    groups of bit-identical depths inside those segments (the word sort's tie fixup).  radix 2: the
+    same lists through the radix binning path."""
     s = make_scene("tiny", n=9000, width=32, height=32)
     if ties:
         s = with_heads(s, 0.0)
@@ -273,7 +281,8 @@ def test_long_lists_multi_run_merge(ties):
             s.means[100 * k:100 * k + 2 + k] = s.means[rng.integers(6100, s.n)]
     ds = _ds(s)
     dstruct, g, _ = gpu_deform(ds, float(s.times[0]))
-    out = gpu_render_debug(ds, s.cameras[0], dstruct)
+    with fgs.tuning(fgs.FGS_TUNE_RADIX, radix):
+        out = gpu_render_debug(ds, s.cameras[0], dstruct)
     assert np.diff(out["ranges"], axis=1).max() > 4096
     ref = OR.render_ref(g, s.opacity_logits, s.sh, s.sh_degree, s.cameras[0])
     ints = compare_integer_work(out, ref["pre"], (ref["tiles"], ref["gids"], ref["ranges"]))
@@ -754,7 +763,7 @@ def test_frames_host_concurrent_threads():
             assert torch.equal(a, b), k
 
 
-@pytest.mark.parametrize("mode", ["default", "long_sort_direct_atomics_unculled"])
+@pytest.mark.parametrize("mode", ["default", "long_sort_direct_atomics_unculled", "radix"])
 def test_repeated_runs_bit_identical(mode):
     """Race stand-in (compute-sanitizer is closed on the GPU pool): 12 back-to-back fgs_frames calls of
     the full metric batch (D: 100k Gaussians, 20 frames of 800x800) must give bit-identical images.  The
@@ -771,10 +780,13 @@ def test_repeated_runs_bit_identical(mode):
     imgs = [torch.empty((3, 800, 800), device="cuda") for _ in range(F)]
     ws = ds.alloc_workspace(F)
     ctx = contextlib.ExitStack()
-    if mode != "default":
+    if mode == "long_sort_direct_atomics_unculled":
+        ctx.enter_context(fgs.tuning(fgs.FGS_TUNE_RADIX, 0))
         ctx.enter_context(fgs.tuning(fgs.FGS_TUNE_TILE_SORT_CAP, 32))
         ctx.enter_context(fgs.tuning(fgs.FGS_TUNE_AGG_TILES, 1))
         ctx.enter_context(fgs.tuning(fgs.FGS_TUNE_BLEND_CULL, 0))
+    elif mode == "radix":
+        ctx.enter_context(fgs.tuning(fgs.FGS_TUNE_RADIX, 2))
     with ctx:
         ref = None
         for it in range(12):
@@ -789,3 +801,46 @@ def test_repeated_runs_bit_identical(mode):
     if mode != "default":
         fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, imgs, ws)
         assert torch.equal(torch.stack(imgs), ref)
+
+
+@pytest.mark.parametrize("name,n,W,H,frames", [("tiny", 2011, 70, 50, 1), ("dnerf", 30_000, 200, 136, 3),
+                                                ("hypernerf", 40_000, 240, 136, 2), ("neu3d", 20_000, 338, 254, 2)])
+def test_radix_path_bit_identical_to_tile_sorts(name, n, W, H, frames):
+    """The radix binning path (FGS_TUNE_RADIX = 2: stable LSD depth sort of the Gaussians, emission in
+    depth order, stable tile passes) gives exactly the per-tile sorts' lists, ranges and images, through
+    fgs_frames batches (several frames per launch, ragged tile grids), and the oracle's lists."""
+    import torch
+    s = make_scene(name, n=n, width=W, height=H, n_frames=frames)
+    ds = _ds(s)
+    outs, _ = ds.alloc_deformed(frames)
+    res = {}
+    for mode in (0, 2):
+        imgs = [torch.empty((3, H, W), device="cuda") for _ in range(frames)]
+        ws = ds.alloc_workspace(frames)
+        with fgs.tuning(fgs.FGS_TUNE_RADIX, mode):
+            fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs, imgs, ws)
+            fgs.fgs_render_status(ws, frames)
+            dbg = gpu_render_debug(ds, s.cameras[0], outs[0])
+        res[mode] = ([im.cpu().numpy() for im in imgs], dbg)
+    for a, b in zip(res[0][0], res[2][0]):
+        assert np.array_equal(a, b)
+    for k in ("sorted_gid", "sorted_tile", "ranges", "image", "n_contrib"):
+        assert np.array_equal(res[0][1][k], res[2][1][k]), k
+    if n <= 2011:
+        _render_parity(s)
+
+
+def test_radix_auto_selection_and_threshold():
+    """Auto mode (FGS_TUNE_RADIX = 1) takes the radix path on long-list frames only (n >= 64 x tiles and
+    mean list >= the threshold); the result is identical for every threshold and to the default path."""
+    import torch
+    s = make_scene("dnerf", n=40_000, width=160, height=128, n_frames=2)      # 80 tiles: lists ~3000
+    ds = _ds(s)
+    dstruct, _, _ = gpu_deform(ds, float(s.times[0]))
+    outs = [gpu_render_debug(ds, s.cameras[0], dstruct)]
+    for thr in (1, 768, 1 << 20):
+        with fgs.tuning(fgs.FGS_TUNE_RADIX, 1), fgs.tuning(fgs.FGS_TUNE_RADIX_MIN_LIST, thr):
+            outs.append(gpu_render_debug(ds, s.cameras[0], dstruct))
+    for o in outs[1:]:
+        for k in ("sorted_gid", "ranges", "image"):
+            assert np.array_equal(o[k], outs[0][k]), k
