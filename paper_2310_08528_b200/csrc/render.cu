@@ -645,7 +645,6 @@ __global__ void __launch_bounds__(32 * kTileSortWarps) tile_sort_kernel(const __
 // all 256 threads, ping-ponging between two shared buffers.  Longer lists: segments of kCtaSortMax
 // sorted that way in place, then merge-path levels in global memory through the inst2 scratch.
 constexpr int kCtaSortMax = 4096;
-constexpr int kCtaWordsMin = 3072;   // segments longer than this sort on 32-bit prefix words (cta_sort_words)
 constexpr size_t kLongSortSmem = 2 * kCtaSortMax * sizeof(unsigned long long);   // 64 KB dynamic
 
 template <typename K>
@@ -670,22 +669,98 @@ __device__ __forceinline__ void block_merge(const K* a, int na, const K* bq, int
   }
 }
 
+// CTA-wide bitonic network over the NT R words of the CTA in the blocked layout (word e = R t + r in
+// register r of thread t), ascending: thread-local stages for partner distances j < R, warp shuffles for
+// partner threads in the same warp (j / R < 32), a shared-memory exchange (transposed: conflict-free) for
+// partners in other warps.  The CTA analogue of warp_sort_words.
+template <int R>
+__device__ __forceinline__ void cta_bitonic_words(uint32_t (&v)[R], uint32_t* xbuf) {
+  constexpr int NT = kLargeSortThreads;
+  constexpr int N2 = NT * R;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 2; k < R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & j) == 0) cmp_swap(v[r], v[r | j], (r & k) == 0);
+    }
+  }
+#pragma unroll 1
+  for (int k = R; k <= N2; k <<= 1) {
+    if (k < 2) continue;
+    const bool up = ((R * t) & k) == 0;
+#pragma unroll 1
+    for (int j = k >> 1; j >= R; j >>= 1) {
+      const int jt = j / R;                          // partner thread distance
+      const bool keep_min = ((t & jt) == 0) == up;
+      if (jt < 32) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], jt);
+          v[r] = ((v[r] < o) == keep_min) ? v[r] : o;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) xbuf[r * NT + t] = v[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t o = xbuf[r * NT + (t ^ jt)];
+          v[r] = ((v[r] < o) == keep_min) ? v[r] : o;
+        }
+        __syncthreads();
+      }
+    }
+#pragma unroll
+    for (int j = R >> 1; j > 0; j >>= 1) {
+      if (j < k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if ((r & j) == 0) cmp_swap(v[r], v[r | j], up);
+      }
+    }
+  }
+}
+
+// words[0..L) (smem) sorted ascending in place by one CTA bitonic network of the smallest power of two
+// >= L (pads 0xFFFFFFFF sort last)
+template <int R>
+__device__ __forceinline__ void cta_sort_words_bitonic(uint32_t* words, int L, uint32_t* xbuf) {
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * threadIdx.x + r;
+    v[r] = e < L ? words[e] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  cta_bitonic_words<R>(v, xbuf);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = R * threadIdx.x + r;
+    if (e < L) words[e] = v[r];
+  }
+  __syncthreads();
+}
+
 // Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA, on 32-bit
 // words as the warp sorts: prefix of the depth key relative to the segment minimum (shifted right by
-// the range bits that do not fit beside 12 slot bits) | slot.  Register runs of 256 by the warps,
-// merge-path levels over all threads on the words in shared memory (unique words: exact splits), then
+// the range bits that do not fit beside 12 slot bits) | slot.  One CTA bitonic network (registers,
+// shuffles, shared-memory exchanges) over the next power of two of L words — round 2: replaced warp runs
+// + merge-path levels (N = 1M tile sort 171 -> 154, 3M 748 -> 674 us per frame, unchanged below) — then
 // each word's slot fetches its instance and neighbours of equal prefix are put in (depth key, gid)
 // order by an odd-even transposition (skipped by a vote when there are none).  sm: kLongSortSmem.
 __device__ void cta_sort_words(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sm) {
   static_assert(kCtaSortMax == 4096, "12 slot bits");
   constexpr int SB = 12;
-  constexpr int NT = kLargeSortThreads, NW = NT / 32;
+  constexpr int NT = kLargeSortThreads;
   uint32_t* wA = reinterpret_cast<uint32_t*>(sm);
   uint32_t* wB = wA + kCtaSortMax;
   FGS_DCHECK(L >= 1 && L <= kCtaSortMax);
   unsigned long long* stage = sm + kCtaSortMax;
   __shared__ uint32_t s_mn, s_mx;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   uint32_t mn = 0xFFFFFFFFu, mx = 0u;
   for (int q = threadIdx.x; q < L; q += NT) {
     const uint32_t h = (uint32_t)(src[q] >> 32);
@@ -701,32 +776,13 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   mn = s_mn;
   mx = s_mx;
   const int s = max(0, (32 - __clz(mx - mn)) - (32 - SB));
-  for (int r0 = warp * 256; r0 < L; r0 += NW * 256) {
-    const int l = min(256, L - r0);
-    uint32_t v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = 8 * lane + r;
-      v[r] = e < l ? (((((uint32_t)(src[r0 + e] >> 32)) - mn) >> s) << SB) | (uint32_t)(r0 + e) : 0xFFFFFFFFu;
-    }
-    warp_sort_words<8>(v, lane);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = 8 * lane + r;
-      if (e < l) wA[r0 + e] = v[r];
-    }
-  }
+  for (int q = threadIdx.x; q < L; q += NT)
+    wA[q] = (((((uint32_t)(src[q] >> 32)) - mn) >> s) << SB) | (uint32_t)q;
   __syncthreads();
-  uint32_t* A = wA;
-  uint32_t* B = wB;
-  for (int w = 256; w < L; w <<= 1) {
-    for (int s0 = 0; s0 < L; s0 += 2 * w) {
-      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
-      block_merge<uint32_t>(A + s0, na, A + s0 + na, nb, B + s0, threadIdx.x, NT);
-    }
-    __syncthreads();
-    uint32_t* t = A; A = B; B = t;
-  }
+  if (L <= 1024) cta_sort_words_bitonic<4>(wA, L, wB);
+  else if (L <= 2048) cta_sort_words_bitonic<8>(wA, L, wB);
+  else cta_sort_words_bitonic<16>(wA, L, wB);
+  const uint32_t* A = wA;
   bool tie = false;
   for (int q = threadIdx.x; q < L; q += NT) {
     FGS_DCHECK((int)(A[q] & ((1u << SB) - 1u)) < L);
@@ -754,34 +810,6 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   __syncthreads();
 }
 
-// Sorts src[0..L) (L <= kCtaSortMax) into dst[0..L) (may alias src) with the whole CTA on the 64-bit
-// instances (segments up to kCtaWordsMin: the word path's range pass and staging cost more there).
-__device__ void cta_sort_keys(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sA,
-                         unsigned long long* sB) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NW = kLargeSortThreads / 32;
-  FGS_DCHECK(L >= 1 && L <= kCtaSortMax);
-  for (int r0 = warp * 256; r0 < L; r0 += NW * 256)
-    warp_sort_upto256(src + r0, sA + r0, min(256, L - r0), lane);
-  __syncthreads();
-  unsigned long long* A = sA;
-  unsigned long long* B = sB;
-  for (int w = 256; w < L; w <<= 1) {
-    const bool last = 2 * w >= L;
-    unsigned long long* out = last ? dst : B;
-    for (int s0 = 0; s0 < L; s0 += 2 * w) {
-      const int na = min(w, L - s0), nb = max(0, min(w, L - s0 - w));
-      block_merge<unsigned long long>(A + s0, na, A + s0 + na, nb, out + s0, threadIdx.x, kLargeSortThreads);
-    }
-    __syncthreads();
-    unsigned long long* t = A; A = B; B = t;
-  }
-  if (L <= 256) {   // a single run: copy it out
-    for (int q = threadIdx.x; q < L; q += kLargeSortThreads) dst[q] = sA[q];
-    __syncthreads();
-  }
-}
-
 __device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned long long* sm) {
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, f, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
@@ -789,8 +817,7 @@ __device__ void long_sort_one(const RenderBatch& b, int f, int tile, unsigned lo
   unsigned long long* B = ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.inst2) + rg.x;
   for (int c0 = 0; c0 < L; c0 += kCtaSortMax) {
     const int l = min(kCtaSortMax, L - c0);
-    if (l > kCtaWordsMin) cta_sort_words(A + c0, A + c0, l, sm);
-    else cta_sort_keys(A + c0, A + c0, l, sm, sm + kCtaSortMax);
+    cta_sort_words(A + c0, A + c0, l, sm);
   }
   if (L > kCtaSortMax && L <= 2 * kCtaSortMax) {
     // two sorted segments: both back into shared memory and one merge-path merge straight into the
