@@ -749,8 +749,8 @@ __device__ __forceinline__ void cta_sort_words_bitonic(uint32_t* words, int L, u
 // the range bits that do not fit beside 12 slot bits) | slot.  One CTA bitonic network (registers,
 // shuffles, shared-memory exchanges) over the next power of two of L words — round 2: replaced warp runs
 // + merge-path levels (N = 1M tile sort 171 -> 154, 3M 748 -> 674 us per frame, unchanged below) — then
-// each word's slot fetches its instance and neighbours of equal prefix are put in (depth key, gid)
-// order by an odd-even transposition (skipped by a vote when there are none).  sm: kLongSortSmem.
+// neighbours of equal prefix are put in (depth key, gid) order and each word's slot fetches its
+// instance for the output.  The segment is read from global memory once.  sm: kLongSortSmem.
 __device__ void cta_sort_words(const unsigned long long* src, unsigned long long* dst, int L, unsigned long long* sm) {
   static_assert(kCtaSortMax == 4096, "12 slot bits");
   constexpr int SB = 12;
@@ -761,9 +761,12 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   unsigned long long* stage = sm + kCtaSortMax;
   __shared__ uint32_t s_mn, s_mx;
   const int lane = threadIdx.x & 31;
+  // the segment is read from global memory ONCE, into the stage; everything after works in shared memory
   uint32_t mn = 0xFFFFFFFFu, mx = 0u;
   for (int q = threadIdx.x; q < L; q += NT) {
-    const uint32_t h = (uint32_t)(src[q] >> 32);
+    const unsigned long long x = src[q];
+    stage[q] = x;
+    const uint32_t h = (uint32_t)(x >> 32);
     mn = min(mn, h);
     mx = max(mx, h);
   }
@@ -777,27 +780,27 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
   mx = s_mx;
   const int s = max(0, (32 - __clz(mx - mn)) - (32 - SB));
   for (int q = threadIdx.x; q < L; q += NT)
-    wA[q] = (((((uint32_t)(src[q] >> 32)) - mn) >> s) << SB) | (uint32_t)q;
+    wA[q] = (((((uint32_t)(stage[q] >> 32)) - mn) >> s) << SB) | (uint32_t)q;
   __syncthreads();
   if (L <= 1024) cta_sort_words_bitonic<4>(wA, L, wB);
   else if (L <= 2048) cta_sort_words_bitonic<8>(wA, L, wB);
   else cta_sort_words_bitonic<16>(wA, L, wB);
-  const uint32_t* A = wA;
+  // neighbours of equal prefix (exact depth ties, or near ones when s > 0) put in (depth key, gid) order:
+  // an odd-even transposition on the WORDS comparing the instances their slots point to (skipped by a
+  // vote when there are none)
+  constexpr uint32_t kSlot = (1u << SB) - 1u;
   bool tie = false;
-  for (int q = threadIdx.x; q < L; q += NT) {
-    FGS_DCHECK((int)(A[q] & ((1u << SB) - 1u)) < L);
-    stage[q] = src[A[q] & ((1u << SB) - 1u)];
-    if (q + 1 < L && (A[q] >> SB) == (A[q + 1] >> SB)) tie = true;
-  }
+  for (int q = threadIdx.x; q + 1 < L; q += NT)
+    if ((wA[q] >> SB) == (wA[q + 1] >> SB)) tie = true;
   if (__syncthreads_or(tie)) {
     for (;;) {
       bool swapped = false;
       for (int ph = 0; ph < 2; ++ph) {
         for (int e = 2 * threadIdx.x + ph; e + 1 < L; e += 2 * NT) {
-          const unsigned long long x = stage[e], y = stage[e + 1];
-          if (((((uint32_t)(x >> 32)) - mn) >> s) == ((((uint32_t)(y >> 32)) - mn) >> s) && x > y) {
-            stage[e] = y;
-            stage[e + 1] = x;
+          const uint32_t x = wA[e], y = wA[e + 1];
+          if ((x >> SB) == (y >> SB) && stage[x & kSlot] > stage[y & kSlot]) {
+            wA[e] = y;
+            wA[e + 1] = x;
             swapped = true;
           }
         }
@@ -806,7 +809,10 @@ __device__ void cta_sort_words(const unsigned long long* src, unsigned long long
       if (!__syncthreads_or(swapped)) break;
     }
   }
-  for (int q = threadIdx.x; q < L; q += NT) dst[q] = stage[q];
+  for (int q = threadIdx.x; q < L; q += NT) {
+    FGS_DCHECK((int)(wA[q] & kSlot) < L);
+    dst[q] = stage[wA[q] & kSlot];
+  }
   __syncthreads();
 }
 
