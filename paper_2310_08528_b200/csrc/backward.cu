@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kBwdThreads) blend_backward_kernel(const __gri
   const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, 0, b.L.inst) + rg.x;
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, 0, b.L.rec);
   __shared__ float4 s_a[kBwdBatch], s_q[kBwdBatch];
-  __shared__ float s_c[kBwdBatch];
+  __shared__ float s_c[kBwdBatch], s_thr[kBwdBatch];
   __shared__ uint32_t s_gid[kBwdBatch];
   __shared__ float s_red[kBwdWarps][kBwdBatch][kNPart];
   // the forward's per-pixel arithmetic: dx = mean_rel.x - x, dy = (mean_rel.y - (y & 3)) - 4 (y >> 2)
@@ -183,11 +183,35 @@ __global__ void __launch_bounds__(kBwdThreads) blend_backward_kernel(const __gri
       s_a[threadIdx.x] = a;
       s_q[threadIdx.x] = rec[3 * g + 1];
       s_c[threadIdx.x] = c.x;
+      s_thr[threadIdx.x] = c.w;       // the forward's ellipse-cull threshold (preprocess record)
       s_gid[threadIdx.x] = g;
     }
+    // every (warp, Gaussian) row of the reduction buffer starts at zero: a warp writes only the rows of
+    // the Gaussians its cull keeps
+    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * kNPart; e += kBwdThreads) (&s_red[0][0][0])[e] = 0.f;
     __syncthreads();
     const int cnt = min(kBwdBatch, L - start);
-    for (int j = 0; j < cnt; ++j) {
+    // warp cull (the forward blend's conservative ellipse-vs-box bound, face_min): lane j tests Gaussian j
+    // against the warp's 16 x 2 pixel box; a Gaussian whose alpha < 1/255 on the whole box changes no
+    // pixel of it and gets no gradient from it, so skipping it is exact
+    uint32_t m = 0;
+    {
+      bool need = false;
+      if (lane < cnt) {
+        const float4 a = s_a[lane];
+        const float qa = -a.z, qb = -a.w, qc = -s_q[lane].x, thr = s_thr[lane];
+        const float xl = 0.f - a.x, xh = 15.f - a.x;
+        const float yl = (float)(2 * warp) - a.y, yh = yl + 1.f;
+        const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
+        const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+        need = face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr;
+      }
+      m = __ballot_sync(0xffffffffu, need);
+      if (!__any_sync(0xffffffffu, !done)) m = 0;
+    }
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
       float part[kNPart];
 #pragma unroll
       for (int k = 0; k < kNPart; ++k) part[k] = 0.f;
@@ -233,19 +257,36 @@ __global__ void __launch_bounds__(kBwdThreads) blend_backward_kernel(const __gri
         }
       }
       if (__any_sync(0xffffffffu, contrib)) {
+        // warp sums of the 9 partials, fixed order (deterministic): partials 0-7 by a transposing
+        // butterfly (each exchange step halves the values a lane keeps: 4 + 2 + 1 + 1 + 1 shuffles, lane l
+        // ends with the sum of partial ((l >> 2) & 7) in bit-reversed order), partial 8 by a plain one
+        float h4[4], h2[2], h1;
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-        for (int k = 0; k < kNPart; ++k) {
-          float v = part[k];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          part[k] = v;
+        for (int i = 0; i < 4; ++i) {
+          const float send = b4 ? part[i] : part[i + 4];
+          const float keep = b4 ? part[i + 4] : part[i];
+          h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
         }
-        if (lane == 0)
 #pragma unroll
-          for (int k = 0; k < kNPart; ++k) s_red[warp][j][k] = part[k];
-      } else if (lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+          const float send = b3 ? h4[i] : h4[i + 2];
+          const float keep = b3 ? h4[i + 2] : h4[i];
+          h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const float send = b2 ? h2[0] : h2[1];
+          const float keep = b2 ? h2[1] : h2[0];
+          h1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        float p8 = part[8];
 #pragma unroll
-        for (int k = 0; k < kNPart; ++k) s_red[warp][j][k] = 0.f;
+        for (int o = 16; o > 0; o >>= 1) p8 += __shfl_xor_sync(0xffffffffu, p8, o);
+        // lane l holds partial 4 b4 + 2 b3 + b2 (the halves kept at each step)
+        if ((lane & 3) == 0) s_red[warp][j][(b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0)] = h1;
+        if (lane == 0) s_red[warp][j][8] = p8;
       }
     }
     __syncthreads();
@@ -464,7 +505,9 @@ __global__ void __launch_bounds__(128) preprocess_backward_kernel(const __grid_c
 // keeps their f_h, dz, f_d and dOut rows in shared memory for the fixed-order MLP weight reduction.
 constexpr int kDbWarps = 8;
 constexpr int kDbThreads = 32 * kDbWarps;
-constexpr int kDbRows = 64;
+// rows (Gaussians) per CTA: 64, or 32 at W = 128 so that two CTAs' shared memory fits an SM
+template <int W>
+constexpr int db_rows() { return W >= 128 ? 32 : 64; }
 
 struct DefBwdArgs {
   DeformBatch p;                    // n_t = 1, t[0]
@@ -475,7 +518,8 @@ struct DefBwdArgs {
 };
 
 template <int W, int IN>
-__global__ void __launch_bounds__(kDbThreads) deform_backward_kernel(const __grid_constant__ DefBwdArgs A) {
+__global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __grid_constant__ DefBwdArgs A) {
+  constexpr int kDbRows = db_rows<W>();
   constexpr int KS = (IN + 31) / 32;       // feature slots per lane
   constexpr int WS = W / 32;               // hidden-unit slots per lane
   const DeformBatch& p = A.p;
@@ -641,25 +685,26 @@ __global__ void __launch_bounds__(kDbThreads) deform_backward_kernel(const __gri
   }
   __syncthreads();
   // ---- MLP weight gradients: the CTA's rows summed in row order, one fixed-point atomic each ----
+  // (fp32 over the CTA's <= 64 rows, in row order; the fixed-point sum over CTAs is exact)
   for (int e = tid; e < W * IN; e += kDbThreads) {
     const int cw = e / IN, k = e - cw * IN;
-    double sacc = 0.0;
-    for (int r = 0; r < nrow; ++r) sacc += (double)sDz[r * W + cw] * sFh[r * IN + k];
+    float sacc = 0.f;
+    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDz[r * W + cw], sFh[r * IN + k], sacc);
     fix_add(A.acc_wd + e, sacc);
   }
   for (int cw = tid; cw < W; cw += kDbThreads) {
-    double sacc = 0.0;
+    float sacc = 0.f;
     for (int r = 0; r < nrow; ++r) sacc += sDz[r * W + cw];
     fix_add(A.acc_bd + cw, sacc);
   }
   for (int e = tid; e < 10 * W; e += kDbThreads) {
     const int o = e / W, cw = e - o * W;
-    double sacc = 0.0;
-    for (int r = 0; r < nrow; ++r) sacc += (double)sDo[r * 10 + o] * sFd[r * W + cw];
+    float sacc = 0.f;
+    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDo[r * 10 + o], sFd[r * W + cw], sacc);
     fix_add(A.acc_wh + e, sacc);
   }
   if (tid < 10) {
-    double sacc = 0.0;
+    float sacc = 0.f;
     for (int r = 0; r < nrow; ++r) sacc += sDo[r * 10 + tid];
     fix_add(A.acc_bh + tid, sacc);
   }
@@ -724,7 +769,7 @@ size_t deform_backward_acc_elems(const DeformBatch& p) {
 
 template <int W, int IN>
 cudaError_t launch_def_bwd_t(const DefBwdArgs& A, unsigned grid, cudaStream_t s) {
-  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + 10 * W + (size_t)kDbRows * (IN + 2 * W + 10));
+  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + 10 * W + (size_t)db_rows<W>() * (IN + 2 * W + 10));
   cudaError_t e = cudaFuncSetAttribute(deform_backward_kernel<W, IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -753,7 +798,8 @@ cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const 
   A.acc_bd = acc + off; off += p.width;
   A.acc_wh = acc + off; off += 10 * (size_t)p.width;
   A.acc_bh = acc + off; off += 10;
-  const unsigned grid = (unsigned)((p.end - p.begin + kDbRows - 1) / kDbRows);
+  const int rows = p.width >= 128 ? db_rows<128>() : db_rows<64>();
+  const unsigned grid = (unsigned)((p.end - p.begin + rows - 1) / rows);
   if (grid > 0) {
 #define FGS_DB(WW, II) if (p.width == WW && p.in_dim == II) e = launch_def_bwd_t<WW, II>(A, grid, s); else
     FGS_DB(32, 16) FGS_DB(32, 32) FGS_DB(32, 64) FGS_DB(64, 16) FGS_DB(64, 32) FGS_DB(64, 64)

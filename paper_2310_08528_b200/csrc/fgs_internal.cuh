@@ -193,6 +193,27 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return d;
 }
 
+// Minimum of the PSD quadratic q2(d) = qa dx^2 + qb dx dy + qc dy^2 over one box [xl,xh] x [yl,yh] of
+// offsets d = pixel - mean (the blend's ellipse-vs-box cull, render.cu, and the backward's warp cull,
+// backward.cu), given the box's x-face candidate ex (xl if xl > 0, xh if xh < 0, else 0) and the
+// minimiser ratios kx = -qb / (2 qa), ky = -qb / (2 qc): at most one x-face and one y-face can hold the
+// minimum when the box excludes 0 (KKT); on each the 1-D minimiser is clamped to the face.
+__device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx, float ky, float ex, float xl,
+                                          float xh, float yl, float yh) {
+  const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
+  float q = 0.f;
+  if (ex != 0.f) {
+    const float yy = fminf(fmaxf(ky * ex, yl), yh);
+    q = fmaf(fmaf(qa, ex, qb * yy), ex, qc * yy * yy);
+  }
+  if (ey != 0.f) {
+    const float xx = fminf(fmaxf(kx * ey, xl), xh);
+    const float q2 = fmaf(fmaf(qc, ey, qb * xx), ey, qa * xx * xx);
+    q = ex != 0.f ? fminf(q, q2) : q2;
+  }
+  return q;
+}
+
 template <typename T>
 __host__ __device__ inline T* ws_ptr(char* base, size_t stride, int f, size_t off) {
   return reinterpret_cast<T*>(base + (size_t)f * stride + off);

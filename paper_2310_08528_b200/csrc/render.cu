@@ -927,24 +927,7 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
 // face whose half-space excludes 0 (KKT), so at most one x-face and one y-face are candidates; on
 // each the 1-D minimiser is clamped to the face.  An inexact minimiser only raises the computed value
 // by qc delta^2 (quadratic in its error), far inside thr's margin.
-// Minimum of q2 over one box [xl,xh] x [yl,yh] given the shared x-face candidate ex and the minimiser
-// ratios (x* = kx ey on a y-face, y* = ky ex on an x-face).
-__device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx, float ky, float ex, float xl,
-                                          float xh, float yl, float yh) {
-  const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
-  float q = 0.f;
-  if (ex != 0.f) {
-    const float yy = fminf(fmaxf(ky * ex, yl), yh);
-    q = fmaf(fmaf(qa, ex, qb * yy), ex, qc * yy * yy);
-  }
-  if (ey != 0.f) {
-    const float xx = fminf(fmaxf(kx * ey, xl), xh);
-    const float q2 = fmaf(fmaf(qc, ey, qb * xx), ey, qa * xx * xx);
-    q = ex != 0.f ? fminf(q, q2) : q2;
-  }
-  return q;
-}
-
+// face_min (fgs_internal.cuh): the minimum of q2 over one box, shared with the backward's warp cull.
 
 // NP pixels per lane: warp w of the tile's NW = 64/NP... warps owns a column block; lane l owns pixel
 // (x, y + 4k), k < NP, of that block (x = l & 7, y = l >> 3).  Sub-box k = rows [4k, 4k+4) of the block.
