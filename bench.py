@@ -808,6 +808,164 @@ def run_shard(args, scene, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, scene, rank, world, local_rank):
+    """SURVEY §8(f) rank 4 (§4.3): the training side measured.  A step = every frame of
+    the config's batch trained once: fgs_deform at its t, fgs_render, fgs_l1_loss against a synthetic
+    target, fgs_render_backward, fgs_deform_backward (field gradients accumulated over the batch), plus
+    one fgs_tv_loss.  Replayed from a CUDA graph; per-stage times from a separate eager pass.  The
+    autograd oracle (oracle/backward.py) is timed beside it on a bounded sample (cpu_baseline)."""
+    import numpy as np
+    import torch
+
+    from paper_2310_08528_b200 import build, fgs
+
+    build.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ds = fgs.DeviceScene(scene, dev)
+    F = scene.n_frames
+    W, H = scene.cameras[0].width, scene.cameras[0].height
+    outs, _ = ds.alloc_deformed(1)
+    img = torch.empty((3, H, W), device=dev)
+    dimg = torch.empty_like(img)
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    targets = [torch.rand((3, H, W), generator=gen).to(dev) for _ in range(F)]
+    ws = ds.alloc_workspace(1, 16 * scene.n)
+    part = torch.empty(fgs.FGS_LOSS_PARTIALS, dtype=torch.float64, device=dev)
+    l1 = torch.empty(1, device=dev)
+    tv = torch.empty(1, device=dev)
+    dg, _ = ds.alloc_gaussian_grads()
+    dc, _ = ds.alloc_gaussian_grads()
+    df, _ = ds.alloc_field_grads()
+    rs = torch.empty(fgs.fgs_render_backward_scratch_bytes(scene.n), dtype=torch.uint8, device=dev)
+    dsb = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device=dev)
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    stage_names = ("deform", "render", "l1_loss", "render_backward", "deform_backward", "tv_loss")
+
+    def frame_calls(f):
+        t = ds.times[f]
+        return (lambda: fgs.fgs_deform(ds.g, ds.field, ds.mlp, t, outs[0]),
+                lambda: fgs.fgs_render(ds.cams[f], outs[0], img, ws),
+                lambda: fgs.fgs_l1_loss(img, targets[f], dimg, part, l1),
+                lambda: fgs.fgs_render_backward(ds.cams[f], outs[0], img, dimg, ws, rs, dg),
+                lambda: fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dg, dc, df, dsb))
+
+    def step():
+        for f in range(F):
+            for c in frame_calls(f):
+                c()
+        fgs.fgs_tv_loss(ds.field, 0.01, df, part, tv)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # per-stage times (eager, events around each call)
+    ms = {k: 0.0 for k in stage_names}
+    for f in range(F):
+        for name, c in zip(stage_names, frame_calls(f)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            c()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms[name] += a.elapsed_time(b)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    fgs.fgs_tv_loss(ds.field, 0.01, df, part, tv)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms["tv_loss"] = a.elapsed_time(b)
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        step()
+        side.synchronize()
+        l0 = fgs.fgs_launch_count()
+        with torch.cuda.graph(graph, stream=side):
+            step()
+        launches_per_step = fgs.fgs_launch_count() - l0
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        graph.replay()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t_ms = sum(x.elapsed_time(y) for x, y in evs)
+    fgs.fgs_render_status(ws, 1)
+    line = {
+        "metric": "training frames/s (deform + render + L1/TV loss + backward) at 800x800, 100k Gaussians",
+        "value": F * args.steps / (t_ms / 1e3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (random target images)", "mode": "train",
+        "config": {"workload": workload_desc(scene), "frames_per_step": F,
+                   "l2": "flushed between steps (512 MiB write outside the events)",
+                   "timed": "CUDA-graph replay of one training step", "tv_weight": 0.01},
+        "stages_ms_per_frame": {k: v / (F if k != "tv_loss" else 1) for k, v in ms.items()},
+        "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        # the autograd oracle on a bounded sample of one frame: the splat backward of 8 random tiles (with
+        # their Gaussians) and the deformation backward of 2000 Gaussians, scaled to the whole frame
+        from threadpoolctl import threadpool_limits
+
+        import oracle
+        from oracle import backward as OB
+        from oracle import render as OR
+        cam = scene.cameras[0]
+        t = float(scene.times[0])
+        G = oracle.deform_ref(scene, t)
+        pre = OR.preprocess_ref(G["means"], G["log_scales"], G["quats"], scene.opacity_logits, scene.sh,
+                                scene.sh_degree, cam)
+        gx, gy = OR.tile_grid(W, H)
+        rng = np.random.default_rng(0)
+        tiles = rng.choice(gx * gy, 8, replace=False)
+        sel = np.unique(np.concatenate([OR.tile_list_ref(pre, cam, int(tl)) for tl in tiles]))
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            sub = {k: v[sel] for k, v in G.items()}
+            OB.render_grads_ref(sub, scene.opacity_logits[sel], scene.sh[sel], scene.sh_degree, cam,
+                                np.random.default_rng(1).normal(size=(3, H, W)))
+            t_r = time.perf_counter() - t0
+            nd = 2000
+            sc = dataclasses_replace_rows(scene, nd)
+            t0 = time.perf_counter()
+            OB.deform_grads_ref(sc, t, {k: np.ones_like(v[:nd]) for k, v in G.items()})
+            t_d = (time.perf_counter() - t0) * scene.n / nd
+        # the render sample covers every tile (all pixels, the sample's Gaussians): scale by the share of
+        # list entries those 8 tiles hold
+        lens = np.array([len(OR.tile_list_ref(pre, cam, int(tl))) for tl in tiles])
+        bins = OR.bin_ref(pre, cam)[2]
+        share = lens.sum() / max(1, int(np.diff(bins, axis=1).sum()))
+        frame_s = t_r / max(share, 1e-9) + t_d
+        line["cpu_baseline"] = {"value": 1.0 / frame_s, "unit": "training frames/s", "cores": 1, "kind": "oracle",
+                                "extrapolated": True,
+                                "sample": (f"1 process: autograd splat backward of the {sel.size} Gaussians of 8 random "
+                                           f"tiles over the whole image (scaled by those tiles' {share:.4f} share of "
+                                           f"the list entries) + deformation backward of {nd}/{scene.n} Gaussians "
+                                           f"(scaled); fp64 PyTorch CPU autograd"),
+                                "cpu_model": cpu_model()}
+    print(json.dumps(line), flush=True)
+
+
+def dataclasses_replace_rows(scene, n):
+    import dataclasses
+    return dataclasses.replace(scene, means=scene.means[:n], log_scales=scene.log_scales[:n],
+                               quats=scene.quats[:n], opacity_logits=scene.opacity_logits[:n], sh=scene.sh[:n])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -830,9 +988,10 @@ def main():
                     help="frames mode under torchrun: every rank renders its own copy of the whole batch (weak "
                          "scaling) instead of its frame_split chunk of it (strong scaling, the default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="frames", choices=["frames", "shard"],
-                    help="frames: every rank renders its own frame batch (e1); shard: multi-view batch, views "
-                         "split across ranks, deformation sharded by Gaussian + NCCL all-gather (e2)")
+    ap.add_argument("--mode", default="frames", choices=["frames", "shard", "train"],
+                    help="frames: the frame batch split across ranks (e1); shard: multi-view batch, views "
+                         "split across ranks, deformation sharded by Gaussian + NCCL all-gather (e2); train: "
+                         "the training side (forward + L1/TV loss + backward, SURVEY 8(f) rank 4)")
     ap.add_argument("--fused", action="store_true",
                     help="with --mode shard: the deform epilogue stores every rank's copy into symmetric "
                          "memory (fgs_deform_range_peers) instead of the NCCL all-gather (SURVEY 8(e2) fused)")
@@ -861,6 +1020,8 @@ def main():
     try:
         if args.mode == "shard":
             run_shard(args, scene, rank, world, local_rank)
+        elif args.mode == "train":
+            run_train(args, scene, rank, world, local_rank)
         else:
             run_fgs(args, scene, rank, world, local_rank)
     finally:
