@@ -54,6 +54,13 @@ if d:
     if cb:
         out.append(f"* oracle (fp64 numpy, {cb.get('cores')} host processes, bounded sample): {cb.get('value'):.3g} "
                    f"{cb.get('unit')} — {cb.get('sample', '')}")
+    pa = d.get("parity") or {}
+    if pa:
+        out.append(f"* whole-frame parity vs the oracle (frame {pa['frame']}, every Gaussian and every pixel): deform max "
+                   f"|err| {pa['deform_max_abs_err']:.3g} (tol 1e-4); integer mismatches {pa['integer_mismatches']} "
+                   f"outside {pa['boundary_gaussians']} boundary Gaussians; PSNR {pa['psnr_db']:.1f} dB; max |err| on "
+                   f"unflagged pixels {pa['max_abs_err_unflagged']:.3g} (tol 2e-3); {pa['flagged_pixels']} flagged of "
+                   f"{pa['pixels']} pixels; pass = {pa['pass']}")
     out.append(f"* clocks during the timed region: {d.get('clocks')}; launches per step "
                f"{d.get('gpu_launches_per_step')}")
     r = d.get("roofline") or {}
@@ -102,6 +109,28 @@ dr = line(f"{G}/{TAG}_reference.log")
 if dr:
     out.append(f"* reference arm (`bench.py --impl reference`: the fp64 oracle on {dr.get('cpu_baseline', {}).get('cores')} "
                f"host processes): {dr['value']:.3g} frames/s")
+
+tr = [x for x in (line(f"{G}/{TAG}_train.log"), line(f"{G}/{TAG}_train_neu3d.log")) if x]
+if tr:
+    out += ["", "## Training side (SURVEY 8(f) rank 4: `bench.py --mode train`)", "",
+            "| config | training frames/s | deform / render / L1 / render backward / deform backward / TV (ms per frame) |",
+            "|---|---|---|"]
+    for d4 in tr:
+        st = d4.get("stages_ms_per_frame", {})
+        out.append(f"| {d4['config']['workload'].split(':')[0]} | {d4['value']:.0f} | "
+                   + " / ".join(f"{st.get(k, 0):.3f}" for k in ("deform", "render", "l1_loss", "render_backward",
+                                                                  "deform_backward", "tv_loss")) + " |")
+    cb4 = tr[0].get("cpu_baseline")
+    if cb4:
+        out.append(f"\nAutograd oracle (extrapolated from a bounded sample): {cb4['value']:.3g} {cb4['unit']} — {cb4['sample']}")
+try:
+    br = json.load(open(f"{G}/{TAG}_bwd_report.json"))
+    errs = br["errors"]["grad_rel_err"]
+    out.append(f"\nGradient parity (GPU chain vs the autograd oracle, one frame of a 60-Gaussian 40x32 scene, max |diff| / "
+               f"max |ref| per tensor): worst {max(errs.values()):.2g} ({max(errs, key=errs.get)}), loss rel. err "
+               f"{br['errors']['loss_rel_err']:.2g}")
+except (OSError, KeyError, ValueError):
+    pass
 
 sw = []
 try:
