@@ -216,3 +216,83 @@ def test_backward_deterministic_full_size():
             assert np.all(np.isfinite(x[k])), k
             assert np.array_equal(x[k], y[k]), k
     assert np.abs(a[1]["means"]).max() > 0 and np.abs(a[2]["w_d"]).max() > 0
+
+
+def test_backward_edge_cases():
+    """Degenerate inputs of the training side: an empty set (calls succeed, nothing written), Gaussians
+    behind the camera / culled (zero splat gradients), opaque Gaussians whose alpha clamps at 0.99 (the
+    oracle's clamp branch: zero dalpha/de), and t at both ends of [0, 1] for the deformation backward."""
+    import torch
+
+    from oracle import backward as B
+    # empty set
+    s0 = _scene(n=1)
+    ds0 = fgs.DeviceScene(dataclasses.replace(s0, means=s0.means[:0], log_scales=s0.log_scales[:0],
+                                              quats=s0.quats[:0], opacity_logits=s0.opacity_logits[:0],
+                                              sh=s0.sh[:0]))
+    d, tens, img, ws = _forward(ds0, ds0.scene, 0)
+    dg, _ = ds0.alloc_gaussian_grads()
+    rs = torch.empty(fgs.fgs_render_backward_scratch_bytes(0), dtype=torch.uint8, device="cuda")
+    fgs.fgs_render_backward(ds0.cams[0], d, img, torch.zeros_like(img), ws, rs, dg)
+    # culled + clamped
+    s = _scene(n=40, seed=5)
+    cam0 = s.cameras[0]
+    R0, t0 = cam0.R.astype(np.float64), cam0.t.astype(np.float64)
+    campos = -R0.T @ t0
+    s.means[:4] = (campos - 1.0 * R0[2]).astype(np.float32)   # 1 unit behind the camera: culled
+    s.opacity_logits[4:12] = 12.0                          # opaque: alpha clamps at 0.99 near their centres
+    ds = fgs.DeviceScene(s)
+    d, tens, img, ws = _forward(ds, s, 0)
+    cam = s.cameras[0]
+    w = np.random.default_rng(3).normal(size=(3, cam.height, cam.width)).astype(np.float32)
+    dg, gt = ds.alloc_gaussian_grads()
+    rs = torch.empty(fgs.fgs_render_backward_scratch_bytes(s.n), dtype=torch.uint8, device="cuda")
+    fgs.fgs_render_backward(ds.cams[0], d, img, torch.from_numpy(w).cuda(), ws, rs, dg)
+    torch.cuda.synchronize()
+    G = {k: v.cpu().numpy() for k, v in tens.items()}
+    ref, _ = B.render_grads_ref(G, s.opacity_logits, s.sh, s.sh_degree, cam, w)
+    for k in ("means", "log_scales", "quats", "opacity_logits", "sh"):
+        g = gt[k].cpu().numpy()
+        assert np.all(g[:4] == 0), k
+        assert _rel(g, ref[k]) <= TOL, (k, _rel(g, ref[k]))
+    # deformation backward at t = 0 and t = 1
+    rng = np.random.default_rng(4)
+    for t in (0.0, 1.0):
+        up = {"means": rng.normal(size=(s.n, 3)).astype(np.float32), "log_scales": rng.normal(size=(s.n, 3)).astype(np.float32),
+              "quats": rng.normal(size=(s.n, 4)).astype(np.float32)}
+        dd, dt = ds.alloc_gaussian_grads()
+        for k, v in up.items():
+            dt[k].copy_(torch.from_numpy(v))
+        dc, ct = ds.alloc_gaussian_grads()
+        df, ft = ds.alloc_field_grads()
+        sb = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device="cuda")
+        fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dd, dc, df, sb)
+        torch.cuda.synchronize()
+        ref = B.deform_grads_ref(s, t, up)
+        for k, v in list(ft.items()) + [(k, ct[k]) for k in ("means", "log_scales", "quats")]:
+            assert _rel(v.cpu().numpy(), ref[k]) <= TOL, (t, k)
+
+
+def test_backward_rejects_bad_arguments():
+    """Synchronous validation (FGS_E_INVALID) of the training-side calls, and FGS_E_NOTIMPL for the
+    backward of the P:1232 colour / opacity decoders."""
+    import torch
+
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = _scene(n=20)
+    ds = fgs.DeviceScene(s)
+    d, tens, img, ws = _forward(ds, s, 0)
+    dg, _ = ds.alloc_gaussian_grads()
+    small = torch.empty(8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(fgs.FgsError) as e:
+        fgs.fgs_render_backward(ds.cams[0], d, img, img, ws, small, dg)
+    assert e.value.code == fgs.FGS_E_INVALID
+    with pytest.raises(fgs.FgsError) as e:
+        fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, 1.5, dg, dg, ds.alloc_field_grads()[0], small)
+    assert e.value.code == fgs.FGS_E_INVALID
+    sc = with_colour_heads(s, 0.1, 0.1)
+    dsc = fgs.DeviceScene(sc)
+    big = torch.empty(fgs.fgs_deform_backward_scratch_bytes(dsc.field, dsc.mlp), dtype=torch.uint8, device="cuda")
+    with pytest.raises(fgs.FgsError) as e:
+        fgs.fgs_deform_backward(dsc.g, dsc.field, dsc.mlp, 0.5, dg, dg, dsc.alloc_field_grads()[0], big)
+    assert e.value.code == fgs.FGS_E_NOTIMPL

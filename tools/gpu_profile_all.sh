@@ -12,4 +12,8 @@ for KS in blend_kernel:2 deform_tc3_kernel:2 preprocess_kernel:2 tile_sort_kerne
      -o gpurun_out/${TAG}_${K} -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
      > gpurun_out/${TAG}_${K}_ncu.log 2>&1
   echo "$K rc=$?"
+  # reports are tens of MB (gpurun brings back <= 64 MiB): keep their text summaries
+  python tools/ncu_summary.py gpurun_out/${TAG}_${K}.ncu-rep > gpurun_out/${TAG}_${K}.summary.txt 2>&1
+  python tools/ncu_lines.py gpurun_out/${TAG}_${K}.ncu-rep 30 > gpurun_out/${TAG}_${K}.lines.txt 2>&1
+  [ "${KEEP_REPS:-0}" = "1" ] || rm -f gpurun_out/${TAG}_${K}.ncu-rep
 done

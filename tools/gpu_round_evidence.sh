@@ -14,3 +14,6 @@ timeout 600 python tools/backward_report.py > gpurun_out/${TAG}_bwd_report.json 
 python tools/bwd_one.py dnerf 3 > gpurun_out/${TAG}_bwd_plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"blend_backward|deform_backward|preprocess_backward" \
     -s 6 -c 3 -o gpurun_out/${TAG}_backward -f python tools/bwd_one.py dnerf 3 > gpurun_out/${TAG}_bwd_ncu.log 2>&1
+python tools/ncu_summary.py gpurun_out/${TAG}_backward.ncu-rep > gpurun_out/${TAG}_backward.summary.txt 2>&1
+python tools/ncu_lines.py gpurun_out/${TAG}_backward.ncu-rep 30 > gpurun_out/${TAG}_backward.lines.txt 2>&1
+[ "${KEEP_REPS:-0}" = "1" ] || rm -f gpurun_out/${TAG}_backward.ncu-rep

@@ -154,10 +154,16 @@ if os.path.exists(lc):
             "`blend_kernel<1>`)", ""]
     out.append(subprocess.run([sys.executable, "tools/ncu_launches.py", lc], capture_output=True, text=True).stdout.strip())
 reps = sorted(glob.glob(f"{G}/{TAG}_*.ncu-rep"))
-if reps:
-    out += ["", "## ncu --set full, one launch per kernel (20-frame batch)", ""]
+txts = sorted(glob.glob(f"{G}/{TAG}_*.summary.txt"))
+if reps or txts:
+    out += ["", "## ncu --set full, one launch per kernel (20-frame batch; backward: one D frame)", ""]
     for rep in reps:
         out.append(subprocess.run([sys.executable, "tools/ncu_summary.py", rep], capture_output=True, text=True).stdout.strip())
+        out.append("")
+    for t in txts:
+        if t.replace(".summary.txt", ".ncu-rep") in reps:
+            continue
+        out.append(open(t).read().strip())
         out.append("")
 open(f"profiles/{NAME}_summary.md", "w").write("\n".join(out) + "\n")
 print(f"profiles/{NAME}_summary.md", len(out), "lines")
