@@ -240,7 +240,11 @@ int fgs_l1_loss(const float* image, const float* target, int32_t width, int32_t 
 int fgs_tv_loss(const fgs_hexplanes* field, float weight, fgs_field_grads* grads, double* partials, float* loss,
                 fgs_stream_t stream);
 /* Splat backward for ONE frame: cam, g and the workspace ws must be those of the fgs_render call that
- * produced `image` (the sorted lists and records are read from ws, which must be unchanged since).
+ * produced `image` (the sorted lists and records are read from ws, which must be unchanged since); for
+ * frame f of an fgs_render_batch / fgs_frames call pass that frame's slice: ws + f * per, per bytes, with
+ * per = (ws_bytes / n_frames) rounded down to a multiple of 256.
+ * Accumulation is in 2^-40 fixed point (64-bit integer atomics): every per-Gaussian and per-weight sum
+ * must stay within +-8.4e6 (ample for the mean-reduced losses above; scale a sum-reduced loss down). */
  * Writes (overwrites) dg->means, log_scales, quats (raw), opacity_logits and sh for all n Gaussians
  * (0 for culled ones).  scratch: device memory of fgs_render_backward_scratch_bytes(n) bytes. */
 size_t fgs_render_backward_scratch_bytes(int64_t n);
