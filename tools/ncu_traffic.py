@@ -34,6 +34,33 @@ def kernel_traffic(rep):
     return res
 
 
+def summary_traffic(path):
+    """The same numbers from a tools/ncu_summary.py text summary (the .ncu-rep deleted on the GPU box)."""
+    res, name, vals = {}, None, {}
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def flush():
+        if name and "gpu__time_duration.sum" in vals:
+            d, du = vals["gpu__time_duration.sum"]
+            dur_s = d * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(du, 1e-9)
+            tot = sum(v * units.get(uu, 1) for k, (v, uu) in vals.items() if k.startswith("dram__bytes_"))
+            res[name] = {"dram_bytes_per_launch": tot, "ncu_duration_s": dur_s, "report": os.path.basename(path)}
+    for line in open(path):
+        if line.startswith("### "):
+            flush()
+            name = line[4:].strip().split("(")[0].split("::")[-1].split("<")[0]
+            vals = {}
+        elif line.startswith("| ") and name:
+            parts = [x.strip() for x in line.strip().strip("|").split("|")]
+            if len(parts) == 3:
+                try:
+                    vals[parts[0]] = (float(parts[1].replace(",", "")), parts[2])
+                except ValueError:
+                    pass
+    flush()
+    return res
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, required=True)
@@ -46,6 +73,6 @@ if __name__ == "__main__":
             "how": "ncu --set full --clock-control none, one launch per kernel of bench.py's default step",
             "kernels": {}}
     for rep in a.reports:
-        data["kernels"].update(kernel_traffic(rep))
+        data["kernels"].update(summary_traffic(rep) if rep.endswith(".txt") else kernel_traffic(rep))
     json.dump(data, open(a.out, "w"), indent=1)
     print(json.dumps(data, indent=1))
