@@ -244,7 +244,7 @@ int fgs_tv_loss(const fgs_hexplanes* field, float weight, fgs_field_grads* grads
  * frame f of an fgs_render_batch / fgs_frames call pass that frame's slice: ws + f * per, per bytes, with
  * per = (ws_bytes / n_frames) rounded down to a multiple of 256.
  * Accumulation is in 2^-40 fixed point (64-bit integer atomics): every per-Gaussian and per-weight sum
- * must stay within +-8.4e6 (ample for the mean-reduced losses above; scale a sum-reduced loss down). */
+ * must stay within +-8.4e6 (ample for the mean-reduced losses above; scale a sum-reduced loss down).
  * Writes (overwrites) dg->means, log_scales, quats (raw), opacity_logits and sh for all n Gaussians
  * (0 for culled ones).  scratch: device memory of fgs_render_backward_scratch_bytes(n) bytes. */
 size_t fgs_render_backward_scratch_bytes(int64_t n);
