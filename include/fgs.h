@@ -261,6 +261,13 @@ int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* field, cons
                         const fgs_gaussian_grads* d_deformed, const fgs_gaussian_grads* d_canonical,
                         const fgs_field_grads* d_field, void* scratch, size_t scratch_bytes, fgs_stream_t stream);
 
+/* One Adam step over n parameters (elementwise, the optimiser [3dgs] and the paper
+ * train with): m = b1 m + (1 - b1) g; v = b2 v + (1 - b2) g^2; p -= lr (m / (1 - b1^step)) /
+ * (sqrt(v / (1 - b2^step)) + eps) (reading A1).  param / m / v updated in place, grad read; step >= 1.
+ * Apply it to every gradient tensor of fgs_gaussian_grads / fgs_field_grads with its own moments. */
+int fgs_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, float lr, float beta1,
+                  float beta2, float eps, int32_t step, fgs_stream_t stream);
+
 /* ---- profiling -------------------------------------------------------------------------------
  * When enabled, the library records a CUDA event pair around every stage it launches, on the
  * stream of the call.  fgs_profile_read synchronises those events and writes the accumulated

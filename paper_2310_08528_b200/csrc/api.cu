@@ -872,6 +872,18 @@ int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* h, const fg
   return e == cudaSuccess ? FGS_OK : cuda_fail(e, "deform backward");
 }
 
+int fgs_adam_step(float* param, const float* grad, float* m, float* v, int64_t n, float lr, float beta1,
+                  float beta2, float eps, int32_t step, fgs_stream_t stream) {
+  FGS_CHECK(n >= 0, "n must be >= 0");
+  if (n == 0) return FGS_OK;
+  FGS_CHECK(param && grad && m && v, "null argument");
+  FGS_CHECK(step >= 1, "step counts from 1");
+  FGS_CHECK(isfinite(lr) && beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f,
+            "bad Adam hyper-parameters");
+  const cudaError_t e = launch_adam(param, grad, m, v, n, lr, beta1, beta2, eps, step, (cudaStream_t)stream);
+  return e == cudaSuccess ? FGS_OK : cuda_fail(e, "adam");
+}
+
 const char* fgs_last_error(void) { return g_err.c_str(); }
 
 

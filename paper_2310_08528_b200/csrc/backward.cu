@@ -710,6 +710,22 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
   }
 }
 
+// ------------------------------------------------------------------ Adam
+// p -= lr m^ / (sqrt(v^) + eps), bias-corrected, elementwise (reading A1: eps outside the square root,
+// t from 1); the moments and the correction factors in fp32, 1 - b^t formed on the host in fp64.
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                  float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
+                                                  float b1, float b2, float eps, float inv_c1, float inv_c2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = fmaf(b1, m[i], (1.f - b1) * gi);
+    const float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi * inv_c1) / (sqrtf(vi * inv_c2) + eps);
+  }
+}
+
 // dst[i] += acc[i] * 2^-40 (fp32); acc zeroed for the next call
 __global__ void fixed_to_float_kernel(unsigned long long* __restrict__ acc, float* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -740,6 +756,16 @@ cudaError_t launch_tv(const TvArgs& a0, cudaStream_t s) {
   tv_kernel<<<kLossPartials, kLossThreads, 0, s>>>(a, 1.0 / terms);
   loss_finish_kernel<<<1, 32, 0, s>>>(a.partials, kLossPartials, a.loss);
   note_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                        float eps, int32_t t, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const double c1 = 1.0 - pow((double)b1, (double)t), c2 = 1.0 - pow((double)b2, (double)t);
+  const unsigned grid = (unsigned)std::min<int64_t>(4096, (n + 255) / 256);
+  adam_kernel<<<grid, 256, 0, s>>>(p, g, m, v, n, lr, b1, b2, eps, (float)(1.0 / c1), (float)(1.0 / c2));
+  note_launches(1);
   return cudaGetLastError();
 }
 

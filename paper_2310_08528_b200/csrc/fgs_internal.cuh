@@ -156,6 +156,8 @@ cudaError_t launch_render_backward(const RenderBatch& b, const float* image, con
                                    unsigned long long* acc, float* d_means, float* d_log_scales, float* d_quats,
                                    float* d_opacity, float* d_sh, cudaStream_t s);
 size_t deform_backward_acc_elems(const DeformBatch& p);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                        float eps, int32_t t, cudaStream_t s);
 cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const float* dls, const float* dq,
                                    float* om, float* ols, float* oq, unsigned long long* acc, float* const* plane_grads,
                                    float* const* mlp_grads, cudaStream_t s);

@@ -80,7 +80,7 @@ EXPORTS = ("fgs_deform", "fgs_deform_range", "fgs_deform_range_peers", "fgs_defo
            "fgs_frames_host_workspace_bytes", "fgs_frames_host", "fgs_frames_host_status", "fgs_profile_enable", "fgs_profile_read",
            "fgs_launch_count", "fgs_set_tuning", "fgs_get_tuning", "fgs_last_error", "fgs_version",
            "fgs_l1_loss", "fgs_tv_loss", "fgs_render_backward_scratch_bytes", "fgs_render_backward",
-           "fgs_deform_backward_scratch_bytes", "fgs_deform_backward")
+           "fgs_deform_backward_scratch_bytes", "fgs_deform_backward", "fgs_adam_step")
 SIZE_EXPORTS = ("fgs_render_workspace_bytes", "fgs_frames_host_workspace_bytes", "fgs_render_backward_scratch_bytes",
                 "fgs_deform_backward_scratch_bytes")
 STAGES = ("deform", "preprocess", "tile_scan", "duplicate", "tile_sort", "blend")
@@ -134,6 +134,8 @@ def lib():
         L.fgs_deform_backward.argtypes = [P(fgs_gaussians), P(fgs_hexplanes), P(fgs_mlp), c_float,
                                           P(fgs_gaussian_grads), P(fgs_gaussian_grads), P(fgs_field_grads), c_void_p,
                                           c_size_t, c_void_p]
+        L.fgs_adam_step.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_float, c_float,
+                                    c_float, c_int32, c_void_p]
         L.fgs_profile_enable.argtypes = [c_int]
         L.fgs_profile_read.argtypes = [P(ctypes.c_double), P(c_int64)]
         L.fgs_launch_count.restype = c_int64
@@ -301,6 +303,12 @@ def fgs_deform_backward(g, field, mlp, t, d_deformed, d_canonical, d_field, scra
     return _check(lib().fgs_deform_backward(ctypes.byref(g), ctypes.byref(field), ctypes.byref(mlp), c_float(t),
                                             ctypes.byref(d_deformed), ctypes.byref(d_canonical), ctypes.byref(d_field),
                                             _ptr(scratch), scratch.numel(), _stream(stream)))
+
+
+def fgs_adam_step(param, grad, m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    """One Adam step on device tensors of equal numel (param, m, v updated in place)."""
+    return _check(lib().fgs_adam_step(_ptr(param), _ptr(grad), _ptr(m), _ptr(v), param.numel(), c_float(lr),
+                                      c_float(beta1), c_float(beta2), c_float(eps), int(step), _stream(stream)))
 
 
 def fgs_profile_enable(enable=True):
