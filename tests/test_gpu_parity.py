@@ -85,11 +85,11 @@ def test_zero_heads_identity_on_gpu():
     assert np.array_equal(g["log_scales"], s.log_scales)
 
 
-def _render_parity(scene, frame=0, tiles_subset=None, check_tiles=True):
+def _render_parity(scene, frame=0, tiles_subset=None, check_tiles=True, max_instances=None):
     ds = _ds(scene)
     cam = scene.cameras[frame]
     dstruct, g, _ = gpu_deform(ds, float(scene.times[frame]))
-    out = gpu_render_debug(ds, cam, dstruct)
+    out = gpu_render_debug(ds, cam, dstruct, max_instances)
     assert out["status"] == fgs.FGS_OK
     ref = OR.render_ref(g, scene.opacity_logits, scene.sh, scene.sh_degree, cam, tiles_subset=tiles_subset)
     ints = compare_integer_work(out, ref["pre"], (ref["tiles"], ref["gids"], ref["ranges"]))
@@ -844,3 +844,16 @@ def test_radix_auto_selection_and_threshold():
     for o in outs[1:]:
         for k in ("sorted_gid", "ranges", "image"):
             assert np.array_equal(o[k], outs[0][k]), k
+
+
+@pytest.mark.parametrize("W,H", [(16384, 24), (20, 16384)])
+def test_maximum_image_extent(W, H):
+    """The largest image side the ABI accepts (16384 px: 1024 tiles along it, the 16-bit packed rect's
+    range): strips through the tiny scene, integer work and pixels against the oracle, tile lists
+    bit-exact (every tile)."""
+    s = make_scene("tiny", n=1500, width=W, height=H)
+    _render_parity(s, max_instances=400 * s.n)        # fx ~ 17.6k px at 16384 wide: big rects
+    with pytest.raises(fgs.FgsError):
+        bad = make_scene("tiny", n=10, width=16385, height=8)
+        ds = _ds(bad)
+        gpu_render_debug(ds, bad.cameras[0], ds.canonical_struct())
