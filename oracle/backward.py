@@ -54,8 +54,9 @@ def params_of(scene, deformable=True):
         for l in range(len(f.planes)):
             for p in range(6):
                 P[f"plane{l}_{p}"] = _t(f.planes[l][p])
-        for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s"):
-            P[k] = _t(getattr(scene.mlp, k))
+        for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s", "w_c", "b_c", "w_a", "b_a"):
+            if getattr(scene.mlp, k, None) is not None:        # phi_C / phi_alpha only when present
+                P[k] = _t(getattr(scene.mlp, k))
     for v in P.values():
         v.requires_grad_(True)
     return P
@@ -91,9 +92,14 @@ def deform_torch(scene, t, P):
         feats.append(f_l)
     f_h = torch.cat(feats, dim=1)
     f_d = torch.relu(f_h @ P["w_d"].T + P["b_d"])
-    return {"means": P["means"] + f_d @ P["w_x"].T + P["b_x"],
-            "quats": P["quats"] + f_d @ P["w_r"].T + P["b_r"],
-            "log_scales": P["log_scales"] + f_d @ P["w_s"].T + P["b_s"]}
+    G = {"means": P["means"] + f_d @ P["w_x"].T + P["b_x"],
+         "quats": P["quats"] + f_d @ P["w_r"].T + P["b_r"],
+         "log_scales": P["log_scales"] + f_d @ P["w_s"].T + P["b_s"]}
+    if "w_c" in P:       # P:1232 colour decoder: C' = C + dC over all K x 3 coefficients (reading C1)
+        G["sh"] = P["sh"] + (f_d @ P["w_c"].T + P["b_c"]).reshape(P["sh"].shape)
+    if "w_a" in P:       # P:1232 opacity decoder: logit' = logit + dalpha
+        G["opacity_logits"] = P["opacity_logits"] + (f_d @ P["w_a"].T + P["b_a"])[:, 0]
+    return G
 
 
 # ------------------------------------------------------------------ S: the splatting
@@ -217,7 +223,8 @@ def tv_loss(planes):
 def frame_loss(scene, frame, target, tv_weight, P):
     """L of one (t, camera) frame: deform (leaf tensors P), render, L1 + w_tv L_tv (B3)."""
     G = deform_torch(scene, float(scene.times[frame]), P)
-    img = render_torch(G, P["opacity_logits"], P["sh"], scene.sh_degree, scene.cameras[frame])
+    img = render_torch(G, G.get("opacity_logits", P["opacity_logits"]), G.get("sh", P["sh"]), scene.sh_degree,
+                       scene.cameras[frame])
     planes = [P[k] for k in sorted(P) if k.startswith("plane")]
     return l1_loss(img, target) + tv_weight * tv_loss(planes), img
 
@@ -246,9 +253,10 @@ def render_grads_ref(deformed, opacity_logits, sh, sh_degree, cam, dL_dimage):
 
 def deform_grads_ref(scene, t, dL_ddeformed):
     """The deformation field alone: gradients of sum_k <dL_ddeformed[k], G'[k]> (k = means, log_scales,
-    quats) w.r.t. the canonical means / log-scales / quats, the planes and the MLP."""
+    quats, and with the P:1232 decoders sh / opacity_logits) w.r.t. the canonical parameters, the planes
+    and the MLP."""
     P = params_of(scene)
     G = deform_torch(scene, t, P)
-    sum(((G[k] * _t(dL_ddeformed[k])).sum() for k in ("means", "log_scales", "quats"))).backward()
+    sum(((G[k] * _t(dL_ddeformed[k])).sum() for k in G)).backward()
     return {k: (v.grad.numpy().copy() if v.grad is not None else np.zeros(tuple(v.shape)))
-            for k, v in P.items() if k not in ("opacity_logits", "sh")}
+            for k, v in P.items() if k in G or k not in ("opacity_logits", "sh")}

@@ -262,3 +262,38 @@ def test_plane_gradient_sparsity_and_linearity():
         acc = gi if acc is None else {k: acc[k] + gi[k] for k in acc}
     for k in full:
         assert np.allclose(full[k], acc[k], rtol=0, atol=1e-12 * max(1.0, np.abs(full[k]).max())), k
+
+
+def test_colour_opacity_decoder_gradients_match_finite_differences():
+    """P:1232 decoders: with phi_C / phi_alpha the deformed SH and opacity logits are G' outputs too; their
+    gradients w.r.t. W_c, b_c, W_a, b_a, the shared phi_d / W_d / planes and the canonical SH / logits
+    against central differences of oracle.deform.deform_ref (which applies the decoders)."""
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = with_colour_heads(_small_scene(n=5, seed=7, heads=0.3), 0.2, 0.3)
+    s = dataclasses.replace(s, sh=s.sh.astype(np.float64), opacity_logits=s.opacity_logits.astype(np.float64))
+    t = float(s.times[0])
+    rng = np.random.default_rng(8)
+    w = {k: rng.normal(size=np.shape(v)) for k, v in oracle.deform_ref(s, t).items()}
+    assert set(w) == {"means", "log_scales", "quats", "sh", "opacity_logits"}
+    grads = B.deform_grads_ref(s, t, w)
+
+    def f_of(mutate):
+        def f(x):
+            G = oracle.deform_ref(mutate(x), t)
+            return float(sum(np.sum(w[k] * G[k]) for k in G)), None
+        return f
+
+    checked = 0
+    for k in ("w_c", "b_c", "w_a", "b_a", "w_d", "b_d"):
+        x0 = getattr(s.mlp, k).astype(np.float64)
+        idxs = range(x0.size) if x0.size <= 30 else rng.choice(x0.size, 30, replace=False)
+        checked += _fd_check(f_of(lambda x, k=k: dataclasses.replace(s, mlp=dataclasses.replace(s.mlp, **{k: x}))),
+                             x0, grads[k], idxs)
+    for k in ("sh", "opacity_logits", "means"):
+        x0 = getattr(s, k).astype(np.float64)
+        idxs = range(x0.size) if x0.size <= 40 else rng.choice(x0.size, 40, replace=False)
+        checked += _fd_check(f_of(lambda x, k=k: dataclasses.replace(s, **{k: x})), x0, grads[k], idxs)
+    # the canonical SH / logits enter additively: their gradient is the upstream one
+    assert np.allclose(grads["sh"], w["sh"], rtol=0, atol=1e-12)
+    assert np.allclose(grads["opacity_logits"], w["opacity_logits"], rtol=0, atol=1e-12)
+    assert checked > 150
