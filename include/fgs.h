@@ -231,6 +231,7 @@ typedef struct {                    /* dL/d per-Gaussian arrays (device, fp32, l
 typedef struct {                    /* dL/d field + MLP (device, fp32, layouts as fgs_hexplanes / fgs_mlp) */
   float* planes[FGS_MAX_SCALES][FGS_PLANES];
   float *w_d, *b_d, *w_x, *b_x, *w_r, *b_r, *w_s, *b_s;
+  float *w_c, *b_c, *w_a, *b_a;     /* the P:1232 decoders' gradients (needed only when the MLP has them) */
 } fgs_field_grads;
 /* loss[0] = mean |image - target| over [3][H][W] (B2); dL_dimage (may be NULL) = sign(image - target) /
  * (3 H W), 0 where equal.  partials: device double[FGS_LOSS_PARTIALS] scratch. */
@@ -251,11 +252,13 @@ size_t fgs_render_backward_scratch_bytes(int64_t n);
 int fgs_render_backward(const fgs_camera* cam, const fgs_deformed* g, const float* image, const float* dL_dimage,
                         const void* ws, size_t ws_bytes, void* scratch, size_t scratch_bytes,
                         const fgs_gaussian_grads* dg, fgs_stream_t stream);
-/* Deformation backward at time t: given dL/dG' (d_deformed: means, log_scales, quats), writes dL/dG for
- * the canonical means (additive path + the query-position path u(X)), log_scales and quats into
- * d_canonical (opacity_logits / sh untouched: they are not deformed), and ADDS dL/d planes and MLP
- * weights into d_field.  Not with the P:1232 decoders (FGS_E_NOTIMPL).  scratch: device memory of
- * fgs_deform_backward_scratch_bytes(field, mlp) bytes. */
+/* Deformation backward at time t: given dL/dG' (d_deformed: means, log_scales, quats; with the P:1232
+ * decoders also sh and/or opacity_logits — the render backward's gradients of the deformed SH / logits),
+ * writes dL/dG for the canonical means (additive path + the query-position path u(X)), log_scales and
+ * quats into d_canonical (and, with the decoders, sh / opacity_logits: the decoders add to them, so their
+ * gradient passes through; without them d_canonical's sh / opacity_logits are untouched — use the render
+ * backward's directly), and ADDS dL/d planes and MLP weights (incl. w_c, b_c, w_a, b_a) into d_field.
+ * scratch: device memory of fgs_deform_backward_scratch_bytes(field, mlp) bytes. */
 size_t fgs_deform_backward_scratch_bytes(const fgs_hexplanes* field, const fgs_mlp* mlp);
 int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* field, const fgs_mlp* mlp, float t,
                         const fgs_gaussian_grads* d_deformed, const fgs_gaussian_grads* d_canonical,

@@ -840,6 +840,8 @@ size_t fgs_deform_backward_scratch_bytes(const fgs_hexplanes* field, const fgs_m
   p.n_scales = field->n_scales; p.feat = field->feat; p.t_res = field->t_res;
   for (int l = 0; l < field->n_scales; ++l) p.res[l] = field->res[l];
   p.width = mlp->width; p.in_dim = mlp->in_dim;
+  p.w_c = mlp->w_c; p.w_a = mlp->w_a;
+  p.n_c = mlp->w_c ? 3 * 16 : 0;     // sized for SH degree 3 (the largest K); exact for lower degrees
   return deform_backward_acc_elems(p) * sizeof(unsigned long long);
 }
 
@@ -851,24 +853,32 @@ int fgs_deform_backward(const fgs_gaussians* g, const fgs_hexplanes* h, const fg
   if ((rc = check_field(h, m)) != FGS_OK) return rc;
   FGS_CHECK(isfinite(t) && t >= 0.f && t <= 1.f, "t must be finite and in [0,1]");
   FGS_CHECK(dd && dc && df && scratch, "null argument");
-  if (m->w_c || m->w_a) return fail(FGS_E_NOTIMPL, "backward of the P:1232 colour / opacity decoders");
   FGS_CHECK(scratch_bytes >= fgs_deform_backward_scratch_bytes(h, m), "scratch too small");
   for (int l = 0; l < h->n_scales; ++l)
     for (int q = 0; q < FGS_PLANES; ++q) FGS_CHECK(df->planes[l][q], "null plane gradient");
   FGS_CHECK(df->w_d && df->b_d && df->w_x && df->b_x && df->w_r && df->b_r && df->w_s && df->b_s,
             "null MLP gradient");
-  if (g->n > 0)
+  if (m->w_c) FGS_CHECK(df->w_c && df->b_c, "phi_C: null w_c / b_c gradient");
+  if (m->w_a) FGS_CHECK(df->w_a && df->b_a, "phi_alpha: null w_a / b_a gradient");
+  if (g->n > 0) {
     FGS_CHECK(dd->means && dd->log_scales && dd->quats && dc->means && dc->log_scales && dc->quats,
               "null per-Gaussian gradient");
+    if (m->w_c) FGS_CHECK(dd->sh && dc->sh, "phi_C: null SH gradient (d_deformed.sh in, d_canonical.sh out)");
+    if (m->w_a) FGS_CHECK(dd->opacity_logits && dc->opacity_logits, "phi_alpha: null opacity gradient");
+  }
   DeformBatch p;
   fill_deform(p, g, h, m);
   p.begin = 0; p.end = g->n; p.n_t = 1; p.t[0] = t;
   float* pg[FGS_MAX_SCALES * FGS_PLANES] = {};
   for (int l = 0; l < h->n_scales; ++l)
     for (int q = 0; q < FGS_PLANES; ++q) pg[l * FGS_PLANES + q] = df->planes[l][q];
-  float* mg[8] = {df->w_d, df->b_d, df->w_x, df->b_x, df->w_r, df->b_r, df->w_s, df->b_s};
-  const cudaError_t e = launch_deform_backward(p, dd->means, dd->log_scales, dd->quats, dc->means, dc->log_scales,
-                                               dc->quats, (unsigned long long*)scratch, pg, mg, (cudaStream_t)stream);
+  float* mg[12] = {df->w_d, df->b_d, df->w_x, df->b_x, df->w_r, df->b_r, df->w_s, df->b_s,
+                   df->w_c, df->b_c, df->w_a, df->b_a};
+  const cudaError_t e = launch_deform_backward(p, dd->means, dd->log_scales, dd->quats, m->w_c ? dd->sh : nullptr,
+                                               m->w_a ? dd->opacity_logits : nullptr, dc->means, dc->log_scales,
+                                               dc->quats, m->w_c ? dc->sh : nullptr,
+                                               m->w_a ? dc->opacity_logits : nullptr, (unsigned long long*)scratch, pg,
+                                               mg, (cudaStream_t)stream);
   return e == cudaSuccess ? FGS_OK : cuda_fail(e, "deform backward");
 }
 

@@ -512,14 +512,23 @@ constexpr int db_rows() { return W >= 128 ? 32 : 64; }
 struct DefBwdArgs {
   DeformBatch p;                    // n_t = 1, t[0]
   const float *d_means, *d_log_scales, *d_quats;     // dL/dG' [n][3|3|4]
+  const float *d_sh, *d_opacity;                     // dL/dG' of the P:1232 decoders' outputs (or NULL)
   float *o_means, *o_log_scales, *o_quats;           // dL/dG (canonical), written
+  float *o_sh, *o_opacity;                           // canonical SH / logits (pass-through copies)
+  int nout;                                          // head outputs: 10 + 3K (phi_C) + 1 (phi_alpha)
   unsigned long long* acc_planes[FGS_MAX_SCALES][FGS_PLANES];   // fixed-point, same layout as planes
-  unsigned long long *acc_wd, *acc_bd, *acc_wh, *acc_bh;         // [W][IN], [W], [10][W], [10]
+  unsigned long long *acc_wd, *acc_bd, *acc_wh, *acc_bh;         // [W][IN], [W], [nout][W], [nout]
 };
 
-template <int W, int IN>
+// head-output rows of the shared weight / dOut buffers: 10 geometry rows, or up to 60 with the decoders
+template <bool COLOR>
+constexpr int db_nout() { return COLOR ? 60 : 10; }
+
+template <int W, int IN, bool COLOR>
 __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __grid_constant__ DefBwdArgs A) {
   constexpr int kDbRows = db_rows<W>();
+  constexpr int NO = db_nout<COLOR>();       // row stride of sWh / sDo
+  const int nout = A.nout;
   constexpr int KS = (IN + 31) / 32;       // feature slots per lane
   constexpr int WS = W / 32;               // hidden-unit slots per lane
   const DeformBatch& p = A.p;
@@ -527,11 +536,11 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
   float* sWd = dsm;                        // [W][IN]   row-major (k contiguous)
   float* sWdT = sWd + W * IN;              // [IN][W]   transposed (cw contiguous)
   float* sBd = sWdT + W * IN;              // [W]
-  float* sWh = sBd + W;                    // [10][W] : rows x(3), r(4), s(3)
-  float* sFh = sWh + 10 * W;               // [kDbRows][IN]
+  float* sWh = sBd + W;                    // [NO][W] : rows x(3), r(4), s(3), then C (3K), alpha
+  float* sFh = sWh + NO * W;               // [kDbRows][IN]
   float* sDz = sFh + kDbRows * IN;         // [kDbRows][W]
   float* sFd = sDz + kDbRows * W;          // [kDbRows][W]
-  float* sDo = sFd + kDbRows * W;          // [kDbRows][10]
+  float* sDo = sFd + kDbRows * W;          // [kDbRows][NO]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < W * IN; e += kDbThreads) {
     const float v = p.w_d[e];
@@ -539,9 +548,11 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
     sWdT[(e % IN) * W + e / IN] = v;
   }
   for (int e = tid; e < W; e += kDbThreads) sBd[e] = p.b_d[e];
-  for (int e = tid; e < 10 * W; e += kDbThreads) {
+  const int n_c = COLOR ? p.n_c : 0;
+  for (int e = tid; e < nout * W; e += kDbThreads) {
     const int o = e / W, c = e - o * W;
-    sWh[e] = o < 3 ? p.w_x[o * W + c] : (o < 7 ? p.w_r[(o - 3) * W + c] : p.w_s[(o - 7) * W + c]);
+    sWh[e] = o < 3 ? p.w_x[o * W + c] : o < 7 ? p.w_r[(o - 3) * W + c] : o < 10 ? p.w_s[(o - 7) * W + c]
+             : o < 10 + n_c ? p.w_c[(o - 10) * W + c] : p.w_a[c];
   }
   __syncthreads();
   const int FEAT = p.feat;
@@ -553,11 +564,11 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
     float* fh = sFh + r * IN;
     float* dz = sDz + r * W;
     float* fd = sFd + r * W;
-    float* dO = sDo + r * 10;
+    float* dO = sDo + r * NO;
     if (r >= nrow) {                          // rows past the range: zero rows for the reduction
       for (int k = lane; k < IN; k += 32) fh[k] = 0.f;
       for (int c = lane; c < W; c += 32) { dz[c] = 0.f; fd[c] = 0.f; }
-      if (lane < 10) dO[lane] = 0.f;
+      for (int o = lane; o < nout; o += 32) dO[o] = 0.f;
       continue;
     }
     const int64_t g = row0 + r;
@@ -594,8 +605,9 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
       }
       fhv[ks] = f;
     }
-    if (lane < 10) dO[lane] = lane < 3 ? A.d_means[g * 3 + lane] : (lane < 7 ? A.d_quats[g * 4 + lane - 3]
-                                                                             : A.d_log_scales[g * 3 + lane - 7]);
+    for (int o = lane; o < nout; o += 32)
+      dO[o] = o < 3 ? A.d_means[g * 3 + o] : o < 7 ? A.d_quats[g * 4 + o - 3] : o < 10 ? A.d_log_scales[g * 3 + o - 7]
+              : o < 10 + n_c ? A.d_sh[g * n_c + (o - 10)] : A.d_opacity[g];
     __syncwarp();
     // ---- z = W_d f_h + b_d (hidden unit cw = lane + 32 w), dz = (W_h^T dOut) [z > 0] ----
     float zz[WS];
@@ -612,7 +624,7 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
       const int cw = lane + 32 * w;
       float dfd = 0.f;
 #pragma unroll
-      for (int o = 0; o < 10; ++o) dfd = fmaf(sWh[o * W + cw], dO[o], dfd);
+      for (int o = 0; o < nout; ++o) dfd = fmaf(sWh[o * W + cw], dO[o], dfd);
       dzv[w] = zz[w] > 0.f ? dfd : 0.f;
       fd[cw] = fmaxf(zz[w], 0.f);
       dz[cw] = dzv[w];
@@ -682,6 +694,10 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
       A.o_log_scales[g * 3 + lane] = A.d_log_scales[g * 3 + lane];
     }
     if (lane < 4) A.o_quats[g * 4 + lane] = A.d_quats[g * 4 + lane];
+    if (COLOR) {   // the decoders add to the canonical SH / logits: their gradient passes through
+      for (int j = lane; j < n_c; j += 32) A.o_sh[g * n_c + j] = A.d_sh[g * n_c + j];
+      if (lane == 0 && nout > 10 + n_c) A.o_opacity[g] = A.d_opacity[g];
+    }
   }
   __syncthreads();
   // ---- MLP weight gradients: the CTA's rows summed in row order, one fixed-point atomic each ----
@@ -710,16 +726,16 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
     for (int r = 0; r < nrow; ++r) sacc += sDz[r * W + cw];
     fix_add(A.acc_bd + cw, sacc);
   }
-  for (int e = tid; e < 10 * W; e += kDbThreads) {
+  for (int e = tid; e < nout * W; e += kDbThreads) {
     const int o = e / W, cw = e - o * W;
     float sacc = 0.f;
-    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDo[r * 10 + o], sFd[r * W + cw], sacc);
+    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDo[r * NO + o], sFd[r * W + cw], sacc);
     fix_add(A.acc_wh + e, sacc);
   }
-  if (tid < 10) {
+  for (int o = tid; o < nout; o += kDbThreads) {
     float sacc = 0.f;
-    for (int r = 0; r < nrow; ++r) sacc += sDo[r * 10 + tid];
-    fix_add(A.acc_bh + tid, sacc);
+    for (int r = 0; r < nrow; ++r) sacc += sDo[r * NO + o];
+    fix_add(A.acc_bh + o, sacc);
   }
 }
 
@@ -798,26 +814,35 @@ cudaError_t launch_render_backward(const RenderBatch& b, const float* image, con
   return cudaGetLastError();
 }
 
+static int head_outputs(const DeformBatch& p) { return 10 + (p.w_c ? p.n_c : 0) + (p.w_a ? 1 : 0); }
+
 size_t deform_backward_acc_elems(const DeformBatch& p) {
   size_t n = 0;
   for (int l = 0; l < p.n_scales; ++l)
     for (int q = 0; q < FGS_PLANES; ++q)
       n += (size_t)(q < 3 ? p.res[l] : p.t_res) * p.res[l] * p.feat;
-  return n + (size_t)p.width * p.in_dim + p.width + 10 * (size_t)p.width + 10;
+  const size_t no = (size_t)head_outputs(p);
+  return n + (size_t)p.width * p.in_dim + p.width + no * (size_t)p.width + no;
 }
 
+template <int W, int IN, bool COLOR>
+cudaError_t launch_def_bwd_c(const DefBwdArgs& A, unsigned grid, cudaStream_t s) {
+  constexpr size_t NO = db_nout<COLOR>();
+  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + NO * W + (size_t)db_rows<W>() * (IN + 2 * W + NO));
+  cudaError_t e = cudaFuncSetAttribute(deform_backward_kernel<W, IN, COLOR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  deform_backward_kernel<W, IN, COLOR><<<grid, kDbThreads, smem, s>>>(A);
+  return cudaGetLastError();
+}
 template <int W, int IN>
 cudaError_t launch_def_bwd_t(const DefBwdArgs& A, unsigned grid, cudaStream_t s) {
-  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + 10 * W + (size_t)db_rows<W>() * (IN + 2 * W + 10));
-  cudaError_t e = cudaFuncSetAttribute(deform_backward_kernel<W, IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  deform_backward_kernel<W, IN><<<grid, kDbThreads, smem, s>>>(A);
-  return cudaGetLastError();
+  return A.nout > 10 ? launch_def_bwd_c<W, IN, true>(A, grid, s) : launch_def_bwd_c<W, IN, false>(A, grid, s);
 }
 
 cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const float* dls, const float* dq,
-                                   float* om, float* ols, float* oq, unsigned long long* acc, float* const* plane_grads,
+                                   const float* dsh, const float* dop, float* om, float* ols, float* oq, float* osh,
+                                   float* oop, unsigned long long* acc, float* const* plane_grads,
                                    float* const* mlp_grads, cudaStream_t s) {
   const size_t total = deform_backward_acc_elems(p);
   cudaError_t e = cudaMemsetAsync(acc, 0, total * sizeof(unsigned long long), s);
@@ -827,6 +852,9 @@ cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const 
   A.p = p;
   A.d_means = dm; A.d_log_scales = dls; A.d_quats = dq;
   A.o_means = om; A.o_log_scales = ols; A.o_quats = oq;
+  A.d_sh = dsh; A.d_opacity = dop; A.o_sh = osh; A.o_opacity = oop;
+  A.nout = head_outputs(p);
+  const size_t NOUT = (size_t)A.nout;
   size_t off = 0;
   for (int l = 0; l < p.n_scales; ++l)
     for (int q = 0; q < FGS_PLANES; ++q) {
@@ -835,8 +863,8 @@ cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const 
     }
   A.acc_wd = acc + off; off += (size_t)p.width * p.in_dim;
   A.acc_bd = acc + off; off += p.width;
-  A.acc_wh = acc + off; off += 10 * (size_t)p.width;
-  A.acc_bh = acc + off; off += 10;
+  A.acc_wh = acc + off; off += NOUT * (size_t)p.width;
+  A.acc_bh = acc + off; off += NOUT;
   const int rows = p.width >= 128 ? db_rows<128>() : db_rows<64>();
   const unsigned grid = (unsigned)((p.end - p.begin + rows - 1) / rows);
   if (grid > 0) {
@@ -858,15 +886,21 @@ cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const 
           acc + off, plane_grads[l * FGS_PLANES + q], (int64_t)n);
       off += n;
     }
-  const size_t W = p.width, IN = p.in_dim;
-  const size_t sizes[8] = {W * IN, W, 3 * W, 3, 4 * W, 4, 3 * W, 3};
-  // acc order: wd | bd | wh (x 3W, r 4W, s 3W) | bh (x 3, r 4, s 3); mlp_grads order w_d b_d w_x b_x w_r b_r w_s b_s
-  const size_t wh0 = off + W * IN + W, bh0 = wh0 + 10 * W;
-  const size_t src[8] = {off, off + W * IN, wh0, bh0, wh0 + 3 * W, bh0 + 3, wh0 + 7 * W, bh0 + 7};
-  for (int k = 0; k < 8; ++k)
+  const size_t W = p.width, IN = p.in_dim, NC = p.w_c ? (size_t)p.n_c : 0, NA = p.w_a ? 1 : 0;
+  const size_t sizes[12] = {W * IN, W, 3 * W, 3, 4 * W, 4, 3 * W, 3, NC * W, NC, NA * W, NA};
+  // acc order: wd | bd | wh (x 3W, r 4W, s 3W, c NC W, a NA W) | bh (x 3, r 4, s 3, c NC, a NA);
+  // mlp_grads order w_d b_d w_x b_x w_r b_r w_s b_s w_c b_c w_a b_a
+  const size_t wh0 = off + W * IN + W, bh0 = wh0 + NOUT * W;
+  const size_t src[12] = {off, off + W * IN, wh0, bh0, wh0 + 3 * W, bh0 + 3, wh0 + 7 * W, bh0 + 7,
+                          wh0 + 10 * W, bh0 + 10, wh0 + (10 + NC) * W, bh0 + 10 + NC};
+  int nk = 0;
+  for (int k = 0; k < 12; ++k) {
+    if (!sizes[k]) continue;
     fixed_to_float_kernel<<<(unsigned)std::min<size_t>(64, (sizes[k] + 255) / 256), 256, 0, s>>>(
         acc + src[k], mlp_grads[k], (int64_t)sizes[k]);
-  note_launches(p.n_scales * FGS_PLANES + 8);
+    ++nk;
+  }
+  note_launches(p.n_scales * FGS_PLANES + nk);
   return cudaGetLastError();
 }
 

@@ -159,7 +159,8 @@ size_t deform_backward_acc_elems(const DeformBatch& p);
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                         float eps, int32_t t, cudaStream_t s);
 cudaError_t launch_deform_backward(const DeformBatch& p, const float* dm, const float* dls, const float* dq,
-                                   float* om, float* ols, float* oq, unsigned long long* acc, float* const* plane_grads,
+                                   const float* dsh, const float* dop, float* om, float* ols, float* oq, float* osh,
+                                   float* oop, unsigned long long* acc, float* const* plane_grads,
                                    float* const* mlp_grads, cudaStream_t s);
 
 // Tuning knobs (api.cu, fgs_set_tuning).

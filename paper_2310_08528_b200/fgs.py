@@ -69,7 +69,7 @@ class fgs_gaussian_grads(ctypes.Structure):
 
 
 class fgs_field_grads(ctypes.Structure):
-    _fields_ = [("planes", (c_void_p * PLANES) * MAX_SCALES)] + [(k, c_void_p) for k in MLP_ARRAYS[:8]]
+    _fields_ = [("planes", (c_void_p * PLANES) * MAX_SCALES)] + [(k, c_void_p) for k in MLP_ARRAYS]
 
 
 FGS_LOSS_PARTIALS = 1024
@@ -496,9 +496,10 @@ class DeviceScene:
             for p, P in enumerate(ps):
                 t[f"plane{l}_{p}"] = torch.zeros_like(P)
                 st.planes[l][p] = t[f"plane{l}_{p}"].data_ptr()
-        for k in MLP_ARRAYS[:8]:
-            t[k] = torch.zeros_like(self.mlp_t[k])
-            setattr(st, k, t[k].data_ptr())
+        for k in MLP_ARRAYS:
+            if k in self.mlp_t:
+                t[k] = torch.zeros_like(self.mlp_t[k])
+                setattr(st, k, t[k].data_ptr())
         st._keep = t
         return st, t
 

@@ -30,21 +30,25 @@ class Trainer:
         self.part = torch.empty(fgs.FGS_LOSS_PARTIALS, dtype=torch.float64, device=dev)
         self.l1 = torch.empty(1, device=dev)
         self.tv = torch.zeros(1, device=dev)
-        self.dg, self.gt = ds.alloc_gaussian_grads()        # splat backward (opacity / SH grads used as is)
-        self.dc, self.ct = ds.alloc_gaussian_grads()        # canonical means / log_scales / quats
+        self.dg, self.gt = ds.alloc_gaussian_grads()        # splat backward: dL/dG' (deformed)
+        self.dc, self.ct = ds.alloc_gaussian_grads()        # canonical dL/dG out of the deformation backward
         self.df, self.ft = ds.alloc_field_grads()
         self.rs = torch.empty(fgs.fgs_render_backward_scratch_bytes(ds.n), dtype=torch.uint8, device=dev)
         self.dsb = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device=dev)
         # (param tensor, grad tensor, lr group) of every trainable tensor; Adam moments per tensor
         self.params = []
+        # SH / logits are deformed only with the P:1232 decoders; otherwise the splat gradient is theirs
+        canon_keys = {"means", "log_scales", "quats"} | ({"sh"} if ds.has_c else set()) \
+            | ({"opacity_logits"} if ds.has_a else set())
         for k in GAUSSIAN_KEYS:
-            grad = self.ct[k] if k in ("means", "log_scales", "quats") else self.gt[k]
+            grad = self.ct[k] if k in canon_keys else self.gt[k]
             self.params.append((getattr(ds, k), grad, "g"))
         for l, ps in enumerate(ds.planes):
             for p, P in enumerate(ps):
                 self.params.append((P, self.ft[f"plane{l}_{p}"], "f"))
-        for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s"):
-            self.params.append((ds.mlp_t[k], self.ft[k], "m"))
+        for k in ("w_d", "b_d", "w_x", "b_x", "w_r", "b_r", "w_s", "b_s", "w_c", "b_c", "w_a", "b_a"):
+            if k in self.ft:
+                self.params.append((ds.mlp_t[k], self.ft[k], "m"))
         self.m = [torch.zeros_like(p) for p, _, _ in self.params]
         self.v = [torch.zeros_like(p) for p, _, _ in self.params]
         self.t = 0

@@ -173,8 +173,9 @@ def _train_frame(ds, s, frame, target_t, tvw):
     fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, float(s.times[frame]), dg, dc, df, dsb)
     torch.cuda.synchronize()
     canon = {k: ct[k].cpu().numpy() for k in ("means", "log_scales", "quats")}
-    canon["opacity_logits"] = gt["opacity_logits"].cpu().numpy()
-    canon["sh"] = gt["sh"].cpu().numpy()
+    # with a P:1232 decoder the canonical SH / logits gradient comes out of the deformation backward
+    canon["opacity_logits"] = (ct if ds.has_a else gt)["opacity_logits"].cpu().numpy()
+    canon["sh"] = (ct if ds.has_c else gt)["sh"].cpu().numpy()
     return float(l1.item() + tv.item()), canon, {k: v.cpu().numpy() for k, v in ft.items()}
 
 
@@ -273,9 +274,75 @@ def test_backward_edge_cases():
             assert _rel(v.cpu().numpy(), ref[k]) <= TOL, (t, k)
 
 
+@pytest.mark.parametrize("deg,colour,opacity", [(1, True, True), (3, True, False), (0, False, True),
+                                                (3, True, True)])
+def test_deform_backward_colour_heads_match_oracle(deg, colour, opacity):
+    """The P:1232 decoders phi_C / phi_alpha in the deformation backward: dL/dC', dL/dlogit' in, their
+    w_c, b_c, w_a, b_a gradients, the pass-through to the canonical SH / logits, and the decoders' share
+    of dL/df_d (hence of every plane and w_d, b_d), against the autograd oracle."""
+    import torch
+
+    from oracle import backward as B
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = with_colour_heads(_scene(n=300, deg=deg, seed=6, heads=0.4), 0.2, 0.3, colour=colour, opacity=opacity)
+    ds = fgs.DeviceScene(s)
+    t = float(s.times[1])
+    rng = np.random.default_rng(11)
+    up = {"means": rng.normal(size=(s.n, 3)), "log_scales": rng.normal(size=(s.n, 3)),
+          "quats": rng.normal(size=(s.n, 4))}
+    if colour:
+        up["sh"] = rng.normal(size=s.sh.shape)
+    if opacity:
+        up["opacity_logits"] = rng.normal(size=(s.n,))
+    up = {k: v.astype(np.float32) for k, v in up.items()}
+    dd, dt = ds.alloc_gaussian_grads()
+    for k, v in up.items():
+        dt[k].copy_(torch.from_numpy(v))
+    dc, ct = ds.alloc_gaussian_grads()
+    df, ft = ds.alloc_field_grads()
+    assert ("w_c" in ft) == colour and ("w_a" in ft) == opacity
+    scratch = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device="cuda")
+    fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dd, dc, df, scratch)
+    torch.cuda.synchronize()
+    ref = B.deform_grads_ref(s, t, up)
+    keys = ["means", "log_scales", "quats"] + (["sh"] if colour else []) + (["opacity_logits"] if opacity else [])
+    for k in keys:
+        err = _rel(ct[k].cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+    if colour:     # the pass-through is exact
+        assert np.array_equal(ct["sh"].cpu().numpy(), up["sh"])
+    if not opacity:
+        assert not ct["opacity_logits"].any()        # untouched
+    for k, v in ft.items():
+        assert np.any(ref[k] != 0), k
+        err = _rel(v.cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+
+
+def test_full_frame_gradients_with_colour_heads():
+    """The whole chain of test_full_frame_gradients_match_oracle with both P:1232 decoders: the render
+    backward's SH / opacity gradients feed the deformation backward."""
+    import torch
+
+    from oracle import backward as B
+    from paper_2310_08528_b200.inputs import with_colour_heads
+    s = with_colour_heads(_scene(n=60, W=40, H=32, deg=1, seed=4), 0.05, 0.1)
+    ds = fgs.DeviceScene(s)
+    frame = 1
+    cam = s.cameras[frame]
+    target = np.random.default_rng(2).uniform(size=(3, cam.height, cam.width)).astype(np.float32)
+    L, canon, field = _train_frame(ds, s, frame, torch.from_numpy(target).cuda(), 0.05)
+    ref, Lref, _ = B.grads_ref(s, frame, target, 0.05)
+    assert abs(L - Lref) <= 1e-4 * abs(Lref)
+    assert set(field) >= {"w_c", "b_c", "w_a", "b_a"}
+    for k, v in list(canon.items()) + list(field.items()):
+        err = _rel(v, ref[k])
+        assert err <= TOL, (k, err)
+
+
 def test_backward_rejects_bad_arguments():
-    """Synchronous validation (FGS_E_INVALID) of the training-side calls, and FGS_E_NOTIMPL for the
-    backward of the P:1232 colour / opacity decoders."""
+    """Synchronous validation (FGS_E_INVALID) of the training-side calls, incl. the P:1232 decoders'
+    gradient pointers."""
     import torch
 
     from paper_2310_08528_b200.inputs import with_colour_heads
@@ -293,9 +360,13 @@ def test_backward_rejects_bad_arguments():
     sc = with_colour_heads(s, 0.1, 0.1)
     dsc = fgs.DeviceScene(sc)
     big = torch.empty(fgs.fgs_deform_backward_scratch_bytes(dsc.field, dsc.mlp), dtype=torch.uint8, device="cuda")
+    df_no_heads = ds.alloc_field_grads()[0]          # no w_c / w_a gradient buffers
+    dfc = dsc.alloc_field_grads()[0]
+    dgc, _ = dsc.alloc_gaussian_grads()
+    fgs.fgs_deform_backward(dsc.g, dsc.field, dsc.mlp, 0.5, dgc, dgc, dfc, big)   # the valid call
     with pytest.raises(fgs.FgsError) as e:
-        fgs.fgs_deform_backward(dsc.g, dsc.field, dsc.mlp, 0.5, dg, dg, dsc.alloc_field_grads()[0], big)
-    assert e.value.code == fgs.FGS_E_NOTIMPL
+        fgs.fgs_deform_backward(dsc.g, dsc.field, dsc.mlp, 0.5, dgc, dgc, df_no_heads, big)
+    assert e.value.code == fgs.FGS_E_INVALID
 
 
 def test_adam_matches_oracle():
@@ -316,7 +387,8 @@ def test_adam_matches_oracle():
     assert np.max(np.abs(m.cpu().numpy() - mr)) <= 1e-5 * np.abs(mr).max()
 
 
-def test_training_steps_reduce_the_loss():
+@pytest.mark.parametrize("decoders", [False, True])
+def test_training_steps_reduce_the_loss(decoders):
     """The whole training side end to end on the GPU (paper's batch size 1): a scene whose means and
     opacities are perturbed from a ground truth is trained against the ground truth's renders with
     fgs_deform -> fgs_render -> fgs_l1_loss -> fgs_render_backward -> fgs_deform_backward -> fgs_adam_step;
@@ -326,6 +398,9 @@ def test_training_steps_reduce_the_loss():
     from paper_2310_08528_b200.train import Trainer
     truth = make_scene("dnerf", n=3000, width=96, height=72, n_frames=4, seed=6)
     truth = with_heads(truth, 0.1, seed=2)
+    if decoders:                                   # P:1232 phi_C / phi_alpha trained too
+        from paper_2310_08528_b200.inputs import with_colour_heads
+        truth = with_colour_heads(truth, 0.05, 0.05)
     dst = fgs.DeviceScene(truth)
     outs, _ = dst.alloc_deformed(4)
     targets = [torch.empty((3, 72, 96), device="cuda") for _ in range(4)]
