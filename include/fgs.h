@@ -136,6 +136,9 @@ typedef struct {
   uint32_t* binning_direct;     /* [2]          CTAs of the per-tile counting [0] and of the key
                                  * duplication [1] whose Gaussians' rect union exceeded the shared
                                  * aggregation box (FGS_TUNE_AGG_TILES) and went to direct global atomics */
+  uint32_t* long_sort_paths;    /* [3]          lists longer than the warp-sort cap sorted by the bucket
+                                 * pass with its scratch in shared memory [0] / in the inst2 scratch [1],
+                                 * and by the networks + merges (a bucket over kBucketMax: skewed depths) [2] */
 } fgs_render_aux;
 
 /* ---- deformation field F --------------------------------------------------
@@ -292,8 +295,8 @@ int64_t fgs_launch_count(void);
 
 /* ---- tuning (process-global; change only while no call of this library is enqueueing) --------
  * FGS_TUNE_TILE_SORT_CAP: tile lists of at most this many instances are sorted by (depth, index) by
- * one warp (registers + shared memory); longer lists by the persistent long-list CTA sort (shared-
- * memory segments, global-memory merge levels).  Both run in FGS_STAGE_TILE_SORT.
+ * one warp (registers + shared memory); longer lists by the persistent long-list CTA sort (see
+ * FGS_TUNE_LONG_SORT).  Both run in FGS_STAGE_TILE_SORT.
  * Range [1, 1024], default 1024.  Results are identical for every value (tests lower it to exercise
  * the long-list path).  fgs_set_tuning returns FGS_E_INVALID for an unknown key or a value out of
  * range; fgs_get_tuning returns -1 for an unknown key.
@@ -312,9 +315,14 @@ int64_t fgs_launch_count(void);
  * M / tiles reaches FGS_TUNE_RADIX_MIN_LIST (default 768; range [1, 2^20]), the per-tile sorts for the
  * others.  Default 0 (the per-tile sorts were faster at every measured N).  The order, hence every image,
  * is identical whichever path a frame takes.
+ * FGS_TUNE_LONG_SORT: how the long-list CTA sort orders a list.  1 (default) = one bucket pass: the
+ * instances bucketed by the top 11 bits of their depth key relative to the list's minimum, each then
+ * placed at its bucket's start + the number of its bucket's instances below it (a list with a bucket of
+ * more than 64 instances falls back to 0); 0 = CTA bitonic networks on 4096-instance segments + merge
+ * levels.  The order is identical either way (fgs_render_aux.long_sort_paths counts which ran).
  * (Key 1 is retired: there is a single deformation kernel.) */
 enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_BLEND_CULL = 2, FGS_TUNE_AGG_TILES = 3, FGS_TUNE_RADIX = 4,
-       FGS_TUNE_RADIX_MIN_LIST = 5 };
+       FGS_TUNE_RADIX_MIN_LIST = 5, FGS_TUNE_LONG_SORT = 6 };
 int fgs_set_tuning(int32_t key, int64_t value);
 int64_t fgs_get_tuning(int32_t key);
 

@@ -215,6 +215,7 @@ int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* 
   local.agg_tiles = agg_tiles();
   local.radix_mode = local.L.ntiles <= kRxMaxTiles ? radix_mode() : 0;
   local.radix_min_list = radix_min_list();
+  local.long_sort = long_sort();
   local.debug = aux != nullptr;
   local.blend_work = aux ? (unsigned long long*)aux->blend_work : nullptr;
   local.ws_stride = per;
@@ -332,12 +333,14 @@ std::atomic<int> g_blend_cull{1};
 std::atomic<int> g_agg_tiles{kAggTilesMax};
 std::atomic<int> g_radix_mode{0};
 std::atomic<int> g_radix_min_list{kRadixMinListDefault};
+std::atomic<int> g_long_sort{1};
 }
 int tile_sort_cap() { return g_tile_sort_cap.load(std::memory_order_relaxed); }
 int blend_cull() { return g_blend_cull.load(std::memory_order_relaxed); }
 int agg_tiles() { return g_agg_tiles.load(std::memory_order_relaxed); }
 int radix_mode() { return g_radix_mode.load(std::memory_order_relaxed); }
 int radix_min_list() { return g_radix_min_list.load(std::memory_order_relaxed); }
+int long_sort() { return g_long_sort.load(std::memory_order_relaxed); }
 
 }  // namespace fgs
 
@@ -496,6 +499,10 @@ int fgs_set_tuning(int32_t key, int64_t value) {
       FGS_CHECK(value >= 1 && value <= (1 << 20), "radix threshold must be in [1, 2^20]");
       g_radix_min_list.store((int)value);
       return FGS_OK;
+    case FGS_TUNE_LONG_SORT:
+      FGS_CHECK(value == 0 || value == 1, "long sort mode must be 0 or 1");
+      g_long_sort.store((int)value);
+      return FGS_OK;
     default:
       return fail(FGS_E_INVALID, "unknown tuning key");
   }
@@ -507,6 +514,7 @@ int64_t fgs_get_tuning(int32_t key) {
   if (key == FGS_TUNE_AGG_TILES) return agg_tiles();
   if (key == FGS_TUNE_RADIX) return radix_mode();
   if (key == FGS_TUNE_RADIX_MIN_LIST) return radix_min_list();
+  if (key == FGS_TUNE_LONG_SORT) return long_sort();
   return -1;
 }
 

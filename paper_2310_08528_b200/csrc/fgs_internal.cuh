@@ -84,6 +84,7 @@ struct RenderBatch {
   int agg_tiles;             // CTA binning aggregation limit in tiles (FGS_TUNE_AGG_TILES, <= 4096)
   int radix_mode;            // FGS_TUNE_RADIX: 0 per-tile sorts only, 1 auto, 2 radix path for every frame
   int radix_min_list;        // auto: a frame takes the radix path when M >= radix_min_list x tiles
+  int long_sort;             // FGS_TUNE_LONG_SORT: 1 bucket pass for long lists, 0 networks + merges
   char* ws;                  // frame f slice = ws + f * ws_stride
   size_t ws_stride;
   WsLayout L;
@@ -169,6 +170,7 @@ int blend_cull();
 int agg_tiles();
 int radix_mode();
 int radix_min_list();
+int long_sort();
 constexpr int kAggTilesMax = 4096;           // shared histogram of the CTA binning aggregation
 constexpr int kRadixMinListDefault = 768;    // FGS_TUNE_RADIX_MIN_LIST default (mean list length)
 

@@ -61,7 +61,7 @@ class fgs_render_aux(ctypes.Structure):
     _fields_ = [(k, c_void_p) for k in ("radii", "rect", "mean2d", "depth_key", "tiles_touched",
                                         "n_instances", "sorted_tile", "sorted_gid", "ranges",
                                         "final_T", "n_contrib", "n_evaluated", "blend_work",
-                                        "binning_direct")]
+                                        "binning_direct", "long_sort_paths")]
 
 
 class fgs_gaussian_grads(ctypes.Structure):
@@ -89,6 +89,7 @@ FGS_TUNE_BLEND_CULL = 2
 FGS_TUNE_AGG_TILES = 3
 FGS_TUNE_RADIX = 4
 FGS_TUNE_RADIX_MIN_LIST = 5
+FGS_TUNE_LONG_SORT = 6
 
 
 def lib():

@@ -49,6 +49,7 @@ def gpu_render_debug(ds, cam, dstruct, max_instances=None):
         "n_evaluated": torch.zeros((H, W), dtype=torch.int32, device=dev),
         "blend_work": torch.zeros(2, dtype=torch.int64, device=dev),
         "binning_direct": torch.zeros(2, dtype=torch.int32, device=dev),
+        "long_sort_paths": torch.zeros(3, dtype=torch.int32, device=dev),
     }
     aux = fgs.fgs_render_aux(**{k: v.data_ptr() for k, v in t.items()})
     image = torch.full((3, H, W), float("nan"), dtype=torch.float32, device=dev)

@@ -74,7 +74,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(fgs.fgs_gaussians) == 8 + 8 + 5 * 8
     assert ctypes.sizeof(fgs.fgs_camera) == 4 * (9 + 3 + 4 + 2 + 3)
     assert fgs.fgs_hexplanes.planes.offset == 56
-    assert ctypes.sizeof(fgs.fgs_render_aux) == 14 * 8
+    assert ctypes.sizeof(fgs.fgs_render_aux) == 15 * 8
     assert ctypes.sizeof(fgs.fgs_mlp) == 8 + 12 * 8
 
 
@@ -105,6 +105,11 @@ def test_tuning_knob_host_only(L):
         assert fgs.fgs_get_tuning(fgs.FGS_TUNE_RADIX) == 2
     assert L.fgs_set_tuning(fgs.FGS_TUNE_RADIX, 3) == fgs.FGS_E_INVALID
     assert L.fgs_set_tuning(fgs.FGS_TUNE_RADIX_MIN_LIST, 0) == fgs.FGS_E_INVALID
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_LONG_SORT) == 1
+    with fgs.tuning(fgs.FGS_TUNE_LONG_SORT, 0):
+        assert fgs.fgs_get_tuning(fgs.FGS_TUNE_LONG_SORT) == 0
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_LONG_SORT) == 1
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_LONG_SORT, 2) == fgs.FGS_E_INVALID
 
 
 def test_stage_names_match_header():

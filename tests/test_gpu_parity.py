@@ -291,6 +291,41 @@ def test_long_lists_multi_run_merge(ties, radix):
     assert pix["psnr"] >= PSNR_MIN and pix["max_unflagged"] <= PIX_TOL, pix
 
 
+@pytest.mark.parametrize("case", ["smem", "global", "skewed"])
+def test_long_sort_bucket_pass_paths(case):
+    """The long-list sort's bucket pass (FGS_TUNE_LONG_SORT = 1, the default) against the networks +
+    merges (0) and the oracle's (tile, depth, index) lists, on each of its paths, asserted through
+    fgs_render_aux.long_sort_paths: scratch in shared memory (lists of 1025..8192), in the inst2 scratch
+    (lists over 8192), and the fallback to the networks when a bucket holds more than 64 instances
+    (hundreds of Gaussians at one bit-identical depth: exact ties, ordered by index)."""
+    W = 16 if case == "global" else 32                          # one 16x16 tile: every kept Gaussian in one list
+    s = make_scene("tiny", n={"smem": 3000, "global": 9500, "skewed": 3000}[case], width=W, height=W)
+    if case == "skewed":
+        s = with_heads(s, 0.0)                                  # zero heads: means as given
+        s.means[:400] = s.means[1000]
+    ds = _ds(s)
+    dstruct, g, _ = gpu_deform(ds, float(s.times[0]))
+    res = {}
+    for mode in (1, 0):
+        with fgs.tuning(fgs.FGS_TUNE_LONG_SORT, mode):
+            res[mode] = gpu_render_debug(ds, s.cameras[0], dstruct)
+    lengths = np.diff(res[1]["ranges"], axis=1)
+    paths = res[1]["long_sort_paths"].tolist()
+    assert lengths.max() > 1024
+    if case == "smem":
+        assert lengths.max() <= 8192 and paths[0] > 0 and paths[2] == 0, paths
+    elif case == "global":
+        assert lengths.max() > 8192 and paths[1] > 0 and paths[2] == 0, paths
+    else:
+        assert paths[2] > 0, paths
+    assert res[0]["long_sort_paths"].tolist()[:2] == [0, 0]
+    for k in ("sorted_gid", "sorted_tile", "ranges", "image", "final_T", "n_contrib"):
+        assert np.array_equal(res[0][k], res[1][k]), k
+    ref = OR.render_ref(g, s.opacity_logits, s.sh, s.sh_degree, s.cameras[0])
+    ints = compare_integer_work(res[1], ref["pre"], (ref["tiles"], ref["gids"], ref["ranges"]))
+    assert ints["tile_lists"] == 0 and ints["rect"] == 0, ints
+
+
 def test_sharded_frames_single_rank_equals_fgs_frames():
     """(e2) pipeline (sharding.sharded_frames) at world size 1: deform via fgs_deform_range into the
     gather buffers + render per time gives the same images as fgs_frames."""
