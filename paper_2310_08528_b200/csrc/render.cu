@@ -965,10 +965,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// thr: the exponent threshold of the alpha >= 1/255 test while the pixel is live, +inf once it has
+// stopped (or lies outside the image) — one compare then covers both "live" and "alpha >= 1/255"
+// (no separate done flag to test and update per evaluation)
 struct PixelState {
-  float T, c0, c1, c2;
-  bool done;
+  float T, c0, c1, c2, thr;
   uint32_t ncon, nev;
+  __device__ __forceinline__ bool done() const { return thr == __int_as_float(0x7f800000); }
 };
 
 // Eq. 4 for one pixel and one Gaussian; e = p2 + log2(o) with p2 = power * log2(e) (R9: skip if
@@ -985,7 +988,7 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
                                            uint32_t pos) {
   (void)lo;
   const float alpha = fminf(kAlphaMax, ex2_approx(e));
-  const bool ok = !s.done && e >= kLog2AlphaMin;
+  const bool ok = e >= s.thr;              // live and alpha >= 1/255 (s.thr = kLog2AlphaMin or +inf)
   const float test_T = fmaf(-alpha, s.T, s.T);
   const bool stop = ok && test_T < kTMin;
   if (ok && !stop) {
@@ -996,10 +999,8 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
     s.T = test_T;
     if (DBG) s.ncon += 1u;
   }
-  if (stop) {
-    s.done = true;
-    if (DBG) s.nev = pos;
-  }
+  s.thr = stop ? __int_as_float(0x7f800000) : s.thr;
+  if (DBG && stop) s.nev = pos;
 }
 
 // Conservative ellipse-vs-box cull: a half-box is skipped only if q2(d) = qa dx^2 + qb dx dy + qc dy^2
@@ -1065,12 +1066,12 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
 #pragma unroll
   for (int k = 0; k < kBlendPix; ++k) {
     const bool in = pxi < b.width && py0 + 4 * k < b.height;
-    P[k] = PixelState{1.f, 0.f, 0.f, 0.f, !in, 0u, (uint32_t)L};
+    P[k] = PixelState{1.f, 0.f, 0.f, 0.f, in ? kLog2AlphaMin : __int_as_float(0x7f800000), 0u, (uint32_t)L};
   }
   auto all_done = [&]() {
     bool d = true;
 #pragma unroll
-    for (int k = 0; k < kBlendPix; ++k) d = d && P[k].done;
+    for (int k = 0; k < kBlendPix; ++k) d = d && P[k].done();
     return d;
   };
   for (int start = 0; start < L; start += BATCH) {
@@ -1097,7 +1098,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
       uint32_t live = 0;
 #pragma unroll
       for (int k = 0; k < kBlendPix; ++k)
-        if (__any_sync(0xffffffffu, !P[k].done)) live |= 1u << k;
+        if (__any_sync(0xffffffffu, !P[k].done())) live |= 1u << k;
       if (!live) break;
       const int jt = c0 + lane;
       uint32_t need = 0;
@@ -1111,18 +1112,25 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
       uint32_t mk[kBlendPix];
 #pragma unroll
       for (int k = 0; k < kBlendPix; ++k) mk[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+      // walked from the most significant bit of the bit-reversed masks (= list order): the next
+      // Gaussian is one FLO, its bit one shift, clearing it one XOR
       uint32_t m = 0;
 #pragma unroll
-      for (int k = 0; k < kBlendPix; ++k) m |= mk[k];
+      for (int k = 0; k < kBlendPix; ++k) {
+        m |= mk[k];
+        mk[k] = __brev(mk[k]);
+      }
+      m = __brev(m);
       if (DBG) {
         n_tested += (uint32_t)min(32, cnt - c0);
 #pragma unroll
         for (int k = 0; k < kBlendPix; ++k) n_evald += __popc(mk[k]);
       }
       while (m) {
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        const int j = c0 + bit;
+        const int h = 31 - __clz(m);
+        const uint32_t hb = 1u << h;
+        m ^= hb;
+        const int j = c0 + 31 - h;
         const float4 a = srec[j].a, q = srec[j].q;
         const float bch = srec[j].c.x;
         const float dx = a.x - lx;
@@ -1132,7 +1140,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         const uint32_t pos = (uint32_t)(start + j + 1);
 #pragma unroll
         for (int k = 0; k < kBlendPix; ++k) {
-          if ((mk[k] >> bit) & 1u) {
+          if (mk[k] & hb) {
             const float dy = dy0 - 4.f * k;
             const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
             blend_step<DBG>(P[k], e, q.y, q.z, q.w, bch, pos);
