@@ -24,6 +24,7 @@
 // FGS_EXP_NOSTAGE (no time-line staging), FGS_EXP_NOLINE (no line reads), FGS_EXP_NOMMA (no MMAs),
 // FGS_EXP_NOEPI (epilogue releases D without the heads) — each removes one part of the schedule so its
 // share of the kernel time can be measured; results are wrong under any of them.
+// FGS_EXP_TRACE records a per-warp clock64 timeline of CTA 0 (results unchanged; tools/deform_trace.py).
 #include <cuda_runtime.h>
 #include <limits.h>
 
@@ -37,6 +38,20 @@ namespace fgs {
 namespace {
 
 constexpr int kM = 128;
+
+// FGS_EXP_TRACE (experiment builds only): lane 0 of every warp of CTA 0 records (tag, clock64) events
+// into g_trace[warp]; fgs_exp_trace copies them out (tools/deform_trace.py prints the role timeline)
+#ifdef FGS_EXP_TRACE
+constexpr int kTraceN = 2048;
+__device__ unsigned long long g_trace[24][kTraceN];
+#define FGS_TR(tag)                                                                                       \
+  do {                                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_n < kTraceN)                                     \
+      g_trace[threadIdx.x >> 5][tr_n++] = ((unsigned long long)(tag) << 56) | (clock64() & 0xFFFFFFFFFFFFFFull); \
+  } while (0)
+#else
+#define FGS_TR(tag) do {} while (0)
+#endif
 constexpr int kTmemCols = 512;
 constexpr int kMaxG = 16;
 // Shared buffer of the per-frame time lines: only the knot window each axis of a group touches is
@@ -239,6 +254,11 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef FGS_EXP_TRACE
+  int tr_n = 0;
+  if (blockIdx.x == 0 && lane == 0)
+    for (int k = 0; k < kTraceN; ++k) g_trace[warp][k] = 0;
+#endif
 
   // ---- setup (all threads) ----
   for (int i = tid; i < WIDTH * KP; i += kThreads) {
@@ -336,6 +356,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
     uint32_t it = 0;   // tile-frame counter
     for (int gstart = t_beg; gstart < t_end; gstart += G) {
       const int ng = min(G, t_end - gstart);
+      FGS_TR(1);   // group start
       // ---- group prologue: grid coordinates (smem), knot windows, spatial products S (TMEM) ----
       prod_sync<kProdThreads>();     // previous group's line / U readers are done
       if (tid < FGS_MAX_SCALES * 3) { win[2 * tid] = INT_MAX; win[2 * tid + 1] = INT_MIN; }
@@ -441,6 +462,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         }
       }
       tc::tmem_st_wait();
+      FGS_TR(2);   // spatial products stored
       // ---- compact layout of the group's knot windows in the line buffer (or the L2 path) ----
       prod_sync<kProdThreads>();     // windows complete
       if (tid == 0) {
@@ -463,6 +485,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
         const float ft = gt_ - (float)j0;
         // ---- stage the temporal lines at t over the group's knot windows (time lerp of 2 rows) ----
         prod_sync<kProdThreads>();   // U/win visible; previous frame's line readers done
+        FGS_TR(3);   // staging start
 #ifdef FGS_EXP_NOSTAGE
         if (false) {
 #else
@@ -491,7 +514,9 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             }
           }
         }
+        FGS_TR(4);   // staging issued
         prod_sync<kProdThreads>();
+        FGS_TR(5);   // staging complete (all producers)
         for (int gt = 0; gt < ng; ++gt) {
           if (!in_range(gstart + gt, f)) continue;
           const uint32_t itc = it++;
@@ -542,9 +567,11 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
               for (int e = 0; e < 4; ++e) tc::tf32_split(fh[e], hi[l][4 * qq + e], lo[l][4 * qq + e]);
             }
           }
+          FGS_TR(6);   // A values computed
           // A is single-buffered: wait until the MMAs of tile-frame it-1 have read it
           if (itc > 0) tc::mbar_wait(a_free, (itc - 1) & 1u);
           tc::fence_after_sync();
+          FGS_TR(7);   // A free
 #pragma unroll
           for (int l = 0; l < MAXS; ++l) {
             if (l >= NS) break;
@@ -555,6 +582,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) mbar_arrive(a_full);
+          FGS_TR(8);   // A stored + arrived
         }
       }
     }
@@ -571,9 +599,12 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             if (!in_range(gstart + gt, f)) continue;
             const uint32_t itc = it++;
             const uint32_t buf = itc & 1u;
+            FGS_TR(10);
             tc::mbar_wait(a_full, itc & 1u);
+            FGS_TR(11);   // A full
             if (itc >= 2) tc::mbar_wait(d_free + buf, ((itc >> 1) - 1) & 1u);
             tc::fence_after_sync();
+            FGS_TR(12);   // D free
             const uint32_t d = tmem + buf * DW;
 #ifndef FGS_EXP_NOMMA
             for (int s = 0; s < KP / 8; ++s) {
@@ -587,6 +618,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
 #endif
             tc::mma_commit(a_free);
             tc::mma_commit(d_full + buf);
+            FGS_TR(13);   // MMAs issued
           }
         }
       }
@@ -619,8 +651,10 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
             for (int c = 0; c < 3; ++c) cx[7 + c] = __ldg(p.log_scales + g * 3 + c);
           }
           const uint32_t buf = itc & 1u;
+          FGS_TR(20);
           tc::mbar_wait(d_full + buf, (itc >> 1) & 1u);
           tc::fence_after_sync();
+          FGS_TR(21);   // D full
 #ifdef FGS_EXP_NOEPI
           tc::fence_before_sync();
           __syncwarp();
@@ -693,6 +727,7 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
               for (int c = 0; c < 3; ++c) os[c] = ho[7 + c];
             }
           }
+          FGS_TR(22);   // rows stored
         }
       }
     }
@@ -760,3 +795,9 @@ cudaError_t launch_deform_tc3(const DeformBatch& p, cudaStream_t s) {
 }
 
 }  // namespace fgs
+
+#ifdef FGS_EXP_TRACE
+extern "C" int fgs_exp_trace(void* dst) {   // 24 x kTraceN x 8 bytes of CTA 0's events
+  return (int)cudaMemcpyFromSymbol(dst, fgs::g_trace, sizeof(fgs::g_trace));
+}
+#endif
