@@ -6,11 +6,13 @@
 // Kernels:
 //   l1_kernel / tv_kernel      loss value (block partials in fp64, summed in a fixed order by
 //                              loss_finish_kernel) and its gradient, elementwise (B1, B2).
-//   blend_backward_kernel      one CTA per 16x16 tile: every pixel re-walks its list front to back with
-//                              the forward's own fp32 arithmetic (same e, alpha, T, hence the same skip /
-//                              stop decisions), and for each contributing Gaussian forms the 9 partials
-//                              dL/d(mean2d, log2-domain conic, log2 opacity, rgb); warp butterflies and a
-//                              fixed-order sum over the CTA's warps reduce them per (tile, Gaussian), and
+//   blend_backward_kernel      one CTA per 16x16 tile in the forward blend's layout (2 warps, 4 pixels
+//                              per lane, the same sub-box cull): every pixel re-walks its list front to
+//                              back with the forward's own fp32 arithmetic (same e, alpha, T, hence the
+//                              same skip / stop decisions), and for each contributing Gaussian forms the 9
+//                              partials dL/d(mean2d, log2-domain conic, log2 opacity, rgb); a lane's pixels,
+//                              a warp butterfly and a fixed-order sum over the 2 warps reduce them per
+//                              (tile, Gaussian), and
 //                              one fixed-point atomic per component adds them into the Gaussian's
 //                              accumulator.  Integer (2^-40) accumulation is associative: the result is
 //                              bit-identical for every launch order (SPEC S:173 determinism).
@@ -134,9 +136,18 @@ __global__ void loss_finish_kernel(const double* __restrict__ partials, int n, f
 }
 
 // ------------------------------------------------------------------ splat backward
-constexpr int kBwdBatch = 32;
-constexpr int kBwdThreads = 256;
-constexpr int kBwdWarps = kBwdThreads / 32;
+// The forward blend's layout (render.cu blend_kernel): one CTA of kBwdWarps = 2 warps per 16x16 tile,
+// warp w owns the 8-wide column block x in [8w, 8w+8) of all 16 rows, lane l owns the kBwdPix = 4 pixels
+// (8w + (l & 7), (l >> 3) + 4k), k = 0..3 (sub-box k = rows [4k, 4k+4) of the block).  Records are staged
+// kBwdBatch at a time; per 32 of them each lane tests one against the warp's 4 sub-boxes with the
+// forward's conservative ellipse-vs-box bound (subboxes_may_reach) and the warp walks, in list order,
+// each Gaussian some live sub-box may reach, evaluating it on those sub-boxes.  A lane first sums the 9
+// partials of its own pixels (k ascending), then one transposing warp butterfly per (Gaussian, warp)
+// and a fixed-order sum over the 2 warps form the tile's contribution.
+constexpr int kBwdPix = 4;
+constexpr int kBwdWarps = 2;
+constexpr int kBwdThreads = 32 * kBwdWarps;
+constexpr int kBwdBatch = 128;
 constexpr int kNPart = 9;   // d mean2d.x, .y, a2, b2, c2, log2 o, r, g, b
 
 struct BwdArgs {
@@ -146,158 +157,195 @@ struct BwdArgs {
   unsigned long long* acc;          // [n][9] fixed-point accumulators
 };
 
+// One pixel's backward state: the forward's T and prefix colour, dL/dI of the pixel and its final colour.
+struct BwdPixel {
+  float T, pc0, pc1, pc2, g0, g1, g2, C0, C1, C2;
+  bool done;
+};
+
 __global__ void __launch_bounds__(kBwdThreads) blend_backward_kernel(const __grid_constant__ BwdArgs A) {
   const RenderBatch& b = A.b;
   const int tile = blockIdx.x;
   const int tx = tile % b.gx, ty = tile / b.gx;
-  const int lx = threadIdx.x & 15, ly16 = threadIdx.x >> 4;      // pixel (lx, ly16) of the tile
-  const int px = tx * kTile + lx, py = ty * kTile + ly16;
-  const bool inside = px < b.width && py < b.height;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bx0 = warp * 8;
+  const int lxi = bx0 + (lane & 7), lyi = lane >> 3;
+  const int px = tx * kTile + lxi, py0 = ty * kTile + lyi;
   const uint2 rg = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.ranges)[tile];
   const int L = (int)(rg.y - rg.x);
   const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, 0, b.L.inst) + rg.x;
   const float4* rec = ws_ptr<float4>(b.ws, b.ws_stride, 0, b.L.rec);
-  __shared__ float4 s_a[kBwdBatch], s_q[kBwdBatch];
-  __shared__ float s_c[kBwdBatch], s_thr[kBwdBatch];
-  __shared__ uint32_t s_gid[kBwdBatch];
+  struct __align__(16) SRec { float4 a, q; float2 c; float thr; uint32_t gid; };
+  __shared__ SRec srec[kBwdBatch];
   __shared__ float s_red[kBwdWarps][kBwdBatch][kNPart];
-  // the forward's per-pixel arithmetic: dx = mean_rel.x - x, dy = (mean_rel.y - (y & 3)) - 4 (y >> 2)
-  const float fx_ = (float)lx, fy_ = (float)(ly16 & 3), fk4 = 4.f * (float)(ly16 >> 2);
-  float T = 1.f, pc0 = 0.f, pc1 = 0.f, pc2 = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  bool done = !inside;
-  if (inside) {
-    const size_t hw = (size_t)b.width * b.height, pix = (size_t)py * b.width + px;
-    C0 = A.image[pix]; C1 = A.image[hw + pix]; C2 = A.image[2 * hw + pix];
-    g0 = A.dimg[pix]; g1 = A.dimg[hw + pix]; g2 = A.dimg[2 * hw + pix];
+  __shared__ uint32_t s_wrote[kBwdWarps][kBwdBatch / 32];   // rows of s_red a warp wrote this batch
+  // the forward's per-pixel arithmetic: dx = mean_rel.x - x, dy = (mean_rel.y - (y & 3)) - 4 k
+  const float lx = (float)lxi, ly = (float)lyi;
+  const float bxl = (float)bx0, bxh = (float)(bx0 + 7);
+  BwdPixel P[kBwdPix];
+  const size_t hw = (size_t)b.width * b.height;
+#pragma unroll
+  for (int k = 0; k < kBwdPix; ++k) {
+    BwdPixel& q = P[k];
+    const int py = py0 + 4 * k;
+    q.T = 1.f; q.pc0 = q.pc1 = q.pc2 = 0.f;
+    q.g0 = q.g1 = q.g2 = q.C0 = q.C1 = q.C2 = 0.f;
+    q.done = !(px < b.width && py < b.height);
+    if (!q.done) {
+      const size_t pix = (size_t)py * b.width + px;
+      q.C0 = A.image[pix]; q.C1 = A.image[hw + pix]; q.C2 = A.image[2 * hw + pix];
+      q.g0 = A.dimg[pix]; q.g1 = A.dimg[hw + pix]; q.g2 = A.dimg[2 * hw + pix];
+    }
   }
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   for (int start = 0; start < L; start += kBwdBatch) {
-    if (__syncthreads_count(done) == kBwdThreads) break;
-    if (threadIdx.x < kBwdBatch && start + (int)threadIdx.x < L) {
-      const uint32_t g = (uint32_t)inst[start + threadIdx.x];
-      float4 a = rec[3 * g + 0];
-      const float4 c = rec[3 * g + 2];
-      a.x = (a.x - tx0) + c.y;        // tile-relative mean, exactly as the forward stages it
-      a.y = (a.y - ty0) + c.z;
-      s_a[threadIdx.x] = a;
-      s_q[threadIdx.x] = rec[3 * g + 1];
-      s_c[threadIdx.x] = c.x;
-      s_thr[threadIdx.x] = c.w;       // the forward's ellipse-cull threshold (preprocess record)
-      s_gid[threadIdx.x] = g;
+    bool all = true;
+#pragma unroll
+    for (int k = 0; k < kBwdPix; ++k) all = all && P[k].done;
+    if (__syncthreads_count(all) == kBwdThreads) break;
+#pragma unroll
+    for (int r = 0; r < kBwdBatch / kBwdThreads; ++r) {
+      const int idx = start + (int)threadIdx.x + kBwdThreads * r;
+      if (idx < L) {
+        const uint32_t g = (uint32_t)inst[idx];
+        float4 a = rec[3 * g + 0];
+        const float4 c = rec[3 * g + 2];
+        a.x = (a.x - tx0) + c.y;        // tile-relative mean, exactly as the forward stages it
+        a.y = (a.y - ty0) + c.z;
+        SRec& d = srec[threadIdx.x + kBwdThreads * r];
+        d.a = a;
+        d.q = rec[3 * g + 1];
+        d.c = make_float2(c.x, 0.f);
+        d.thr = c.w;                    // the forward's ellipse-cull threshold (preprocess record)
+        d.gid = g;
+      }
     }
-    // every (warp, Gaussian) row of the reduction buffer starts at zero: a warp writes only the rows of
-    // the Gaussians its cull keeps
-    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * kNPart; e += kBwdThreads) (&s_red[0][0][0])[e] = 0.f;
     __syncthreads();
     const int cnt = min(kBwdBatch, L - start);
-    // warp cull (the forward blend's conservative ellipse-vs-box bound, face_min): lane j tests Gaussian j
-    // against the warp's 16 x 2 pixel box; a Gaussian whose alpha < 1/255 on the whole box changes no
-    // pixel of it and gets no gradient from it, so skipping it is exact
-    uint32_t m = 0;
-    {
-      bool need = false;
-      if (lane < cnt) {
-        const float4 a = s_a[lane];
-        const float qa = -a.z, qb = -a.w, qc = -s_q[lane].x, thr = s_thr[lane];
-        const float xl = 0.f - a.x, xh = 15.f - a.x;
-        const float yl = (float)(2 * warp) - a.y, yh = yl + 1.f;
-        const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
-        const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
-        need = face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr;
-      }
-      m = __ballot_sync(0xffffffffu, need);
-      if (!__any_sync(0xffffffffu, !done)) m = 0;
-    }
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      float part[kNPart];
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      uint32_t live = 0;
 #pragma unroll
-      for (int k = 0; k < kNPart; ++k) part[k] = 0.f;
-      bool contrib = false;
-      if (!done) {
-        const float4 a = s_a[j], q = s_q[j];
-        const float bch = s_c[j];
-        const float dx = a.x - fx_;
-        const float bdx = a.w * dx;
-        const float base = fmaf(a.z * dx, dx, q.y);
-        const float dy = (a.y - fy_) - fk4;
-        const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
-        const float ex = ex2_approx_b(e);
-        const float alpha = fminf(kAlphaMaxB, ex);
-        if (e >= kLog2AlphaMinB) {
-          const float test_T = fmaf(-alpha, T, T);
-          if (test_T < kTMinB) {
-            done = true;
-          } else {
+      for (int k = 0; k < kBwdPix; ++k)
+        if (__any_sync(0xffffffffu, !P[k].done)) live |= 1u << k;
+      uint32_t wrote = 0;
+      if (live) {
+        const int jt = c0 + lane;
+        uint32_t need = 0;
+        if (jt < cnt) {
+          // a Gaussian whose alpha < 1/255 on a whole sub-box changes no pixel of it and gets no gradient
+          // from it, so skipping it there is exact
+          const float4 a = srec[jt].a;
+          need = subboxes_may_reach<kBwdPix>(-a.z, -a.w, -srec[jt].q.x, srec[jt].thr, bxl - a.x, bxh - a.x, -a.y) &
+                 live;
+        }
+        uint32_t mk[kBwdPix], m = 0;
+#pragma unroll
+        for (int k = 0; k < kBwdPix; ++k) {
+          mk[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+          m |= mk[k];
+        }
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          m &= m - 1;
+          const int j = c0 + bit;
+          const float4 a = srec[j].a, q = srec[j].q;
+          const float bch = srec[j].c.x;
+          const float dx = a.x - lx;
+          const float bdx = a.w * dx;
+          const float base = fmaf(a.z * dx, dx, q.y);
+          const float dy0 = a.y - ly;
+          float part[kNPart];
+#pragma unroll
+          for (int i = 0; i < kNPart; ++i) part[i] = 0.f;
+          bool contrib = false;
+#pragma unroll
+          for (int k = 0; k < kBwdPix; ++k) {
+            if (!((mk[k] >> bit) & 1u)) continue;
+            BwdPixel& s = P[k];
+            if (s.done) continue;
+            const float dy = dy0 - 4.f * k;
+            const float e = fmaf(dy, fmaf(q.x, dy, bdx), base);
+            const float ex = ex2_approx_b(e);
+            const float alpha = fminf(kAlphaMaxB, ex);
+            if (!(e >= kLog2AlphaMinB)) continue;
+            const float test_T = fmaf(-alpha, s.T, s.T);
+            if (test_T < kTMinB) {
+              s.done = true;
+              continue;
+            }
             contrib = true;
-            const float w = alpha * T;
-            pc0 = fmaf(q.z, w, pc0);
-            pc1 = fmaf(q.w, w, pc1);
-            pc2 = fmaf(bch, w, pc2);
+            const float w = alpha * s.T;
+            s.pc0 = fmaf(q.z, w, s.pc0);
+            s.pc1 = fmaf(q.w, w, s.pc1);
+            s.pc2 = fmaf(bch, w, s.pc2);
             // suffix after this Gaussian: S = C_pixel - prefix (incl. this one); dC/dalpha = c T - S / (1 - alpha)
             const float inv1ma = 1.f / (1.f - alpha);
-            const float dA = g0 * (q.z * T - (C0 - pc0) * inv1ma) + g1 * (q.w * T - (C1 - pc1) * inv1ma)
-                             + g2 * (bch * T - (C2 - pc2) * inv1ma);
-            part[6] = g0 * w;
-            part[7] = g1 * w;
-            part[8] = g2 * w;
+            const float dA = s.g0 * (q.z * s.T - (s.C0 - s.pc0) * inv1ma) + s.g1 * (q.w * s.T - (s.C1 - s.pc1) * inv1ma)
+                             + s.g2 * (bch * s.T - (s.C2 - s.pc2) * inv1ma);
+            part[6] += s.g0 * w;
+            part[7] += s.g1 * w;
+            part[8] += s.g2 * w;
             if (ex < kAlphaMaxB) {          // alpha = 2^e unclamped: dalpha/de = alpha ln 2
               const float dE = dA * alpha * (float)kLn2;
-              part[0] = dE * (2.f * a.z * dx + a.w * dy);       // de / d mean.x (dx = mean - pixel)
-              part[1] = dE * (a.w * dx + 2.f * q.x * dy);       // de / d mean.y
-              part[2] = dE * dx * dx;                           // de / d a2
-              part[3] = dE * dx * dy;                           // de / d b2
-              part[4] = dE * dy * dy;                           // de / d c2
-              part[5] = dE;                                     // de / d log2 o
+              part[0] += dE * (2.f * a.z * dx + a.w * dy);       // de / d mean.x (dx = mean - pixel)
+              part[1] += dE * (a.w * dx + 2.f * q.x * dy);       // de / d mean.y
+              part[2] += dE * dx * dx;                           // de / d a2
+              part[3] += dE * dx * dy;                           // de / d b2
+              part[4] += dE * dy * dy;                           // de / d c2
+              part[5] += dE;                                     // de / d log2 o
             }
-            T = test_T;
+            s.T = test_T;
+          }
+          if (__any_sync(0xffffffffu, contrib)) {
+            // warp sums of the 9 partials, fixed order (deterministic): partials 0-7 by a transposing
+            // butterfly (each exchange step halves the values a lane keeps: 4 + 2 + 1 + 1 + 1 shuffles,
+            // lane l ends with the sum of partial ((l >> 2) & 7) in bit-reversed order), partial 8 by a
+            // plain one
+            float h4[4], h2[2], h1;
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float send = b4 ? part[i] : part[i + 4];
+              const float keep = b4 ? part[i + 4] : part[i];
+              h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const float send = b3 ? h4[i] : h4[i + 2];
+              const float keep = b3 ? h4[i + 2] : h4[i];
+              h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            {
+              const float send = b2 ? h2[0] : h2[1];
+              const float keep = b2 ? h2[1] : h2[0];
+              h1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+            h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+            float p8 = part[8];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) p8 += __shfl_xor_sync(0xffffffffu, p8, o);
+            // lane l holds partial 4 b4 + 2 b3 + b2 (the halves kept at each step)
+            if ((lane & 3) == 0) s_red[warp][j][(b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0)] = h1;
+            if (lane == 0) s_red[warp][j][8] = p8;
+            wrote |= 1u << bit;
           }
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-        // warp sums of the 9 partials, fixed order (deterministic): partials 0-7 by a transposing
-        // butterfly (each exchange step halves the values a lane keeps: 4 + 2 + 1 + 1 + 1 shuffles, lane l
-        // ends with the sum of partial ((l >> 2) & 7) in bit-reversed order), partial 8 by a plain one
-        float h4[4], h2[2], h1;
-        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float send = b4 ? part[i] : part[i + 4];
-          const float keep = b4 ? part[i + 4] : part[i];
-          h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const float send = b3 ? h4[i] : h4[i + 2];
-          const float keep = b3 ? h4[i + 2] : h4[i];
-          h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-        {
-          const float send = b2 ? h2[0] : h2[1];
-          const float keep = b2 ? h2[1] : h2[0];
-          h1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-        float p8 = part[8];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p8 += __shfl_xor_sync(0xffffffffu, p8, o);
-        // lane l holds partial 4 b4 + 2 b3 + b2 (the halves kept at each step)
-        if ((lane & 3) == 0) s_red[warp][j][(b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0)] = h1;
-        if (lane == 0) s_red[warp][j][8] = p8;
-      }
+      if (lane == 0) s_wrote[warp][c0 >> 5] = wrote;
     }
     __syncthreads();
-    // per (Gaussian, component): the CTA's warps summed in warp order, one fixed-point atomic
+    // per (Gaussian, component): the tile's warps summed in warp order (rows a warp did not write count
+    // as 0), one fixed-point atomic (fix_add skips zeros)
     for (int idx = threadIdx.x; idx < cnt * kNPart; idx += kBwdThreads) {
       const int j = idx / kNPart, k = idx - j * kNPart;
-      double s = 0.0;
+      double sum = 0.0;
 #pragma unroll
-      for (int w = 0; w < kBwdWarps; ++w) s += (double)s_red[w][j][k];
-      fix_add(A.acc + (size_t)s_gid[j] * kNPart + k, s);
+      for (int w = 0; w < kBwdWarps; ++w)
+        if ((s_wrote[w][j >> 5] >> (j & 31)) & 1u) sum += (double)s_red[w][j][k];
+      fix_add(A.acc + (size_t)srec[j].gid * kNPart + k, sum);
     }
+    __syncthreads();
   }
 }
 

@@ -219,6 +219,23 @@ __device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx
   return q;
 }
 
+// All NP 8x4 sub-boxes of a warp's 8-wide column (rows y0 + 4k .. y0 + 4k + 3, k < NP) at once, with
+// the shared x-face and minimiser ratios: bit k set if the Gaussian's alpha may reach 1/255 somewhere in
+// sub-box k (face_min <= thr).  The forward blend and its backward re-walk cull with the same test.
+template <int NP>
+__device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
+                                                       float y0) {
+  const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
+  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
+  uint32_t need = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const float yl = y0 + 4.f * k, yh = yl + 3.f;
+    if (face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr) need |= 1u << k;
+  }
+  return need;
+}
+
 template <typename T>
 __host__ __device__ inline T* ws_ptr(char* base, size_t stride, int f, size_t off) {
   return reinterpret_cast<T*>(base + (size_t)f * stride + off);

@@ -1009,27 +1009,13 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
 // face whose half-space excludes 0 (KKT), so at most one x-face and one y-face are candidates; on
 // each the 1-D minimiser is clamped to the face.  An inexact minimiser only raises the computed value
 // by qc delta^2 (quadratic in its error), far inside thr's margin.
-// face_min (fgs_internal.cuh): the minimum of q2 over one box, shared with the backward's warp cull.
+// face_min / subboxes_may_reach (fgs_internal.cuh): shared with the backward re-walk (backward.cu).
 
 // NP pixels per lane: warp w of the tile's NW = 64/NP... warps owns a column block; lane l owns pixel
 // (x, y + 4k), k < NP, of that block (x = l & 7, y = l >> 3).  Sub-box k = rows [4k, 4k+4) of the block.
 constexpr int kBlendPix = 4;                         // pixels per lane
 constexpr int kBlendBatch = 128;                     // records staged per batch (6 KB of smem)
 constexpr int kBlendWarps = 256 / (32 * kBlendPix);  // warps per 16x16 tile (2)
-
-// All kBlendPix 8x4 sub-boxes of a warp's column at once (shared x-face and minimiser ratios).
-__device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
-                                                       float y0) {
-  const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
-  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
-  uint32_t need = 0;
-#pragma unroll
-  for (int k = 0; k < kBlendPix; ++k) {
-    const float yl = y0 + 4.f * k, yh = yl + 3.f;
-    if (face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr) need |= 1u << k;
-  }
-  return need;
-}
 
 template <bool DBG>
 __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __grid_constant__ RenderBatch b) {
@@ -1106,7 +1092,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         const float4 a = srec[jt].a;
         // b.cull = 0 (FGS_TUNE_BLEND_CULL): every Gaussian on every live sub-box — the unculled Eq. 4
         // loop, which the culled one must equal bit for bit
-        need = b.cull ? subboxes_may_reach(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live
+        need = b.cull ? subboxes_may_reach<kBlendPix>(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live
                       : live;
       }
       uint32_t mk[kBlendPix];
