@@ -572,6 +572,211 @@ struct DefBwdArgs {
 template <bool COLOR>
 constexpr int db_nout() { return COLOR ? 60 : 10; }
 
+// FAST path of deform_backward_kernel (see there): in_dim 64, phi_d width 64 or 128, no decoders
+template <int W, int IN, bool COLOR>
+constexpr bool db_fast() { return !COLOR && IN == 64 && (W == 64 || W == 128); }
+
+// Plane gradients of one row (warp, lanes over features k = lane + 32 ks): dv_p = dfh * prod_{q != p} v_q
+// scattered to the 4 corners with fixed-point atomics, du from dv / du; returns du (lane partials).
+template <int KS, int IN>
+__device__ __forceinline__ void db_plane_grads(const DefBwdArgs& A, const float* u, const float* dfh, int lane,
+                                               float* du) {
+  const DeformBatch& p = A.p;
+  const int FEAT = p.feat;
+  const int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {1, 2, 2, 3, 3, 3};
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = lane + 32 * ks;
+    if (k >= IN || dfh[ks] == 0.f) continue;
+    const int l = k / FEAT, c = k - l * FEAT;
+    float v[6], w00[6], w01[6], w10[6], w11[6], dva[6], dvb[6];
+    size_t base[6];
+    int rowb[6];
+#pragma unroll
+    for (int pl = 0; pl < 6; ++pl) {
+      const int na = PA[pl] < 3 ? p.res[l] : p.t_res, nb = PB[pl] < 3 ? p.res[l] : p.t_res;
+      const float ga = u[PA[pl]] * (float)(na - 1), gb = u[PB[pl]] * (float)(nb - 1);
+      const int i0 = min((int)floorf(ga), na - 2), j0 = min((int)floorf(gb), nb - 2);
+      const float fa = ga - (float)i0, fb = gb - (float)j0;
+      base[pl] = ((size_t)j0 * na + i0) * FEAT + c;
+      rowb[pl] = na * FEAT;
+      const float* P = p.planes[l][pl] + base[pl];
+      const float v00 = __ldg(P), v01 = __ldg(P + FEAT), v10 = __ldg(P + rowb[pl]), v11 = __ldg(P + rowb[pl] + FEAT);
+      w00[pl] = (1.f - fa) * (1.f - fb); w01[pl] = fa * (1.f - fb);
+      w10[pl] = (1.f - fa) * fb;         w11[pl] = fa * fb;
+      v[pl] = w00[pl] * v00 + w01[pl] * v01 + w10[pl] * v10 + w11[pl] * v11;
+      dva[pl] = ((1.f - fb) * (v01 - v00) + fb * (v11 - v10)) * (float)(na - 1);   // dv / du_a
+      dvb[pl] = ((1.f - fa) * (v10 - v00) + fa * (v11 - v01)) * (float)(nb - 1);   // dv / du_b
+    }
+#pragma unroll
+    for (int pl = 0; pl < 6; ++pl) {
+      float others = 1.f;
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        if (q != pl) others *= v[q];
+      const float dv = dfh[ks] * others;
+      unsigned long long* Ag = A.acc_planes[l][pl] + base[pl];
+      fix_add(Ag, (double)dv * w00[pl]);
+      fix_add(Ag + FEAT, (double)dv * w01[pl]);
+      fix_add(Ag + rowb[pl], (double)dv * w10[pl]);
+      fix_add(Ag + rowb[pl] + FEAT, (double)dv * w11[pl]);
+      if (PA[pl] < 3) du[PA[pl]] += dv * dva[pl];
+      if (PB[pl] < 3) du[PB[pl]] += dv * dvb[pl];
+    }
+  }
+}
+
+template <int W, int IN, int NO>
+__device__ __forceinline__ void db_fast_phases(const DefBwdArgs& A, const float* sWd, const float* sBd,
+                                               const float* sWh, float* sFh, float* sDz, float* sFd, float* sDo,
+                                               float* sDfh, int nrow, int64_t row0, int warp, int lane, int tid) {
+  constexpr int R = db_rows<W>();
+  constexpr int LDK = IN + 4, LDW = W + 4, KS = IN / 32;
+  const DeformBatch& p = A.p;
+  const int FEAT = p.feat, nout = A.nout;
+  const int PA[6] = {0, 0, 1, 0, 1, 2}, PB[6] = {1, 2, 2, 3, 3, 3};
+  const float ut = p.t[0];
+  auto row_u = [&](int64_t g, float* u, bool* inb) {
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3) {
+      const float v = (p.means[g * 3 + a3] - p.bmin[a3]) / p.ext[a3];
+      inb[a3] = v >= 0.f && v <= 1.f;
+      u[a3] = fminf(fmaxf(v, 0.f), 1.f);
+    }
+    u[3] = ut;
+  };
+  // ---- phase 1 (warp per row, lanes over features): f_h = prod of the 6 bilinear samples; dOut ----
+  for (int r = warp; r < R; r += kDbWarps) {
+    float* fh = sFh + r * LDK;
+    float* dO = sDo + r * NO;
+    if (r >= nrow) {                          // rows past the range: zero inputs
+      for (int k = lane; k < IN; k += 32) fh[k] = 0.f;
+      for (int o = lane; o < nout; o += 32) dO[o] = 0.f;
+      continue;
+    }
+    const int64_t g = row0 + r;
+    float u[4];
+    bool inb[3];
+    row_u(g, u, inb);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = lane + 32 * ks;
+      const int l = k / FEAT, c = k - l * FEAT;
+      float f = 1.f;
+#pragma unroll
+      for (int pl = 0; pl < 6; ++pl) {
+        const int na = PA[pl] < 3 ? p.res[l] : p.t_res, nb = PB[pl] < 3 ? p.res[l] : p.t_res;
+        const float ga = u[PA[pl]] * (float)(na - 1), gb = u[PB[pl]] * (float)(nb - 1);
+        const int i0 = min((int)floorf(ga), na - 2), j0 = min((int)floorf(gb), nb - 2);
+        const float fa = ga - (float)i0, fb = gb - (float)j0;
+        const float* P = p.planes[l][pl] + ((size_t)j0 * na + i0) * FEAT + c;
+        const float v00 = __ldg(P), v01 = __ldg(P + FEAT);
+        const float v10 = __ldg(P + (size_t)na * FEAT), v11 = __ldg(P + (size_t)na * FEAT + FEAT);
+        f *= (1.f - fa) * (1.f - fb) * v00 + fa * (1.f - fb) * v01 + (1.f - fa) * fb * v10 + fa * fb * v11;
+      }
+      fh[k] = f;
+    }
+    for (int o = lane; o < nout; o += 32)
+      dO[o] = o < 3 ? A.d_means[g * 3 + o] : o < 7 ? A.d_quats[g * 4 + o - 3] : A.d_log_scales[g * 3 + o - 7];
+  }
+  __syncthreads();
+  // ---- phase 2a: z = W_d f_h + b_d, dz = (W_h^T dOut) [z > 0], f_d = relu(z): 4 x 4 tiles of (row,
+  //      hidden unit), rows rb + RB i and units cb + CB j (strided, so the 16 column rows a warp reads
+  //      at one k are consecutive rows: conflict-free with the padded stride) ----
+  {
+    constexpr int CB = W / 4, RB = R / 4;
+    static_assert(CB * RB == kDbThreads, "one 4 x 4 tile per thread");
+    const int cb = tid % CB, rb = tid / CB;
+    float z[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) z[i][j] = sBd[cb + CB * j];
+    for (int k = 0; k < IN; k += 4) {
+      float4 F4[4], W4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) F4[i] = *reinterpret_cast<const float4*>(sFh + (rb + RB * i) * LDK + k);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) W4[j] = *reinterpret_cast<const float4*>(sWd + (cb + CB * j) * LDK + k);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          z[i][j] = fmaf(W4[j].x, F4[i].x, z[i][j]);
+          z[i][j] = fmaf(W4[j].y, F4[i].y, z[i][j]);
+          z[i][j] = fmaf(W4[j].z, F4[i].z, z[i][j]);
+          z[i][j] = fmaf(W4[j].w, F4[i].w, z[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = rb + RB * i, cw = cb + CB * j;
+        float dfd = 0.f;
+        for (int o = 0; o < nout; ++o) dfd = fmaf(sWh[o * W + cw], sDo[r * NO + o], dfd);
+        sDz[r * LDW + cw] = z[i][j] > 0.f ? dfd : 0.f;
+        sFd[r * LDW + cw] = fmaxf(z[i][j], 0.f);
+      }
+  }
+  __syncthreads();
+  // ---- phase 2b: d f_h[k] = sum_cw W_d[cw][k] dz[cw]: tiles of TR rows x 4 features ----
+  {
+    constexpr int KB = IN / 4, TR = R * IN / (kDbThreads * 4), RB = R / TR;
+    static_assert(KB * RB == kDbThreads, "one TR x 4 tile per thread");
+    const int kb = tid % KB, rb = tid / KB;
+    float d[TR][4];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[i][j] = 0.f;
+    for (int cw = 0; cw < W; cw += 4) {
+      float4 D4[TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) D4[i] = *reinterpret_cast<const float4*>(sDz + (rb + RB * i) * LDW + cw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 Wq = *reinterpret_cast<const float4*>(sWd + (cw + q) * LDK + 4 * kb);
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          const float dz = q == 0 ? D4[i].x : q == 1 ? D4[i].y : q == 2 ? D4[i].z : D4[i].w;
+          d[i][0] = fmaf(Wq.x, dz, d[i][0]);
+          d[i][1] = fmaf(Wq.y, dz, d[i][1]);
+          d[i][2] = fmaf(Wq.z, dz, d[i][2]);
+          d[i][3] = fmaf(Wq.w, dz, d[i][3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+      *reinterpret_cast<float4*>(sDfh + (rb + RB * i) * LDK + 4 * kb) = make_float4(d[i][0], d[i][1], d[i][2], d[i][3]);
+  }
+  __syncthreads();
+  // ---- phase 3 (warp per row): plane gradients, dX; outputs ----
+  for (int r = warp; r < nrow; r += kDbWarps) {
+    const int64_t g = row0 + r;
+    float u[4];
+    bool inb[3];
+    row_u(g, u, inb);
+    float dfh[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dfh[ks] = sDfh[r * LDK + lane + 32 * ks];
+    float du[3] = {0.f, 0.f, 0.f};
+    db_plane_grads<KS, IN>(A, u, dfh, lane, du);
+    // du summed over the lanes by a fixed butterfly (deterministic)
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) du[a3] += __shfl_xor_sync(0xffffffffu, du[a3], o);
+    if (lane < 3) {
+      const float dux = inb[lane] ? du[lane] / p.ext[lane] : 0.f;
+      A.o_means[g * 3 + lane] = A.d_means[g * 3 + lane] + dux;
+      A.o_log_scales[g * 3 + lane] = A.d_log_scales[g * 3 + lane];
+    }
+    if (lane < 4) A.o_quats[g * 4 + lane] = A.d_quats[g * 4 + lane];
+  }
+}
+
 template <int W, int IN, bool COLOR>
 __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __grid_constant__ DefBwdArgs A) {
   constexpr int kDbRows = db_rows<W>();
@@ -580,20 +785,29 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
   constexpr int KS = (IN + 31) / 32;       // feature slots per lane
   constexpr int WS = W / 32;               // hidden-unit slots per lane
   const DeformBatch& p = A.p;
+  // FAST (the configs' fields: in_dim 64, phi_d width 64 / 128, no decoders): the MLP steps run as
+  // CTA-wide register-tiled products over the CTA's rows (phase 2) between a forward pass (phase 1) and
+  // the plane-gradient pass (phase 3), instead of per-row shuffle loops; every output is still summed
+  // over its inputs in ascending order with fmaf, so the values are the per-row loops' bit for bit.
+  // Row strides padded by 4 floats (LDK, LDW) so the tiles' shared loads are conflict-free.
+  constexpr bool FAST = db_fast<W, IN, COLOR>();
+  constexpr int LDK = FAST ? IN + 4 : IN;
+  constexpr int LDW = FAST ? W + 4 : W;
   extern __shared__ __align__(16) float dsm[];
-  float* sWd = dsm;                        // [W][IN]   row-major (k contiguous)
-  float* sWdT = sWd + W * IN;              // [IN][W]   transposed (cw contiguous)
-  float* sBd = sWdT + W * IN;              // [W]
+  float* sWd = dsm;                        // [W][LDK]  row-major (k contiguous)
+  float* sWdT = sWd + W * LDK;             // [IN][W]   transposed (cw contiguous; not with FAST)
+  float* sBd = sWdT + (FAST ? 0 : W * IN); // [W]
   float* sWh = sBd + W;                    // [NO][W] : rows x(3), r(4), s(3), then C (3K), alpha
-  float* sFh = sWh + NO * W;               // [kDbRows][IN]
-  float* sDz = sFh + kDbRows * IN;         // [kDbRows][W]
-  float* sFd = sDz + kDbRows * W;          // [kDbRows][W]
-  float* sDo = sFd + kDbRows * W;          // [kDbRows][NO]
+  float* sFh = sWh + NO * W;               // [kDbRows][LDK]
+  float* sDz = sFh + kDbRows * LDK;        // [kDbRows][LDW]
+  float* sFd = sDz + kDbRows * LDW;        // [kDbRows][LDW]
+  float* sDo = sFd + kDbRows * LDW;        // [kDbRows][NO]
+  float* sDfh = sDo + kDbRows * NO;        // FAST: [kDbRows][LDK] d f_h
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < W * IN; e += kDbThreads) {
     const float v = p.w_d[e];
-    sWd[e] = v;
-    sWdT[(e % IN) * W + e / IN] = v;
+    sWd[(e / IN) * LDK + e % IN] = v;
+    if constexpr (!FAST) sWdT[(e % IN) * W + e / IN] = v;
   }
   for (int e = tid; e < W; e += kDbThreads) sBd[e] = p.b_d[e];
   const int n_c = COLOR ? p.n_c : 0;
@@ -608,6 +822,9 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
   const int64_t row0 = p.begin + (int64_t)blockIdx.x * kDbRows;
   const int nrow = (int)(p.end - row0 < (int64_t)kDbRows ? p.end - row0 : (int64_t)kDbRows);
   const float ut = p.t[0];
+  if constexpr (FAST) {
+    db_fast_phases<W, IN, NO>(A, sWd, sBd, sWh, sFh, sDz, sFd, sDo, sDfh, nrow, row0, warp, lane, tid);
+  } else
   for (int r = warp; r < kDbRows; r += kDbWarps) {
     float* fh = sFh + r * IN;
     float* dz = sDz + r * W;
@@ -756,8 +973,8 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
     const int cw0 = (e / (IN / 4)) * 4, k0 = (e % (IN / 4)) * 4;
     float acc4[4][4] = {};
     for (int r = 0; r < nrow; ++r) {
-      const float4 dz4 = *reinterpret_cast<const float4*>(sDz + r * W + cw0);
-      const float4 fh4 = *reinterpret_cast<const float4*>(sFh + r * IN + k0);
+      const float4 dz4 = *reinterpret_cast<const float4*>(sDz + r * LDW + cw0);
+      const float4 fh4 = *reinterpret_cast<const float4*>(sFh + r * LDK + k0);
       const float dzv[4] = {dz4.x, dz4.y, dz4.z, dz4.w}, fhv[4] = {fh4.x, fh4.y, fh4.z, fh4.w};
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -771,13 +988,13 @@ __global__ void __launch_bounds__(kDbThreads, 2) deform_backward_kernel(const __
   }
   for (int cw = tid; cw < W; cw += kDbThreads) {
     float sacc = 0.f;
-    for (int r = 0; r < nrow; ++r) sacc += sDz[r * W + cw];
+    for (int r = 0; r < nrow; ++r) sacc += sDz[r * LDW + cw];
     fix_add(A.acc_bd + cw, sacc);
   }
   for (int e = tid; e < nout * W; e += kDbThreads) {
     const int o = e / W, cw = e - o * W;
     float sacc = 0.f;
-    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDo[r * NO + o], sFd[r * W + cw], sacc);
+    for (int r = 0; r < nrow; ++r) sacc = fmaf(sDo[r * NO + o], sFd[r * LDW + cw], sacc);
     fix_add(A.acc_wh + e, sacc);
   }
   for (int o = tid; o < nout; o += kDbThreads) {
@@ -876,7 +1093,10 @@ size_t deform_backward_acc_elems(const DeformBatch& p) {
 template <int W, int IN, bool COLOR>
 cudaError_t launch_def_bwd_c(const DefBwdArgs& A, unsigned grid, cudaStream_t s) {
   constexpr size_t NO = db_nout<COLOR>();
-  const size_t smem = sizeof(float) * (2 * (size_t)W * IN + W + NO * W + (size_t)db_rows<W>() * (IN + 2 * W + NO));
+  constexpr bool FAST = db_fast<W, IN, COLOR>();
+  constexpr size_t LDK = FAST ? IN + 4 : IN, LDW = FAST ? W + 4 : W;
+  const size_t smem = sizeof(float) * ((size_t)W * LDK + (FAST ? 0 : (size_t)W * IN) + W + NO * W +
+                                       (size_t)db_rows<W>() * (LDK + 2 * LDW + NO + (FAST ? LDK : 0)));
   cudaError_t e = cudaFuncSetAttribute(deform_backward_kernel<W, IN, COLOR>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
