@@ -119,6 +119,41 @@ def test_deform_backward_matches_oracle():
     assert _rel(ft["w_d"].cpu().numpy(), 2 * ref["w_d"]) <= TOL
 
 
+@pytest.mark.parametrize("config,n", [("neu3d", 100), ("hypernerf", 45)])
+def test_deform_backward_width128_matches_oracle(config, n):
+    """phi_d width 128 (the H / N3 / S fields): the deform backward's CTA-tiled path at 32 rows per CTA,
+    with a ragged last CTA (100 = 3 x 32 + 4; 45 = 32 + 13), against the autograd oracle."""
+    import torch
+
+    from oracle import backward as B
+    s = make_scene(config, n=n, width=48, height=40, n_frames=2, seed=4)
+    s = dataclasses.replace(s, means=(s.means * 0.6).astype(np.float32))
+    s = with_heads(s, 0.5, seed=11, bias_sigma=0.05)
+    assert s.mlp.w_d.shape == (128, 64)
+    ds = fgs.DeviceScene(s)
+    t = float(s.times[1])
+    rng = np.random.default_rng(19)
+    up = {"means": rng.normal(size=(s.n, 3)), "log_scales": rng.normal(size=(s.n, 3)),
+          "quats": rng.normal(size=(s.n, 4))}
+    up = {k: v.astype(np.float32) for k, v in up.items()}
+    dd, dt = ds.alloc_gaussian_grads()
+    for k, v in up.items():
+        dt[k].copy_(torch.from_numpy(v))
+    dc, ct = ds.alloc_gaussian_grads()
+    df, ft = ds.alloc_field_grads()
+    scratch = torch.empty(fgs.fgs_deform_backward_scratch_bytes(ds.field, ds.mlp), dtype=torch.uint8, device="cuda")
+    fgs.fgs_deform_backward(ds.g, ds.field, ds.mlp, t, dd, dc, df, scratch)
+    torch.cuda.synchronize()
+    ref = B.deform_grads_ref(s, t, up)
+    for k in ("means", "log_scales", "quats"):
+        err = _rel(ct[k].cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+    for k, v in ft.items():
+        assert np.any(ref[k] != 0), k
+        err = _rel(v.cpu().numpy(), ref[k])
+        assert err <= TOL, (k, err)
+
+
 def test_losses_match_oracle():
     """L1 value and gradient (B2), TV value and plane gradients (B1) against the oracle."""
     import torch
