@@ -965,11 +965,22 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// d = a * (w, w) + c per component, rounded once each (fma.rn.f32x2: sm_100a's FFMA2, bit-equal to two fmaf)
+__device__ __forceinline__ float2 ffma2_bcast(float2 a, float w, float2 c) {
+  unsigned long long d;
+  const float2 ww = make_float2(w, w);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&ww)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
 // thr: the exponent threshold of the alpha >= 1/255 test while the pixel is live, +inf once it has
 // stopped (or lies outside the image) — one compare then covers both "live" and "alpha >= 1/255"
 // (no separate done flag to test and update per evaluation)
 struct PixelState {
-  float T, c0, c1, c2, thr;
+  float2 c01;                // red, green: one packed FFMA2 per step (fma.rn.f32x2, bit-equal to 2 x fmaf)
+  float T, c2, thr;
   uint32_t ncon, nev;
   __device__ __forceinline__ bool done() const { return thr == __int_as_float(0x7f800000); }
 };
@@ -993,8 +1004,7 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
   const bool stop = ok && test_T < kTMin;
   if (ok && !stop) {
     const float w = alpha * s.T;
-    s.c0 = fmaf(r, w, s.c0);
-    s.c1 = fmaf(g, w, s.c1);
+    s.c01 = ffma2_bcast(make_float2(r, g), w, s.c01);
     s.c2 = fmaf(bch, w, s.c2);
     s.T = test_T;
     if (DBG) s.ncon += 1u;
@@ -1052,7 +1062,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
 #pragma unroll
   for (int k = 0; k < kBlendPix; ++k) {
     const bool in = pxi < b.width && py0 + 4 * k < b.height;
-    P[k] = PixelState{1.f, 0.f, 0.f, 0.f, in ? kLog2AlphaMin : __int_as_float(0x7f800000), 0u, (uint32_t)L};
+    P[k] = PixelState{make_float2(0.f, 0.f), 1.f, 0.f, in ? kLog2AlphaMin : __int_as_float(0x7f800000), 0u, (uint32_t)L};
   }
   auto all_done = [&]() {
     bool d = true;
@@ -1099,7 +1109,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
 #pragma unroll
       for (int k = 0; k < kBlendPix; ++k) mk[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
       // walked from the most significant bit of the bit-reversed masks (= list order): the next
-      // Gaussian is one FLO, its bit one shift, clearing it one XOR
+      // Gaussian is one FLO (bfind), its bit one shift, clearing it one XOR
       uint32_t m = 0;
 #pragma unroll
       for (int k = 0; k < kBlendPix; ++k) {
@@ -1112,18 +1122,21 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
 #pragma unroll
         for (int k = 0; k < kBlendPix; ++k) n_evald += __popc(mk[k]);
       }
+      // record of bit h = list entry c0 + 31 - h: one multiply-add from the chunk's last record
+      const char* rlast = reinterpret_cast<const char*>(&srec[c0 + 31]);
       while (m) {
-        const int h = 31 - __clz(m);
+        int h;                                 // bit index of m's most significant set bit (FLO)
+        asm("bfind.u32 %0, %1;" : "=r"(h) : "r"(m));
         const uint32_t hb = 1u << h;
         m ^= hb;
-        const int j = c0 + 31 - h;
-        const float4 a = srec[j].a, q = srec[j].q;
-        const float bch = srec[j].c.x;
+        const SRec& rj = *reinterpret_cast<const SRec*>(rlast - h * (int)sizeof(SRec));
+        const float4 a = rj.a, q = rj.q;
+        const float bch = rj.c.x;
         const float dx = a.x - lx;
         const float bdx = a.w * dx;                              // b2 dx, shared by the lane's pixels
         const float base = fmaf(a.z * dx, dx, q.y);              // a2 dx^2 + log2(o)
         const float dy0 = a.y - ly;
-        const uint32_t pos = (uint32_t)(start + j + 1);
+        const uint32_t pos = (uint32_t)(start + c0 + 31 - h + 1);
 #pragma unroll
         for (int k = 0; k < kBlendPix; ++k) {
           if (mk[k] & hb) {
@@ -1149,8 +1162,8 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
     const int py = py0 + 4 * k;
     if (!(pxi < b.width && py < b.height)) continue;
     const size_t pix = (size_t)py * b.width + pxi;
-    img[pix] = s.c0 + s.T * cm.bg[0];
-    img[hw + pix] = s.c1 + s.T * cm.bg[1];
+    img[pix] = s.c01.x + s.T * cm.bg[0];
+    img[hw + pix] = s.c01.y + s.T * cm.bg[1];
     img[2 * hw + pix] = s.c2 + s.T * cm.bg[2];
     if (DBG) {
       if (b.final_T[f]) b.final_T[f][pix] = s.T;
