@@ -975,6 +975,21 @@ __device__ __forceinline__ float2 ffma2_bcast(float2 a, float w, float2 c) {
   return *reinterpret_cast<float2*>(&d);
 }
 
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 bits_f2(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+// (a.x + b.x, a.y + b.y), each rounded as the scalar add (add.rn.f32x2: FADD2)
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+// (a.x * w, a.y * w), each rounded as the scalar multiply (mul.rn.f32x2: FMUL2)
+__device__ __forceinline__ float2 fmul2_bcast(float2 a, float w) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(make_float2(w, w))));
+  return bits_f2(d);
+}
+
 // thr: the exponent threshold of the alpha >= 1/255 test while the pixel is live, +inf once it has
 // stopped (or lies outside the image) — one compare then covers both "live" and "alpha >= 1/255"
 // (no separate done flag to test and update per evaluation)
@@ -1056,6 +1071,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
   __shared__ SRec srec[BATCH];
   const float tx0 = (float)(tx * kTile), ty0 = (float)(ty * kTile);
   const float lx = (float)lxi, ly = (float)lyi;
+  const float2 nl = make_float2(-lx, -ly);   // a - l == a + (-l) exactly
   const float bxl = (float)bx0, bxh = (float)(bx0 + 7);
   uint32_t n_tested = 0, n_evald = 0;    // DBG: per-warp cull statistics (sub-box evaluations)
   PixelState P[kBlendPix];
@@ -1132,10 +1148,12 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         const SRec& rj = *reinterpret_cast<const SRec*>(rlast - h * (int)sizeof(SRec));
         const float4 a = rj.a, q = rj.q;
         const float bch = rj.c.x;
-        const float dx = a.x - lx;
-        const float bdx = a.w * dx;                              // b2 dx, shared by the lane's pixels
-        const float base = fmaf(a.z * dx, dx, q.y);              // a2 dx^2 + log2(o)
-        const float dy0 = a.y - ly;
+        // packed pairs (each half rounded as its scalar op): (dx, dy0) = mean - pixel, (a2 dx, b2 dx)
+        const float2 d0 = fadd2(make_float2(a.x, a.y), nl);
+        const float dx = d0.x, dy0 = d0.y;
+        const float2 abdx = fmul2_bcast(make_float2(a.z, a.w), dx);
+        const float bdx = abdx.y;                                // b2 dx, shared by the lane's pixels
+        const float base = fmaf(abdx.x, dx, q.y);                // a2 dx^2 + log2(o)
         const uint32_t pos = (uint32_t)(start + c0 + 31 - h + 1);
 #pragma unroll
         for (int k = 0; k < kBlendPix; ++k) {
