@@ -160,13 +160,13 @@ __device__ __noinline__ float4 lerp_plane(const float* __restrict__ P, int R, in
   return lerp4(a, b, fa);
 }
 
-// Head outputs (transposed weights [W][NOUTP], 12 per pass of the epilogue): 10 geometry outputs
+// Head outputs (transposed weights [W][NOUTP]; with the decoders 12 per pass of the epilogue): 10 geometry outputs
 // (dX 3, dr 4, ds 3), then with the P:1232 decoders 3K colour outputs and 1 opacity output.
 constexpr int kNoutColor = 60;   // 10 + 48 + 1 = 59 at SH degree 3, padded to a multiple of 12
 
 template <int WIDTH, bool COLOR = false>
 struct Tc3Smem {
-  static constexpr int NOUTP = COLOR ? kNoutColor : 12;
+  static constexpr int NOUTP = COLOR ? kNoutColor : 10;   // [W][10] without the decoders: column pairs 80 B
   static constexpr int B_BYTES = 64 * WIDTH * 4;
   static constexpr int OFF_BHI = 0;
   static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
@@ -182,6 +182,7 @@ struct Tc3Smem {
   static constexpr int OFF_BAR = OFF_SEG + 16 * 4;
   // barriers: 0 a_full, 1 a_free, 2-3 d_full, 4-5 d_free; then the TMEM base address
   static constexpr int TOTAL = OFF_BAR + 6 * 8 + 16;
+  static_assert(OFF_BAR % 8 == 0 && OFF_WH % 16 == 0 && OFF_BD % 16 == 0, "smem carve-up alignment");
 };
 
 // With the colour decoders the epilogue (59 head outputs) is the bottleneck: it gets the registers
@@ -679,18 +680,43 @@ __global__ void __launch_bounds__(Roles<FEAT>::THREADS, 1) deform_tc3_kernel(con
                 if (lane == 0) mbar_arrive(d_free + buf);
               }
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float fd = fmaxf(v[i] + bd[c0 + i], 0.f);
-                FGS_DCHECK((c0 + i) * NOUTP + 12 * pass + 12 <= NOUTP * WIDTH);
-                const float4* w4 = reinterpret_cast<const float4*>(Wh + (c0 + i) * NOUTP + 12 * pass);
-                const float4 wa = w4[0], wb = w4[1], wc = w4[2];
-                const float2 fd2 = make_float2(fd, fd);
-                acc[0] = ffma2(fd2, make_float2(wa.x, wa.y), acc[0]);
-                acc[1] = ffma2(fd2, make_float2(wa.z, wa.w), acc[1]);
-                acc[2] = ffma2(fd2, make_float2(wb.x, wb.y), acc[2]);
-                acc[3] = ffma2(fd2, make_float2(wb.z, wb.w), acc[3]);
-                acc[4] = ffma2(fd2, make_float2(wc.x, wc.y), acc[4]);
-                if (COLOR) acc[5] = ffma2(fd2, make_float2(wc.z, wc.w), acc[5]);
+              for (int i = 0; i < 16; i += 2) {
+                // bias added to the column pair (c, c + 1) by one FADD2 (each half rounded as the
+                // scalar add); every output sums its columns in ascending order, as before
+                const int c = c0 + i;
+                const float2 z = fadd2(make_float2(v[i], v[i + 1]), make_float2(bd[c], bd[c + 1]));
+                const float2 fa = make_float2(fmaxf(z.x, 0.f), fmaxf(z.x, 0.f));
+                const float2 fb = make_float2(fmaxf(z.y, 0.f), fmaxf(z.y, 0.f));
+                if constexpr (!COLOR) {
+                  // the pair's 20 weights are 80 contiguous bytes ([W][10]): five 16-B loads
+                  FGS_DCHECK((c + 2) * NOUTP <= NOUTP * WIDTH);
+                  const float4* w4 = reinterpret_cast<const float4*>(Wh + c * NOUTP);
+                  const float4 w0 = w4[0], w1 = w4[1], w2 = w4[2], w3 = w4[3], w5 = w4[4];
+                  acc[0] = ffma2(fa, make_float2(w0.x, w0.y), acc[0]);
+                  acc[1] = ffma2(fa, make_float2(w0.z, w0.w), acc[1]);
+                  acc[2] = ffma2(fa, make_float2(w1.x, w1.y), acc[2]);
+                  acc[3] = ffma2(fa, make_float2(w1.z, w1.w), acc[3]);
+                  acc[4] = ffma2(fa, make_float2(w2.x, w2.y), acc[4]);
+                  acc[0] = ffma2(fb, make_float2(w2.z, w2.w), acc[0]);
+                  acc[1] = ffma2(fb, make_float2(w3.x, w3.y), acc[1]);
+                  acc[2] = ffma2(fb, make_float2(w3.z, w3.w), acc[2]);
+                  acc[3] = ffma2(fb, make_float2(w5.x, w5.y), acc[3]);
+                  acc[4] = ffma2(fb, make_float2(w5.z, w5.w), acc[4]);
+                } else {
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const float2 fd2 = h ? fb : fa;
+                    FGS_DCHECK((c + h) * NOUTP + 12 * pass + 12 <= NOUTP * WIDTH);
+                    const float4* w4 = reinterpret_cast<const float4*>(Wh + (c + h) * NOUTP + 12 * pass);
+                    const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+                    acc[0] = ffma2(fd2, make_float2(wa.x, wa.y), acc[0]);
+                    acc[1] = ffma2(fd2, make_float2(wa.z, wa.w), acc[1]);
+                    acc[2] = ffma2(fd2, make_float2(wb.x, wb.y), acc[2]);
+                    acc[3] = ffma2(fd2, make_float2(wb.z, wb.w), acc[3]);
+                    acc[4] = ffma2(fd2, make_float2(wc.x, wc.y), acc[4]);
+                    acc[5] = ffma2(fd2, make_float2(wc.z, wc.w), acc[5]);
+                  }
+                }
               }
             }
             if (pass == 0) {

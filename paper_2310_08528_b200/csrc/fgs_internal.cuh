@@ -178,7 +178,8 @@ constexpr int kRadixMinListDefault = 768;    // FGS_TUNE_RADIX_MIN_LIST default 
 void prof_mark(int stage, bool begin, cudaStream_t s);
 void note_launches(int64_t k);
 
-// Packed fp32x2 arithmetic (sm_100: FFMA2 / FMUL2, two fp32 lanes per instruction).
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2, two fp32 lanes per instruction, each lane
+// rounded exactly as the scalar fmaf / + / * — bit-equal results).
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
   asm("{\n.reg .b64 ra, rb, rc, rd;\n"
@@ -186,6 +187,15 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
       "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
       : "=f"(d.x), "=f"(d.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\n"
+      "add.rn.f32x2 rd, ra, rb;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {

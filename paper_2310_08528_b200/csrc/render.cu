@@ -965,36 +965,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// d = a * (w, w) + c per component, rounded once each (fma.rn.f32x2: sm_100a's FFMA2, bit-equal to two fmaf)
-__device__ __forceinline__ float2 ffma2_bcast(float2 a, float w, float2 c) {
-  unsigned long long d;
-  const float2 ww = make_float2(w, w);
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
-      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&ww)),
-        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&d);
-}
-
-__device__ __forceinline__ unsigned long long f2_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
-__device__ __forceinline__ float2 bits_f2(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
-// (a.x + b.x, a.y + b.y), each rounded as the scalar add (add.rn.f32x2: FADD2)
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return bits_f2(d);
-}
-// (a.x * w, a.y * w), each rounded as the scalar multiply (mul.rn.f32x2: FMUL2)
-__device__ __forceinline__ float2 fmul2_bcast(float2 a, float w) {
-  unsigned long long d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(make_float2(w, w))));
-  return bits_f2(d);
-}
-
 // thr: the exponent threshold of the alpha >= 1/255 test while the pixel is live, +inf once it has
 // stopped (or lies outside the image) — one compare then covers both "live" and "alpha >= 1/255"
 // (no separate done flag to test and update per evaluation)
 struct PixelState {
-  float2 c01;                // red, green: one packed FFMA2 per step (fma.rn.f32x2, bit-equal to 2 x fmaf)
+  float2 c01;                // red, green: one packed FFMA2 per step
   float T, c2, thr;
   uint32_t ncon, nev;
   __device__ __forceinline__ bool done() const { return thr == __int_as_float(0x7f800000); }
@@ -1019,7 +994,7 @@ __device__ __forceinline__ void blend_step(PixelState& s, float e, float lo, flo
   const bool stop = ok && test_T < kTMin;
   if (ok && !stop) {
     const float w = alpha * s.T;
-    s.c01 = ffma2_bcast(make_float2(r, g), w, s.c01);
+    s.c01 = ffma2(make_float2(r, g), make_float2(w, w), s.c01);   // FFMA2, bit-equal to 2 x fmaf
     s.c2 = fmaf(bch, w, s.c2);
     s.T = test_T;
     if (DBG) s.ncon += 1u;
@@ -1151,7 +1126,7 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         // packed pairs (each half rounded as its scalar op): (dx, dy0) = mean - pixel, (a2 dx, b2 dx)
         const float2 d0 = fadd2(make_float2(a.x, a.y), nl);
         const float dx = d0.x, dy0 = d0.y;
-        const float2 abdx = fmul2_bcast(make_float2(a.z, a.w), dx);
+        const float2 abdx = fmul2(make_float2(a.z, a.w), make_float2(dx, dx));
         const float bdx = abdx.y;                                // b2 dx, shared by the lane's pixels
         const float base = fmaf(abdx.x, dx, q.y);                // a2 dx^2 + log2(o)
         const uint32_t pos = (uint32_t)(start + c0 + 31 - h + 1);
