@@ -208,41 +208,42 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   return d;
 }
 
-// Minimum of the PSD quadratic q2(d) = qa dx^2 + qb dx dy + qc dy^2 over one box [xl,xh] x [yl,yh] of
-// offsets d = pixel - mean (the blend's ellipse-vs-box cull, render.cu, and the backward's warp cull,
-// backward.cu), given the box's x-face candidate ex (xl if xl > 0, xh if xh < 0, else 0) and the
-// minimiser ratios kx = -qb / (2 qa), ky = -qb / (2 qc): at most one x-face and one y-face can hold the
-// minimum when the box excludes 0 (KKT); on each the 1-D minimiser is clamped to the face.
-__device__ __forceinline__ float face_min(float qa, float qb, float qc, float kx, float ky, float ex, float xl,
-                                          float xh, float yl, float yh) {
-  const float ey = yl > 0.f ? yl : (yh < 0.f ? yh : 0.f);
-  float q = 0.f;
-  if (ex != 0.f) {
-    const float yy = fminf(fmaxf(ky * ex, yl), yh);
-    q = fmaf(fmaf(qa, ex, qb * yy), ex, qc * yy * yy);
-  }
-  if (ey != 0.f) {
-    const float xx = fminf(fmaxf(kx * ey, xl), xh);
-    const float q2 = fmaf(fmaf(qc, ey, qb * xx), ey, qa * xx * xx);
-    q = ex != 0.f ? fminf(q, q2) : q2;
-  }
-  return q;
-}
-
-// All NP 8x4 sub-boxes of a warp's 8-wide column (rows y0 + 4k .. y0 + 4k + 3, k < NP) at once, with
-// the shared x-face and minimiser ratios: bit k set if the Gaussian's alpha may reach 1/255 somewhere in
-// sub-box k (face_min <= thr).  The forward blend and its backward re-walk cull with the same test.
+// Conservative ellipse-vs-box cull (the blend, render.cu, and the backward's re-walk, backward.cu, cull
+// with this same test): bit k set if the Gaussian's alpha may reach 1/255 somewhere in sub-box k (rows
+// y0 + 4k .. y0 + 4k + 3 of the warp's 8-wide column [xl, xh], offsets d = pixel - mean), i.e. if the
+// minimum of the PSD quadratic q2(d) = qa dx^2 + qb dx dy + qc dy^2 over the box is <= thr.
+// The minimum of a convex quadratic over a box lies at d = 0 if the box holds 0, else on a face whose
+// half-space excludes 0 (KKT): at most the x-face ex (xl if xl > 0, xh if xh < 0) and the y-face ey.  On
+// each face the 1-D minimiser (ratios kx = -qb / 2qa, ky = -qb / 2qc) is clamped to the face.  Branch
+// free: both face candidates are always evaluated — with ex = 0 (resp. ey = 0) the "face" is the line
+// x = 0 (y = 0) through the box, whose clamped point is still a point of the box, so the minimum of the
+// two candidates is exactly the box minimum in every case (0 when the box holds the origin).
 template <int NP>
-__device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
-                                                       float y0) {
+__device__ __forceinline__ void subboxes_reach(float qa, float qb, float qc, float thr, float xl, float xh, float y0,
+                                               bool (&reach)[NP]) {
   const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
-  const float ex = xl > 0.f ? xl : (xh < 0.f ? xh : 0.f);
-  uint32_t need = 0;
+  const float ex = fmaxf(xl, fminf(xh, 0.f));     // xl if xl > 0, xh if xh < 0, else 0
+  const float kyex = ky * ex;
+  const float a0 = qa * ex * ex, b0 = qb * ex;     // q2(ex, y) = a0 + y (b0 + qc y)
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
     const float yl = y0 + 4.f * k, yh = yl + 3.f;
-    if (face_min(qa, qb, qc, kx, ky, ex, xl, xh, yl, yh) <= thr) need |= 1u << k;
+    const float ey = fmaxf(yl, fminf(yh, 0.f));
+    const float yy = fminf(fmaxf(kyex, yl), yh);
+    const float qx = fmaf(yy, fmaf(qc, yy, b0), a0);
+    const float xx = fminf(fmaxf(kx * ey, xl), xh);
+    const float qy = fmaf(xx, fmaf(qa, xx, qb * ey), qc * ey * ey);
+    reach[k] = fminf(qx, qy) <= thr;
   }
+}
+template <int NP>
+__device__ __forceinline__ uint32_t subboxes_may_reach(float qa, float qb, float qc, float thr, float xl, float xh,
+                                                       float y0) {
+  bool r[NP];
+  subboxes_reach<NP>(qa, qb, qc, thr, xl, xh, y0, r);
+  uint32_t need = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) need |= r[k] ? 1u << k : 0u;
   return need;
 }
 

@@ -1088,17 +1088,19 @@ __global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __gri
         if (__any_sync(0xffffffffu, !P[k].done())) live |= 1u << k;
       if (!live) break;
       const int jt = c0 + lane;
-      uint32_t need = 0;
-      if (jt < cnt) {
-        const float4 a = srec[jt].a;
+      bool reach[kBlendPix];
+#pragma unroll
+      for (int k = 0; k < kBlendPix; ++k) reach[k] = jt < cnt;
+      if (jt < cnt && b.cull) {
         // b.cull = 0 (FGS_TUNE_BLEND_CULL): every Gaussian on every live sub-box — the unculled Eq. 4
         // loop, which the culled one must equal bit for bit
-        need = b.cull ? subboxes_may_reach<kBlendPix>(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y) & live
-                      : live;
+        const float4 a = srec[jt].a;
+        subboxes_reach<kBlendPix>(-a.z, -a.w, -srec[jt].q.x, srec[jt].c.y, bxl - a.x, bxh - a.x, -a.y, reach);
       }
+      // sub-box masks straight from the per-lane predicates; a stopped sub-box (not live) gets none
       uint32_t mk[kBlendPix];
 #pragma unroll
-      for (int k = 0; k < kBlendPix; ++k) mk[k] = __ballot_sync(0xffffffffu, (need >> k) & 1u);
+      for (int k = 0; k < kBlendPix; ++k) mk[k] = __ballot_sync(0xffffffffu, reach[k]) & (0u - ((live >> k) & 1u));
       // walked from the most significant bit of the bit-reversed masks (= list order): the next
       // Gaussian is one FLO (bfind), its bit one shift, clearing it one XOR
       uint32_t m = 0;
