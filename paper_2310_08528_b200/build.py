@@ -56,12 +56,12 @@ def build(force=False, verbose=False, checked=None):
         try:
             if not force and not needs_build(lib):
                 return lib
-            return _build(verbose, checked)
+            return _build(verbose, checked, force)
         finally:
             fcntl.flock(lk, fcntl.LOCK_UN)
 
 
-def _build(verbose=False, checked=False):
+def _build(verbose=False, checked=False, force=False):
     nvcc = nvcc_path()
     objdir = os.path.join(HERE, "build", "checked") if checked else os.path.join(HERE, "build")
     LIB_OUT = LIB_CHECKED if checked else LIB
@@ -69,18 +69,38 @@ def _build(verbose=False, checked=False):
     objs = []
     logs = []
     procs = []
+    # incremental: an object newer than its source, every header and this file is reused (its ptxas log
+    # is kept beside it); experiment builds (FGS_NVCC_EXTRA) and force=True always recompile
+    extra = os.environ.get("FGS_NVCC_EXTRA", "").split()
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "fgs.h"), __file__]
+    stamp = os.path.join(objdir, ".plain")      # present when the objects came from a build without extras
+    reuse_ok = not force and not extra and os.path.exists(stamp)
+    if os.path.exists(stamp):
+        os.remove(stamp)
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if reuse_ok and os.path.exists(obj) and os.path.exists(obj + ".log") and all(
+                os.path.getmtime(d) < os.path.getmtime(obj) for d in [src] + hdrs):
+            procs.append((src, obj, None))
+            continue
         # FGS_NVCC_EXTRA: extra flags for experiments (e.g. -D switches); not set in normal builds
-        cmd = ([nvcc] + NVCC_FLAGS + (["-DFGS_CHECKED"] if checked else [])
-               + os.environ.get("FGS_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj])
+        cmd = ([nvcc] + NVCC_FLAGS + (["-DFGS_CHECKED"] if checked else []) + extra + ["-c", src, "-o", obj])
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for src, obj, p in procs:
+        if p is None:
+            with open(obj + ".log") as fh:
+                logs.append(fh.read())
+            objs.append(obj)
+            continue
         out = p.communicate()[0].decode(errors="replace")
         logs.append(out)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{out}")
+        with open(obj + ".log", "w") as fh:
+            fh.write(out)
         objs.append(obj)
+    if not extra:
+        open(stamp, "w").close()
     tmp = LIB_OUT + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            "-o", tmp] + objs + ["-cudart", "static"]
