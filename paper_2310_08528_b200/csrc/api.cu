@@ -560,14 +560,16 @@ HostLayout host_layout(const fgs_gaussians* g, const fgs_hexplanes* h, const fgs
 
 namespace {
 constexpr int kHostChunkFrames = 4;
-// Side stream + events of ONE fgs_frames_host call.  Calls take a set from a per-device free list for
+// Side streams + events of ONE fgs_frames_host call (`up`: the SH upload, `copy`: the image downloads —
+// two streams, so that when calls on different caller streams are in flight together the upload of one
+// never queues behind the downloads of another).  Calls take a set from a per-device free list for
 // the duration of their enqueue and give it back before returning, so concurrent calls (distinct
 // workspaces, any threads) never share a stream or an event while enqueueing.  Re-recording an event
 // after the set is returned does not affect the waits already enqueued on it (a wait captures the
 // event's state at enqueue time), so a set is reusable as soon as its call has returned.
 struct CopySet {
   int dev = -1;
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy = nullptr, up = nullptr;
   cudaEvent_t done = nullptr, fork = nullptr, sh_done = nullptr;
   std::vector<cudaEvent_t> evs;
   cudaError_t event(int i, cudaEvent_t* out) {
@@ -604,6 +606,7 @@ cudaError_t acquire_copy_set(CopySet** out) {
   CopySet* c = new CopySet();
   c->dev = dev;
   e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->sh_done, cudaEventDisableTiming);
@@ -690,10 +693,10 @@ int fgs_frames_host(const fgs_gaussians* gh, const fgs_hexplanes* hh, const fgs_
   if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
   if (sh_side) {
     if ((e = cudaEventRecord(cs.fork, s)) != cudaSuccess) return cuda_fail(e, "event record");
-    if ((e = cudaStreamWaitEvent(cs.copy, cs.fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
-    if ((e = cudaMemcpyAsync(d + L.sh, gh->sh, 12 * K * n, cudaMemcpyHostToDevice, cs.copy)) != cudaSuccess)
+    if ((e = cudaStreamWaitEvent(cs.up, cs.fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    if ((e = cudaMemcpyAsync(d + L.sh, gh->sh, 12 * K * n, cudaMemcpyHostToDevice, cs.up)) != cudaSuccess)
       return cuda_fail(e, "host->device copy");
-    if ((e = cudaEventRecord(cs.sh_done, cs.copy)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaEventRecord(cs.sh_done, cs.up)) != cudaSuccess) return cuda_fail(e, "event record");
   }
   fgs_gaussians gd = *gh;
   gd.means = (const float*)(d + L.means); gd.log_scales = (const float*)(d + L.log_scales);
