@@ -798,6 +798,44 @@ def test_frames_host_concurrent_threads():
             assert torch.equal(a, b), k
 
 
+def test_frames_host_two_calls_in_flight():
+    """bench.py's pipelined e2e: one host thread keeps two fgs_frames_host calls in flight on two
+    streams (each lane its own workspace and pinned images; the SH upload and the image downloads ride
+    separate side streams), eight steps alternating two different batches of times.  Every lane ends
+    with the images of its last batch, bit-equal to the one-call-at-a-time result."""
+    import dataclasses
+    import numpy as np
+    import torch
+    F = 6
+    s0 = make_scene("dnerf", n=40_000, width=208, height=160, n_frames=F)
+    s1 = dataclasses.replace(s0, times=np.asarray(s0.times[::-1], np.float32).copy())
+    hs = [fgs.HostScene(s0), fgs.HostScene(s1)]
+    nbytes = fgs.fgs_frames_host_workspace_bytes(hs[0].g, hs[0].field, hs[0].mlp, F, 208, 160, 16 * s0.n)
+    ref = []
+    for h in hs:
+        out = [torch.empty((3, 160, 208)).pin_memory() for _ in range(F)]
+        dws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        fgs.fgs_frames_host(h.g, h.field, h.mlp, h.times, h.cams, out, dws)
+        torch.cuda.synchronize()
+        ref.append(out)
+    assert not all(torch.equal(a, b) for a, b in zip(ref[0], ref[1]))   # the two batches differ
+    lanes = [torch.cuda.Stream() for _ in range(2)]
+    wss = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    outs = [[torch.full((3, 160, 208), float("nan")).pin_memory() for _ in range(F)] for _ in range(2)]
+    last = [None, None]
+    for k in range(8):
+        j = k % 2
+        which = (k // 2) % 2          # lane j renders batch 0, 1, 0, 1
+        h = hs[which]
+        fgs.fgs_frames_host(h.g, h.field, h.mlp, h.times, h.cams, outs[j], wss[j], stream=lanes[j])
+        last[j] = which
+    for j in range(2):
+        fgs.fgs_frames_host_status(hs[last[j]].g, hs[last[j]].field, hs[last[j]].mlp, hs[last[j]].cams, wss[j],
+                                   stream=lanes[j])
+        for a, b in zip(ref[last[j]], outs[j]):
+            assert torch.equal(a, b), j
+
+
 @pytest.mark.parametrize("mode", ["default", "long_sort_direct_atomics_unculled", "radix"])
 def test_repeated_runs_bit_identical(mode):
     """Race stand-in (compute-sanitizer is closed on the GPU pool): 12 back-to-back fgs_frames calls of
