@@ -1017,8 +1017,11 @@ constexpr int kBlendPix = 4;                         // pixels per lane
 constexpr int kBlendBatch = 128;                     // records staged per batch (6 KB of smem)
 constexpr int kBlendWarps = 256 / (32 * kBlendPix);  // warps per 16x16 tile (2)
 
+#ifndef FGS_BLEND_MIN_CTAS
+#define FGS_BLEND_MIN_CTAS 24   // 40 registers (sweep: DESIGN 7b / 7c)
+#endif
 template <bool DBG>
-__global__ void __launch_bounds__(32 * kBlendWarps, 24) blend_kernel(const __grid_constant__ RenderBatch b) {
+__global__ void __launch_bounds__(32 * kBlendWarps, FGS_BLEND_MIN_CTAS) blend_kernel(const __grid_constant__ RenderBatch b) {
   // One CTA (kBlendWarps warps) per 16x16 tile.  Warp w owns the 8-wide column block x in [8w, 8w+8)
   // of all 16 rows; lane l owns the kBlendPix pixels (8w + (l&7), (l>>3) + 4k).  The tile's list (sorted
   // by (depth, gid)) is walked in batches of kBlendBatch records staged in smem; per 32 Gaussians each lane tests
