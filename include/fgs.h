@@ -320,9 +320,17 @@ int64_t fgs_launch_count(void);
  * placed at its bucket's start + the number of its bucket's instances below it (a list with a bucket of
  * more than 64 instances falls back to 0); 0 = CTA bitonic networks on 4096-instance segments + merge
  * levels.  The order is identical either way (fgs_render_aux.long_sort_paths counts which ran).
+ * FGS_TUNE_TILE_CULL: 0 (default) = a tile's list holds every kept Gaussian whose [3dgs] rect covers the
+ * tile (the oracle's lists, bit for bit); 1 = a Gaussian whose rect holds at most 64 tiles is left
+ * out of the list of a tile on which its alpha provably stays below 1/255 at every pixel (fp64 minimum of
+ * its Eq. 1 exponent over the tile's 16x16 pixel box against the blend's own threshold with margin): the
+ * lists are then ordered subsequences of the [3dgs] lists that keep every contributing entry, and images,
+ * final T and contributor counts are identical (tests check both on whole full-size frames);
+ * fgs_render_aux.tiles_touched counts the remaining tiles, n_instances the remaining entries.  With 1
+ * the per-tile sorts are used for every frame (FGS_TUNE_RADIX is ignored).
  * (Key 1 is retired: there is a single deformation kernel.) */
 enum { FGS_TUNE_TILE_SORT_CAP = 0, FGS_TUNE_BLEND_CULL = 2, FGS_TUNE_AGG_TILES = 3, FGS_TUNE_RADIX = 4,
-       FGS_TUNE_RADIX_MIN_LIST = 5, FGS_TUNE_LONG_SORT = 6 };
+       FGS_TUNE_RADIX_MIN_LIST = 5, FGS_TUNE_LONG_SORT = 6, FGS_TUNE_TILE_CULL = 7 };
 int fgs_set_tuning(int32_t key, int64_t value);
 int64_t fgs_get_tuning(int32_t key);
 

@@ -216,6 +216,8 @@ int render_impl(const fgs_camera* cams, const fgs_deformed* defs, float* const* 
   local.radix_mode = local.L.ntiles <= kRxMaxTiles ? radix_mode() : 0;
   local.radix_min_list = radix_min_list();
   local.long_sort = long_sort();
+  local.tile_cull = tile_cull();
+  if (local.tile_cull) local.radix_mode = 0;   // the radix path emits whole rects
   local.debug = aux != nullptr;
   local.blend_work = aux ? (unsigned long long*)aux->blend_work : nullptr;
   local.ws_stride = per;
@@ -312,6 +314,7 @@ WsLayout make_layout(int64_t n, int width, int height, int64_t cap) {
   L.rx_hist = take(4 * 256 * (size_t)L.rx_blocks);
   L.rx_dtot = take(4 * 256);
   L.rx_bsum = take(4 * (size_t)((std::max<int64_t>(n, 1) + kRxItems - 1) / kRxItems));
+  L.tmask = take(8 * nn);
   L.total = o;
   return L;
 }
@@ -334,6 +337,7 @@ std::atomic<int> g_agg_tiles{kAggTilesMax};
 std::atomic<int> g_radix_mode{0};
 std::atomic<int> g_radix_min_list{kRadixMinListDefault};
 std::atomic<int> g_long_sort{1};
+std::atomic<int> g_tile_cull{0};
 }
 int tile_sort_cap() { return g_tile_sort_cap.load(std::memory_order_relaxed); }
 int blend_cull() { return g_blend_cull.load(std::memory_order_relaxed); }
@@ -341,6 +345,7 @@ int agg_tiles() { return g_agg_tiles.load(std::memory_order_relaxed); }
 int radix_mode() { return g_radix_mode.load(std::memory_order_relaxed); }
 int radix_min_list() { return g_radix_min_list.load(std::memory_order_relaxed); }
 int long_sort() { return g_long_sort.load(std::memory_order_relaxed); }
+int tile_cull() { return g_tile_cull.load(std::memory_order_relaxed); }
 
 }  // namespace fgs
 
@@ -503,6 +508,10 @@ int fgs_set_tuning(int32_t key, int64_t value) {
       FGS_CHECK(value == 0 || value == 1, "long sort mode must be 0 or 1");
       g_long_sort.store((int)value);
       return FGS_OK;
+    case FGS_TUNE_TILE_CULL:
+      FGS_CHECK(value == 0 || value == 1, "tile cull must be 0 or 1");
+      g_tile_cull.store((int)value);
+      return FGS_OK;
     default:
       return fail(FGS_E_INVALID, "unknown tuning key");
   }
@@ -515,6 +524,7 @@ int64_t fgs_get_tuning(int32_t key) {
   if (key == FGS_TUNE_RADIX) return radix_mode();
   if (key == FGS_TUNE_RADIX_MIN_LIST) return radix_min_list();
   if (key == FGS_TUNE_LONG_SORT) return long_sort();
+  if (key == FGS_TUNE_TILE_CULL) return tile_cull();
   return -1;
 }
 

@@ -60,6 +60,8 @@ struct WsLayout {
   size_t rx_hist = 0;        // uint32[256][rx_blocks] per-block digit counts -> offsets (radix.cu)
   size_t rx_dtot = 0;        // uint32[256] digit totals of a pass
   size_t rx_bsum = 0;        // uint32[ceil(n / kRxItems)] tiles_touched sums of depth-ordered blocks
+  size_t tmask = 0;          // uint64[n] tiles of the rect (row-major bit (ty - y0) * w + tx - x0) a Gaussian
+                             // stays listed on (FGS_TUNE_TILE_CULL = 1; rects of at most 64 tiles)
   size_t total = 0;
 };
 
@@ -85,6 +87,7 @@ struct RenderBatch {
   int radix_mode;            // FGS_TUNE_RADIX: 0 per-tile sorts only, 1 auto, 2 radix path for every frame
   int radix_min_list;        // auto: a frame takes the radix path when M >= radix_min_list x tiles
   int long_sort;             // FGS_TUNE_LONG_SORT: 1 bucket pass for long lists, 0 networks + merges
+  int tile_cull;             // FGS_TUNE_TILE_CULL: 1 = non-contributing (tile, Gaussian) pairs left out of the lists
   char* ws;                  // frame f slice = ws + f * ws_stride
   size_t ws_stride;
   WsLayout L;
@@ -171,6 +174,7 @@ int agg_tiles();
 int radix_mode();
 int radix_min_list();
 int long_sort();
+int tile_cull();
 constexpr int kAggTilesMax = 4096;           // shared histogram of the CTA binning aggregation
 constexpr int kRadixMinListDefault = 768;    // FGS_TUNE_RADIX_MIN_LIST default (mean list length)
 

@@ -134,7 +134,70 @@ __device__ __forceinline__ bool agg_fits(const AggBox& r, int limit) {
   return r.x1 > r.x0 && (int64_t)(r.x1 - r.x0) * (r.y1 - r.y0) <= limit;
 }
 
-template <int DEG>
+// The tiles (tx, ty) of a rect a Gaussian is listed on, in row-major order.  CULL: the set bits of tmask
+// (bit (ty - y0) * w + tx - x0) for rects of at most 64 tiles; every tile otherwise.
+template <bool CULL, typename Fn>
+__device__ __forceinline__ void for_each_tile(int x0, int y0, int x1, int y1, unsigned long long tmask, Fn&& fn) {
+  const int w = x1 - x0;
+  if (!CULL || w * (y1 - y0) > 64) {
+    for (int ty = y0; ty < y1; ++ty)
+      for (int tx = x0; tx < x1; ++tx) fn(tx, ty);
+  } else {
+    const unsigned long long wm = w >= 64 ? ~0ull : (1ull << w) - 1ull;
+    int sh = 0;
+    for (int ty = y0; ty < y1; ++ty, sh += w) {
+      unsigned long long rm = (tmask >> sh) & wm;
+      while (rm) {
+        const int rx = __ffsll((long long)rm) - 1;
+        rm &= rm - 1ull;
+        fn(x0 + rx, ty);
+      }
+    }
+  }
+}
+// May alpha reach 1/255 on the tile whose pixel offsets d = pixel - mean span [xl, xl + 15] x [yl, yl + 15]?
+// The minimum of the PSD quadratic q2 over the box is 0 if the box holds 0, else it lies on the x- or
+// y-face nearest to 0 at the clamped 1-D minimiser (kx = -qb / 2qa, ky = -qb / 2qc): the blend's
+// sub-box bound (subboxes_reach, fgs_internal.cuh) on the 16x16 box.
+__device__ __forceinline__ bool tile_box_reach(float qa, float qb, float qc, float kx, float ky, float thr,
+                                               float xl, float yl) {
+  const float xh = xl + (float)(kTile - 1), yh = yl + (float)(kTile - 1);
+  const float ex = fmaxf(xl, fminf(xh, 0.f)), ey = fmaxf(yl, fminf(yh, 0.f));
+  const float yy = fminf(fmaxf(ky * ex, yl), yh);
+  const float qx = fmaf(yy, fmaf(qc, yy, qb * ex), qa * ex * ex);
+  const float xx = fminf(fmaxf(kx * ey, xl), xh);
+  const float qy = fmaf(xx, fmaf(qa, xx, qb * ey), qc * ey * ey);
+  return fminf(qx, qy) <= thr;
+}
+
+// Per-tile instance counts of a CTA's Gaussians: aggregated in shared memory over the CTA's
+// rect union when it holds at most agg_tiles tiles (one global atomic per touched tile), else direct
+// global atomics (cnt67[0] counts the CTAs that took that path: fgs_render_aux.binning_direct[0]).
+// CULL: only the tiles of tmask (FGS_TUNE_TILE_CULL).  Called by every thread of the CTA.
+template <bool CULL>
+__device__ __forceinline__ void count_tiles(bool keep, int x0, int y0, int x1, int y1, unsigned long long tmask,
+                                            uint32_t* tile_count, int gx, int gy, int agg_tiles, uint32_t* cnt67,
+                                            int* sbox, uint32_t* scount) {
+  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
+  if (agg_fits(box, agg_tiles)) {
+    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= gx && box.y1 <= gy);
+    for (int q = threadIdx.x; q < area; q += blockDim.x) scount[q] = 0;
+    __syncthreads();
+    if (keep)
+      for_each_tile<CULL>(x0, y0, x1, y1, tmask,
+                          [&](int tx, int ty) { atomicAdd(scount + (ty - box.y0) * bw + (tx - box.x0), 1u); });
+    __syncthreads();
+    for (int q = threadIdx.x; q < area; q += blockDim.x)
+      if (scount[q]) atomicAdd(tile_count + (box.y0 + q / bw) * gx + box.x0 + q % bw, scount[q]);
+  } else {
+    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt67, 1u);
+    if (keep)
+      for_each_tile<CULL>(x0, y0, x1, y1, tmask, [&](int tx, int ty) { atomicAdd(tile_count + ty * gx + tx, 1u); });
+  }
+}
+
+template <int DEG, bool CULL>
 __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constant__ RenderBatch b) {
   // frame-minor CTA order: the F CTAs of one Gaussian block are adjacent in launch order, so its SH
   // (192 B per Gaussian at degree 3, frame-invariant) come from HBM once and from L2 for the other frames
@@ -222,29 +285,49 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
     keep = (x1 - x0) * (y1 - y0) > 0;
   }
   keep = keep && valid;
+  // ---- FGS_TUNE_TILE_CULL: the tiles of the rect on which the Gaussian stays listed ----
+  // Bit (ty - y0) * w + (tx - x0) of tmask; all ones without the cull or for rects over 64 tiles.  A
+  // tile is dropped only if the minimum over its 16x16 pixel box of q2(d) = qa dx^2 + qb dx dy + qc dy^2
+  // (d = pixel - mean) exceeds the blend's threshold thr_keep (below: log2(255 o) plus the margin that
+  // covers fp32 evaluation): then every pixel of the tile has alpha < 1/255 in the blend.  Same bound
+  // as the blend's sub-box cull (tile_box_reach above), whose sub-boxes lie inside the tile's box.
+  unsigned long long tmask = ~0ull;
+  int ntl = (x1 - x0) * (y1 - y0);
+  // blend threshold: q2 = -p2 >= 0; alpha >= 1/255 needs q2 <= log2(255 o).  The margin covers the fp32
+  // evaluation of q2 in the blend and in the cull tests, whose relative error grows with the conic's
+  // condition number kappa = lambda_max / lambda_min of Sigma2.  (Computed here with the tile cull, which
+  // needs it; after the counts otherwise, where fewer values are live.)
+  float opac = 0.f, thr_keep = 0.f;
+  double idet = 0.0;
+  auto blend_threshold = [&]() {
+    opac = 1.f / (1.f + __expf(-b.opacity[f][i]));
+    idet = kLog2e / det;
+    const float root = (float)sqrt(fmax(0.0, mid * mid - det));
+    const float lam_max = (float)mid + root, lam_min = fmaxf((float)mid - root, 1e-30f);
+    const float thr2 = __log2f(255.f * opac);
+    thr_keep = thr2 + (fabsf(thr2) + 1.f) * (2e-3f + 4e-6f * (lam_max / lam_min));
+  };
+  if (CULL && keep) {
+    blend_threshold();
+    if (ntl <= 64) {
+      const float qa = (float)(0.5 * cc * idet), qb = (float)(-bb * idet), qc = (float)(0.5 * a * idet);
+      const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
+      const float fmx = (float)mx, fmy = (float)my;
+      tmask = 0ull;
+      int bit = 0;
+      for (int ty = y0; ty < y1; ++ty) {
+        const float yl = (float)(ty * kTile) - fmy;
+        for (int tx = x0; tx < x1; ++tx, ++bit)
+          if (tile_box_reach(qa, qb, qc, kx, ky, thr_keep, (float)(tx * kTile) - fmx, yl)) tmask |= 1ull << bit;
+      }
+      ntl = __popcll(tmask);
+    }
+  }
   // ---- instance counts per tile (the bucket sizes of the duplication) ----
   __shared__ int sbox[4];
   __shared__ uint32_t scount[kAggTilesMax];
-  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
-  if (agg_fits(box, b.agg_tiles)) {
-    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
-    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= b.gx && box.y1 <= b.gy);
-    for (int q = threadIdx.x; q < area; q += blockDim.x) scount[q] = 0;
-    __syncthreads();
-    if (keep)
-      for (int ty = y0; ty < y1; ++ty)
-        for (int tx = x0; tx < x1; ++tx) atomicAdd(scount + (ty - box.y0) * bw + (tx - box.x0), 1u);
-    __syncthreads();
-    for (int q = threadIdx.x; q < area; q += blockDim.x)
-      if (scount[q]) atomicAdd(tile_count + (box.y0 + q / bw) * b.gx + box.x0 + q % bw, scount[q]);
-  } else {
-    // direct global atomics (the CTA's rect union exceeds the shared histogram); cnt[6] counts the
-    // CTAs that took this path (debug evidence, fgs_render_aux.binning_direct[0])
-    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt_ptr(b, f) + 6, 1u);
-    if (keep)
-      for (int ty = y0; ty < y1; ++ty)
-        for (int tx = x0; tx < x1; ++tx) atomicAdd(tile_count + ty * b.gx + tx, 1u);
-  }
+  uint32_t* cnt67 = cnt_ptr(b, f) + 6;
+  count_tiles<CULL>(keep, x0, y0, x1, y1, tmask, tile_count, b.gx, b.gy, b.agg_tiles, cnt67, sbox, scount);
   if (!valid) return;
   if (!keep) {
     keys[i] = 0u;
@@ -255,7 +338,8 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
   }
   // ---- step 11: depth key = bits of fp32(p.z) (> 0.2 so unsigned order = depth order) ----
   keys[i] = __float_as_uint((float)pz);
-  tt[i] = (uint32_t)((x1 - x0) * (y1 - y0));
+  tt[i] = (uint32_t)ntl;      // tiles the Gaussian is listed on (the whole rect without the tile cull)
+  if (CULL) ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.tmask)[i] = tmask;
   rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
   radii[i] = (int32_t)rad;
   // ---- step 12: SH colour at d = normalize(X - campos), campos = -R^T t (R10, R11) ----
@@ -271,15 +355,7 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
   //   p2 = a2 dx^2 + b2 dx dy + c2 dy^2 = power * log2(e);  alpha = min(0.99, 2^(p2 + log2 o))
   const float mxh = (float)mx, myh = (float)my;
   const float mxl = (float)(mx - (double)mxh), myl = (float)(my - (double)myh);
-  const float opac = 1.f / (1.f + __expf(-b.opacity[f][i]));
-  const double idet = kLog2e / det;
-  // Ellipse cull threshold (blend): q2 = -p2 >= 0; alpha >= 1/255 needs q2 <= log2(255 o).  The
-  // margin covers the fp32 evaluation of q2 in the blend and in the cull test, whose relative
-  // error grows with the conic's condition number kappa = lambda_max / lambda_min of Sigma2.
-  const float root = (float)sqrt(fmax(0.0, mid * mid - det));
-  const float lam_max = (float)mid + root, lam_min = fmaxf((float)mid - root, 1e-30f);
-  const float thr2 = __log2f(255.f * opac);
-  const float thr_keep = thr2 + (fabsf(thr2) + 1.f) * (2e-3f + 4e-6f * (lam_max / lam_min));
+  if (!CULL) blend_threshold();
   rec[3 * i + 0] = make_float4(mxh, myh, (float)(-0.5 * cc * idet), (float)(bb * idet));
   rec[3 * i + 1] = make_float4((float)(-0.5 * a * idet), __log2f(opac), fmaxf(col[0], 0.f), fmaxf(col[1], 0.f));
   rec[3 * i + 2] = make_float4(fmaxf(col[2], 0.f), mxl, myl, thr_keep);
@@ -376,6 +452,43 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const __grid_co
 }
 
 // ------------------------------------------------------------------------------ duplicate (a5)
+// Key duplication of a CTA's Gaussians: one global cursor claim per touched tile for the
+// whole CTA with the slots handed out in shared memory, or direct global atomics when the CTA's rect
+// union exceeds agg_tiles (cnt7 counts those CTAs: fgs_render_aux.binning_direct[1]).  CULL: only the
+// tiles of tmask (FGS_TUNE_TILE_CULL; the same mask preprocess counted with).
+template <bool CULL>
+__device__ __forceinline__ void emit_instances(bool keep, int x0, int y0, int x1, int y1, unsigned long long tmask,
+                                               unsigned long long v, uint32_t* cursor, unsigned long long* inst,
+                                               uint64_t cap, int gx, int gy, int agg_tiles, uint32_t* cnt7,
+                                               int* sbox, uint32_t* sbase) {
+  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
+  if (agg_fits(box, agg_tiles)) {
+    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
+    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= gx && box.y1 <= gy);
+    for (int q = threadIdx.x; q < area; q += blockDim.x) sbase[q] = 0;
+    __syncthreads();
+    if (keep)
+      for_each_tile<CULL>(x0, y0, x1, y1, tmask,
+                          [&](int tx, int ty) { atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u); });
+    __syncthreads();
+    for (int q = threadIdx.x; q < area; q += blockDim.x)
+      if (sbase[q]) sbase[q] = atomicAdd(cursor + (box.y0 + q / bw) * gx + box.x0 + q % bw, sbase[q]);
+    __syncthreads();
+    if (keep)
+      for_each_tile<CULL>(x0, y0, x1, y1, tmask, [&](int tx, int ty) {
+        const uint32_t pos = atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
+        if (pos < cap) inst[pos] = v;
+      });
+  } else {
+    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt7, 1u);
+    if (keep)
+      for_each_tile<CULL>(x0, y0, x1, y1, tmask, [&](int tx, int ty) {
+        const uint32_t pos = atomicAdd(cursor + ty * gx + tx, 1u);
+        if (pos < cap) inst[pos] = v;
+      });
+  }
+}
+
 __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ RenderBatch b) {
   const int f = blockIdx.y;
   if (cnt_ptr(b, f)[8]) return;                 // the radix path emits this frame's instances (radix.cu)
@@ -396,34 +509,13 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const __grid_constant__ 
   const unsigned long long v = ((unsigned long long)key << 32) | (uint32_t)i;
   __shared__ int sbox[4];
   __shared__ uint32_t sbase[kAggTilesMax];
-  const AggBox box = cta_rect_union(keep, x0, y0, x1, y1, sbox);
-  if (agg_fits(box, b.agg_tiles)) {
-    // one global cursor claim per touched tile for the whole CTA, slots handed out in smem
-    const int bw = box.x1 - box.x0, area = bw * (box.y1 - box.y0);
-    FGS_DCHECK(area <= kAggTilesMax && box.x0 >= 0 && box.y0 >= 0 && box.x1 <= b.gx && box.y1 <= b.gy);
-    for (int q = threadIdx.x; q < area; q += blockDim.x) sbase[q] = 0;
-    __syncthreads();
-    if (keep)
-      for (int ty = y0; ty < y1; ++ty)
-        for (int tx = x0; tx < x1; ++tx) atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
-    __syncthreads();
-    for (int q = threadIdx.x; q < area; q += blockDim.x)
-      if (sbase[q]) sbase[q] = atomicAdd(cursor + (box.y0 + q / bw) * b.gx + box.x0 + q % bw, sbase[q]);
-    __syncthreads();
-    if (keep)
-      for (int ty = y0; ty < y1; ++ty)
-        for (int tx = x0; tx < x1; ++tx) {
-          const uint32_t pos = atomicAdd(sbase + (ty - box.y0) * bw + (tx - box.x0), 1u);
-          if (pos < cap) inst[pos] = v;
-        }
+  if (b.tile_cull) {
+    const unsigned long long tmask = keep ? ws_ptr<unsigned long long>(b.ws, b.ws_stride, f, b.L.tmask)[i] : 0ull;
+    emit_instances<true>(keep, x0, y0, x1, y1, tmask, v, cursor, inst, cap, b.gx, b.gy, b.agg_tiles,
+                         cnt_ptr(b, f) + 7, sbox, sbase);
   } else {
-    if (threadIdx.x == 0 && box.x1 > box.x0) atomicAdd(cnt_ptr(b, f) + 7, 1u);   // binning_direct[1]
-    if (keep)
-      for (int ty = y0; ty < y1; ++ty)
-        for (int tx = x0; tx < x1; ++tx) {
-          const uint32_t pos = atomicAdd(cursor + ty * b.gx + tx, 1u);
-          if (pos < cap) inst[pos] = v;
-        }
+    emit_instances<false>(keep, x0, y0, x1, y1, ~0ull, v, cursor, inst, cap, b.gx, b.gy, b.agg_tiles,
+                          cnt_ptr(b, f) + 7, sbox, sbase);
   }
 }
 
@@ -1187,11 +1279,20 @@ cudaError_t launch_render(const RenderBatch& b, cudaStream_t s) {
   prof_mark(FGS_STAGE_PREPROCESS, true, s);
   clear_kernel<<<dim3((unsigned)std::min(64, (b.ntiles + 255) / 256), F), 256, 0, s>>>(b);
   const dim3 pre_grid((unsigned)(nb * (unsigned)F));   // 1-D, frame-minor (see preprocess_kernel)
-  switch (b.sh_degree) {
-    case 0: preprocess_kernel<0><<<pre_grid, 256, 0, s>>>(b); break;
-    case 1: preprocess_kernel<1><<<pre_grid, 256, 0, s>>>(b); break;
-    case 2: preprocess_kernel<2><<<pre_grid, 256, 0, s>>>(b); break;
-    default: preprocess_kernel<3><<<pre_grid, 256, 0, s>>>(b); break;
+  if (b.tile_cull) {
+    switch (b.sh_degree) {
+      case 0: preprocess_kernel<0, true><<<pre_grid, 256, 0, s>>>(b); break;
+      case 1: preprocess_kernel<1, true><<<pre_grid, 256, 0, s>>>(b); break;
+      case 2: preprocess_kernel<2, true><<<pre_grid, 256, 0, s>>>(b); break;
+      default: preprocess_kernel<3, true><<<pre_grid, 256, 0, s>>>(b); break;
+    }
+  } else {
+    switch (b.sh_degree) {
+      case 0: preprocess_kernel<0, false><<<pre_grid, 256, 0, s>>>(b); break;
+      case 1: preprocess_kernel<1, false><<<pre_grid, 256, 0, s>>>(b); break;
+      case 2: preprocess_kernel<2, false><<<pre_grid, 256, 0, s>>>(b); break;
+      default: preprocess_kernel<3, false><<<pre_grid, 256, 0, s>>>(b); break;
+    }
   }
   note_launches(2);
   prof_mark(FGS_STAGE_PREPROCESS, false, s);
@@ -1246,7 +1347,7 @@ __global__ void debug_copy_kernel(const __grid_constant__ RenderBatch b, fgs_ren
   const uint2* ranges = ws_ptr<uint2>(b.ws, b.ws_stride, 0, b.L.ranges);
   const unsigned long long* inst = ws_ptr<unsigned long long>(b.ws, b.ws_stride, 0, b.L.inst);
   if (i < b.n) {
-    const bool kept = tt[i] != 0;
+    const bool kept = radii[i] != 0;       // (not tt: the tile cull may leave a kept Gaussian on no tile)
     if (aux.radii) aux.radii[i] = radii[i];
     if (aux.tiles_touched) aux.tiles_touched[i] = tt[i];
     if (aux.depth_key) aux.depth_key[i] = kept ? keys[i] : 0u;

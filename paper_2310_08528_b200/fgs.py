@@ -90,6 +90,7 @@ FGS_TUNE_AGG_TILES = 3
 FGS_TUNE_RADIX = 4
 FGS_TUNE_RADIX_MIN_LIST = 5
 FGS_TUNE_LONG_SORT = 6
+FGS_TUNE_TILE_CULL = 7
 
 
 def lib():

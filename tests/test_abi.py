@@ -93,6 +93,11 @@ def test_tuning_knob_host_only(L):
         assert fgs.fgs_get_tuning(fgs.FGS_TUNE_BLEND_CULL) == 0
     assert fgs.fgs_get_tuning(fgs.FGS_TUNE_BLEND_CULL) == 1
     assert L.fgs_set_tuning(fgs.FGS_TUNE_BLEND_CULL, 2) == fgs.FGS_E_INVALID
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_CULL) == 0
+    with fgs.tuning(fgs.FGS_TUNE_TILE_CULL, 1):
+        assert fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_CULL) == 1
+    assert fgs.fgs_get_tuning(fgs.FGS_TUNE_TILE_CULL) == 0
+    assert L.fgs_set_tuning(fgs.FGS_TUNE_TILE_CULL, 2) == fgs.FGS_E_INVALID
     assert fgs.fgs_get_tuning(fgs.FGS_TUNE_AGG_TILES) == 4096
     with fgs.tuning(fgs.FGS_TUNE_AGG_TILES, 1):
         assert fgs.fgs_get_tuning(fgs.FGS_TUNE_AGG_TILES) == 1

@@ -121,3 +121,28 @@ def test_blend_cull_exact_on_whole_fullsize_frames(name):
         assert np.array_equal(imgs[f].cpu().numpy(), on["image"])
         # the cull really skipped work: fewer (warp, Gaussian) evaluations than the unculled loop
         assert on["blend_work"][0] < off["blend_work"][0]
+
+
+@pytest.mark.parametrize("name", ["dnerf", "scaling", "neu3d"])
+def test_tile_cull_exact_on_whole_fullsize_frames(name):
+    """FGS_TUNE_TILE_CULL = 1 (non-contributing (tile, Gaussian) pairs left out of the lists) must not
+    change any pixel: two full-size frames per config, image / final T / contributor counts bit-identical
+    with the knob on and off, the lists shorter, and no tile's list longer than before."""
+    s = make_scene(name, n_frames=2)
+    ds, outs, tens, imgs = _run_frames(s)
+    for f in range(2):
+        f0 = next(i for i in range(2) if np.float32(s.times[i]).tobytes() == np.float32(s.times[f]).tobytes())
+        off = gpu_render_debug(ds, s.cameras[f], outs[f0])
+        with fgs.tuning(fgs.FGS_TUNE_TILE_CULL, 1):
+            on = gpu_render_debug(ds, s.cameras[f], outs[f0])
+        assert on["status"] == off["status"] == fgs.FGS_OK
+        for k in ("image", "final_T", "n_contrib"):
+            assert np.array_equal(on[k], off[k]), (name, f, k, int(np.sum(on[k] != off[k])))
+        assert on["M"] < off["M"]
+        assert np.all(np.diff(on["ranges"], axis=1) <= np.diff(off["ranges"], axis=1))
+    # and through fgs_frames (the batch path) with the knob on
+    with fgs.tuning(fgs.FGS_TUNE_TILE_CULL, 1):
+        ds2, outs2, tens2, imgs2 = _run_frames(s)
+    for f in range(2):
+        assert np.array_equal(imgs[f].cpu().numpy(), imgs2[f].cpu().numpy()), (name, f)
+

@@ -798,6 +798,60 @@ def test_frames_host_concurrent_threads():
             assert torch.equal(a, b), k
 
 
+@pytest.mark.parametrize("case", ["tiny", "dnerf", "elongated"])
+def test_tile_cull_keeps_every_contributor(case):
+    """FGS_TUNE_TILE_CULL = 1 leaves a Gaussian out of a tile's list only where it cannot contribute: the
+    image, final T and contributor counts equal the unculled render bit for bit; every tile's list is an
+    order-preserving subsequence of the [3dgs] list (which the oracle's lists pin with the knob off); and
+    each (tile, Gaussian) pair left out has, by the fp64 oracle's conic, mean and opacity (Eq. 1 / Eq. 4,
+    P:694), alpha < 1/255 at every pixel of the tile.  tiles_touched and n_instances count what
+    remains, and something is in fact removed."""
+    if case == "tiny":
+        s = make_scene("tiny", n=3000, width=150, height=106)
+    elif case == "dnerf":
+        s = make_scene("dnerf", n=25_000, width=208, height=160)
+    else:                                # long thin Gaussians: big rects, few tiles reached
+        s = with_heads(make_scene("tiny", n=1500, width=160, height=128), 0.0)
+        s.log_scales[:, 0] += 1.6
+        s.log_scales[:, 1:] -= 1.2
+    ds = _ds(s)
+    cam = s.cameras[0]
+    dstruct, g, _ = gpu_deform(ds, float(s.times[0]))
+    cap = 80 * s.n if case == "elongated" else None      # 80 tiles: every Gaussian on every tile fits
+    off = gpu_render_debug(ds, cam, dstruct, cap)
+    with fgs.tuning(fgs.FGS_TUNE_TILE_CULL, 1):
+        on = gpu_render_debug(ds, cam, dstruct, cap)
+    assert off["status"] == fgs.FGS_OK and on["status"] == fgs.FGS_OK
+    for k in ("image", "final_T", "n_contrib", "radii", "rect", "depth_key"):
+        assert np.array_equal(off[k], on[k]), k
+    assert on["M"] < off["M"] and on["M"] == int(on["tiles_touched"].sum())
+    assert np.all(on["tiles_touched"] <= off["tiles_touched"])
+    pre = OR.preprocess_ref(g["means"], g["log_scales"], g["quats"], s.opacity_logits, s.sh, s.sh_degree, cam)
+    gx = (cam.width + 15) // 16
+    n_dropped = 0
+    worst = 0.0
+    for tile in range(off["ranges"].shape[0]):
+        a = off["sorted_gid"][off["ranges"][tile, 0]:off["ranges"][tile, 1]]
+        b = on["sorted_gid"][on["ranges"][tile, 0]:on["ranges"][tile, 1]]
+        pos = {int(gid): k for k, gid in enumerate(a)}
+        idx = [pos.get(int(gid), -1) for gid in b]
+        assert all(i >= 0 for i in idx) and all(x < y for x, y in zip(idx, idx[1:])), tile
+        dropped = np.setdiff1d(a, b)
+        if len(dropped) == 0:
+            continue
+        n_dropped += len(dropped)
+        tx, ty = tile % gx, tile // gx
+        px, py = np.meshgrid(np.arange(16 * tx, min(16 * tx + 16, cam.width), dtype=np.float64),
+                             np.arange(16 * ty, min(16 * ty + 16, cam.height), dtype=np.float64))
+        for gid in dropped:
+            dx, dy = pre["mean2d"][gid, 0] - px, pre["mean2d"][gid, 1] - py
+            A, B, C = pre["conic"][gid]
+            alpha = pre["opacity"][gid] * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
+            worst = max(worst, float(alpha.max()))
+    assert n_dropped == off["M"] - on["M"]
+    assert worst < 1.0 / 255.0, worst
+
+
 def test_frames_host_two_calls_in_flight():
     """bench.py's pipelined e2e: one host thread keeps two fgs_frames_host calls in flight on two
     streams (each lane its own workspace and pinned images; the SH upload and the image downloads ride
