@@ -583,6 +583,31 @@ def run_fgs(args, scene, rank, world, local_rank):
     step_stats = {"median": statistics.median(per_step), "p10": per_step[int(0.1 * (len(per_step) - 1))],
                   "p90": per_step[int(round(0.9 * (len(per_step) - 1)))], "unit": "ms (this rank)"}
     clk = clocks.stop()
+    # --tile-cull: the same step with FGS_TUNE_TILE_CULL = 1 (non-contributing (tile, Gaussian) pairs left
+    # out of the lists; an opt-in knob, default off) timed the same way, its images compared bit for bit
+    tile_cull = None
+    if args.tile_cull and F and graph is not None:
+        ref_imgs = [im.clone() for im in images]
+        with fgs.tuning(fgs.FGS_TUNE_TILE_CULL, 1):
+            for _ in range(args.warmup):
+                step_eager()
+            fgs.fgs_render_status(ws, F)
+            t_e2, _, st2 = timed(step_eager, True)
+            graph2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph2):
+                fgs.fgs_frames(ds.g, ds.field, ds.mlp, ds.times, ds.cams, outs[:F], images, ws,
+                               stream=torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            for _ in range(args.warmup):
+                graph2.replay()
+            t2, _, _ = timed(graph2.replay, False)
+        fps = F_all if split else F_all * world
+        tile_cull = {"value": fps * args.steps / (t2 / 1e3), "unit": "frames/s", "ms_per_step": t2 / args.steps,
+                     "value_eager": fps * args.steps / (t_e2 / 1e3),
+                     "stages_ms_per_step": {k: v[0] / args.steps for k, v in st2.items()},
+                     "images_identical": all(torch.equal(a, b) for a, b in zip(ref_imgs, images)),
+                     "note": "FGS_TUNE_TILE_CULL = 1 (opt-in; the headline value above is with the default, 0)"}
+        del graph2, ref_imgs
     frames_per_step = F_all if split else F_all * world
     value = frames_per_step * args.steps / (t_max / 1e3)
     value_eager = frames_per_step * args.steps / (t_eager / 1e3)
@@ -736,6 +761,8 @@ def run_fgs(args, scene, rank, world, local_rank):
         "clocks": clk,
         "e2e": e2e,
     }
+    if tile_cull is not None:
+        line["tile_cull"] = tile_cull
     if split_check is not None:
         line["frame_split_check"] = split_check
     if not args.no_cpu_baseline and F:
@@ -1037,6 +1064,8 @@ def main():
                     help="FGS_TUNE_RADIX: 0 per-tile sorts, 1 auto (library default), 2 radix binning path")
     ap.add_argument("--radix-min-list", type=int, default=None, help="FGS_TUNE_RADIX_MIN_LIST (auto threshold)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-cull", action="store_true",
+                    help="also time the step with FGS_TUNE_TILE_CULL = 1 (adds a tile_cull object to the line)")
     ap.add_argument("--no-e2e-pipeline", action="store_true",
                     help="e2e: one fgs_frames_host call at a time only (no two-in-flight pipelined measurement)")
     ap.add_argument("--weak", action="store_true",

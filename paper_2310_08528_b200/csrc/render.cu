@@ -155,21 +155,11 @@ __device__ __forceinline__ void for_each_tile(int x0, int y0, int x1, int y1, un
     }
   }
 }
-// May alpha reach 1/255 on the tile whose pixel offsets d = pixel - mean span [xl, xl + 15] x [yl, yl + 15]?
-// The minimum of the PSD quadratic q2 over the box is 0 if the box holds 0, else it lies on the x- or
-// y-face nearest to 0 at the clamped 1-D minimiser (kx = -qb / 2qa, ky = -qb / 2qc): the blend's
-// sub-box bound (subboxes_reach, fgs_internal.cuh) on the 16x16 box.
-__device__ __forceinline__ bool tile_box_reach(float qa, float qb, float qc, float kx, float ky, float thr,
-                                               float xl, float yl) {
-  const float xh = xl + (float)(kTile - 1), yh = yl + (float)(kTile - 1);
-  const float ex = fmaxf(xl, fminf(xh, 0.f)), ey = fmaxf(yl, fminf(yh, 0.f));
-  const float yy = fminf(fmaxf(ky * ex, yl), yh);
-  const float qx = fmaf(yy, fmaf(qc, yy, qb * ex), qa * ex * ex);
-  const float xx = fminf(fmaxf(kx * ey, xl), xh);
-  const float qy = fmaf(xx, fmaf(qa, xx, qb * ey), qc * ey * ey);
-  return fminf(qx, qy) <= thr;
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-
 // Per-tile instance counts of a CTA's Gaussians: aggregated in shared memory over the CTA's
 // rect union when it holds at most agg_tiles tiles (one global atomic per touched tile), else direct
 // global atomics (cnt67[0] counts the CTAs that took that path: fgs_render_aux.binning_direct[0]).
@@ -289,8 +279,8 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
   // Bit (ty - y0) * w + (tx - x0) of tmask; all ones without the cull or for rects over 64 tiles.  A
   // tile is dropped only if the minimum over its 16x16 pixel box of q2(d) = qa dx^2 + qb dx dy + qc dy^2
   // (d = pixel - mean) exceeds the blend's threshold thr_keep (below: log2(255 o) plus the margin that
-  // covers fp32 evaluation): then every pixel of the tile has alpha < 1/255 in the blend.  Same bound
-  // as the blend's sub-box cull (tile_box_reach above), whose sub-boxes lie inside the tile's box.
+  // covers fp32 evaluation): then every pixel of the tile has alpha < 1/255 in the blend (the blend's
+  // sub-box cull applies the same bound to sub-boxes of the tile).
   unsigned long long tmask = ~0ull;
   int ntl = (x1 - x0) * (y1 - y0);
   // blend threshold: q2 = -p2 >= 0; alpha >= 1/255 needs q2 <= log2(255 o).  The margin covers the fp32
@@ -310,15 +300,41 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(const __grid_constan
   if (CULL && keep) {
     blend_threshold();
     if (ntl <= 64) {
-      const float qa = (float)(0.5 * cc * idet), qb = (float)(-bb * idet), qc = (float)(0.5 * a * idet);
-      const float kx = __fdividef(-qb, 2.f * qa), ky = __fdividef(-qb, 2.f * qc);
-      const float fmx = (float)mx, fmy = (float)my;
+      // One x-interval per tile ROW: the ellipse E = {q2 <= thr_keep} is, in pixel offsets d = pixel - mean,
+      // {d^T Sigma2^-1 d <= T} with T = 2 thr_keep / log2(e).  E meets the strip y in [yl, yh] of a tile row
+      // in a convex set whose x-projection is [X_lo, X_hi]: x_hi(y) = (b/c) y + sqrt((T - y^2/c) det/c)
+      // (Sigma2 = [[a, b], [b, c]]) is concave with its maximum at the ordinate y_r = (b/a) sqrt(T a) of
+      // E's rightmost point, so X_hi = x_hi(clamp(y_r, yl, yh)) and, by symmetry, X_lo = x_lo(clamp(-y_r,
+      // yl, yh)).  A tile of the row (it spans the strip's whole height) meets E iff its x-range meets
+      // [X_lo, X_hi]: the listed tiles of a row are one contiguous run of mask bits.  Coefficients from
+      // the fp64 covariance rounded to fp32 (no cancellation: det is formed in fp64); strip and interval are
+      // widened by 0.01 px (+ 1e-5 relative), which covers the fp32 mean (ulp 0.002 px at 16384) and the
+      // approximate square roots, on top of thr_keep's margin.
       tmask = 0ull;
-      int bit = 0;
-      for (int ty = y0; ty < y1; ++ty) {
-        const float yl = (float)(ty * kTile) - fmy;
-        for (int tx = x0; tx < x1; ++tx, ++bit)
-          if (tile_box_reach(qa, qb, qc, kx, ky, thr_keep, (float)(tx * kTile) - fmx, yl)) tmask |= 1ull << bit;
+      const float Tq = thr_keep * (float)(2.0 / kLog2e);
+      if (Tq > 0.f) {
+        const float fa = (float)a, fb = (float)bb, fc = (float)cc, fmx = (float)mx, fmy = (float)my;
+        const float inv_c = __frcp_rn(fc), r_bc = fb * inv_c, s_c = (float)det * inv_c;
+        const float ymax = sqrt_approx(Tq * fc) * 1.00001f + 1e-2f;
+        const float y_r = fb * __frcp_rn(fa) * sqrt_approx(Tq * fa);
+        const int w = x1 - x0;
+        float yl = (float)(y0 * kTile) - fmy - 1e-2f;          // strip widened by 0.01 px (fp32 mean2d)
+        for (int ty = y0, sh = 0; ty < y1; ++ty, sh += w, yl += (float)kTile) {
+          const float yh = yl + ((float)(kTile - 1) + 2e-2f);
+          if (yl > ymax || yh < -ymax) continue;
+          const float ya = fminf(fmaxf(y_r, yl), yh), yb = fminf(fmaxf(-y_r, yl), yh);
+          float X_hi = fmaf(r_bc, ya, sqrt_approx(fmaxf(0.f, fmaf(-ya * ya, inv_c, Tq)) * s_c));
+          float X_lo = fmaf(r_bc, yb, -sqrt_approx(fmaxf(0.f, fmaf(-yb * yb, inv_c, Tq)) * s_c));
+          X_hi += 1e-2f + 1e-5f * fabsf(X_hi);
+          X_lo -= 1e-2f + 1e-5f * fabsf(X_lo);
+          const int ta = max(x0, __float2int_ru((X_lo + fmx - (float)(kTile - 1)) * (1.f / kTile)));
+          const int tb = min(x1 - 1, __float2int_rd((X_hi + fmx) * (1.f / kTile)));
+          if (tb >= ta) {
+            const int nrun = tb - ta + 1;
+            const unsigned long long run = nrun >= 64 ? ~0ull : (1ull << nrun) - 1ull;
+            tmask |= run << (sh + ta - x0);
+          }
+        }
       }
       ntl = __popcll(tmask);
     }
