@@ -47,9 +47,17 @@ if d:
     e = d.get("e2e") or {}
     if e:
         out.append(f"* e2e (fgs_frames_host: pinned host model in, host images out, copies inside the timed "
-                   f"region): {e['value']:.0f} frames/s; {e['h2d_bytes_per_step'] / 1e6:.1f} MB in, "
+                   f"region): {e['value']:.0f} frames/s"
+                   + (f" with two calls in flight ({e['serial_value']:.0f} one call at a time)" if "serial_value" in e else "")
+                   + f"; {e['h2d_bytes_per_step'] / 1e6:.1f} MB in, "
                    f"{e['d2h_bytes_per_step'] / 1e6:.1f} MB out per step (PCIe: 54-57 GB/s measured each way, "
                    "`tools/numa_probe.py`)")
+    for tl in open(f"profiles/{NAME}_tile_cull.jsonl") if os.path.exists(f"profiles/{NAME}_tile_cull.jsonl") else []:
+        t = json.loads(tl)
+        tc = t.get("tile_cull") or {}
+        if tc:
+            out.append(f"* `--tile-cull` ({t['config']['workload'].split(':')[0]}): {t['value']:.0f} -> {tc['value']:.0f} frames/s with "
+                       f"FGS_TUNE_TILE_CULL = 1 (opt-in, default off), images identical: {tc['images_identical']}")
     cb = d.get("cpu_baseline") or {}
     if cb:
         out.append(f"* oracle (fp64 numpy, {cb.get('cores')} host processes, bounded sample): {cb.get('value'):.3g} "
