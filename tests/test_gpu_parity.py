@@ -326,6 +326,33 @@ def test_long_sort_bucket_pass_paths(case):
     assert ints["tile_lists"] == 0 and ints["rect"] == 0, ints
 
 
+@pytest.mark.parametrize("case", ["n200", "n600", "n1000", "ties"])
+def test_warp_bucket_sort_matches_networks(case):
+    """Warp-sorted lists of 129..1024 instances take one bucket pass (512 depth buckets, rank within the
+    bucket) when FGS_TUNE_LONG_SORT = 1 (the default) and the register networks + merge when it is 0; a
+    list with a bucket of more than 32 instances (here 300 Gaussians at one bit-identical depth: exact
+    ties, ordered by index) falls back to the networks.  One 16x16 tile holds every kept Gaussian; both
+    modes give the oracle's (tile, depth, index) list and identical images."""
+    n = {"n200": 200, "n600": 600, "n1000": 1000, "ties": 800}[case]
+    s = make_scene("tiny", n=n, width=16, height=16)
+    if case == "ties":
+        s = with_heads(s, 0.0)                                  # zero heads: means as given
+        s.means[:300] = s.means[500]
+    ds = _ds(s)
+    dstruct, g, _ = gpu_deform(ds, float(s.times[0]))
+    res = {}
+    for mode in (1, 0):
+        with fgs.tuning(fgs.FGS_TUNE_LONG_SORT, mode):
+            res[mode] = gpu_render_debug(ds, s.cameras[0], dstruct)
+    L = int(np.diff(res[1]["ranges"], axis=1).max())
+    assert 128 < L <= 1024, L
+    for k in ("sorted_gid", "sorted_tile", "ranges", "image", "final_T", "n_contrib"):
+        assert np.array_equal(res[0][k], res[1][k]), k
+    ref = OR.render_ref(g, s.opacity_logits, s.sh, s.sh_degree, s.cameras[0])
+    ints = compare_integer_work(res[1], ref["pre"], (ref["tiles"], ref["gids"], ref["ranges"]))
+    assert ints["tile_lists"] == 0 and ints["rect"] == 0, ints
+
+
 def test_sharded_frames_single_rank_equals_fgs_frames():
     """(e2) pipeline (sharding.sharded_frames) at world size 1: deform via fgs_deform_range into the
     gather buffers + render per time gives the same images as fgs_frames."""
