@@ -708,7 +708,10 @@ __device__ __forceinline__ void warp_merge(const unsigned long long* a, int na, 
 // sort_cap <= 1024) as two runs sorted in registers into the warp's shared buffer (256-key runs up to
 // 512, 512-key runs beyond: one merge level either way) and merged by merge path straight into the
 // list.  Longer lists are queued for long_sort_kernel.
-constexpr int kTileSortWarps = 4;
+#ifndef FGS_TILE_SORT_WARPS
+#define FGS_TILE_SORT_WARPS 2
+#endif
+constexpr int kTileSortWarps = FGS_TILE_SORT_WARPS;
 // A warp's list (129..1024 instances) sorted by ONE bucket pass, the warp-level form of long_sort_bucket
 // below: the 64-bit instances (depth_key << 32 | gid) are all distinct, so with the monotone map
 // bucket(x) = (depth_key - list min) >> shift (512 buckets) an instance's final position is its bucket's
