@@ -322,8 +322,9 @@ int64_t fgs_launch_count(void);
  * levels.  The order is identical either way (fgs_render_aux.long_sort_paths counts which ran).
  * FGS_TUNE_TILE_CULL: 0 (default) = a tile's list holds every kept Gaussian whose [3dgs] rect covers the
  * tile (the oracle's lists, bit for bit); 1 = a Gaussian whose rect holds at most 64 tiles is left
- * out of the list of a tile on which its alpha provably stays below 1/255 at every pixel (fp64 minimum of
- * its Eq. 1 exponent over the tile's 16x16 pixel box against the blend's own threshold with margin): the
+ * out of the list of a tile on which its alpha provably stays below 1/255 at every pixel (the ellipse where
+ * its Eq. 1 exponent reaches the blend's own threshold, margin included, does not meet the tile's 16x16
+ * pixel box: one x-interval of the ellipse per tile row, widened by 0.01 px): the
  * lists are then ordered subsequences of the [3dgs] lists that keep every contributing entry, and images,
  * final T and contributor counts are identical (tests check both on whole full-size frames);
  * fgs_render_aux.tiles_touched counts the remaining tiles, n_instances the remaining entries.  With 1

@@ -1,6 +1,8 @@
 """FGS_TUNE_TILE_CULL on vs off: images / final T / contributor counts bit-identical, instance counts, stage times.
     python tools/tile_cull_check.py [config] [frames]"""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json
 import numpy as np
 import torch
