@@ -659,7 +659,7 @@ def run_fgs(args, scene, rank, world, local_rank):
         # alternating workspaces (>= 2 x the batch's images) exceed the 126 MB L2.
         pipe = None
         if F and not args.no_e2e_pipeline:
-            depth = 2
+            depth = max(2, args.e2e_depth)
             dws2 = [dws] + [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(depth - 1)]
             himgs2 = [himgs] + [[torch.empty((3, H, W), dtype=torch.float32).pin_memory() for _ in range(F)]
                                 for _ in range(depth - 1)]
@@ -699,7 +699,7 @@ def run_fgs(args, scene, rank, world, local_rank):
                "h2d_bytes_per_step": hs.h2d_bytes() + F * 4, "d2h_bytes_per_step": F * 3 * H * W * 4,
                "api": "fgs_frames_host (pinned host model in, host images out)", "matches_device_path": same,
                "serial_value": serial,
-               "mode": ("%d fgs_frames_host calls in flight (two streams, two workspaces): one event pair around "
+               "mode": ("%d fgs_frames_host calls in flight (one stream and one workspace each): one event pair around "
                         "all K steps, every step's copies inside it" % pipe["depth"]) if pipe else
                        "one call at a time, per-step events, L2 flushed between steps",
                "serial_note": "serial_value: one call at a time (the next upload starts after the last download)"}
@@ -1066,6 +1066,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-cull", action="store_true",
                     help="also time the step with FGS_TUNE_TILE_CULL = 1 (adds a tile_cull object to the line)")
+    ap.add_argument("--e2e-depth", type=int, default=2, help="fgs_frames_host calls in flight in the pipelined e2e")
     ap.add_argument("--no-e2e-pipeline", action="store_true",
                     help="e2e: one fgs_frames_host call at a time only (no two-in-flight pipelined measurement)")
     ap.add_argument("--weak", action="store_true",
