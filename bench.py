@@ -705,6 +705,9 @@ def run_fgs(args, scene, rank, world, local_rank):
                "serial_note": "serial_value: one call at a time (the next upload starts after the last download)"}
         if pipe:
             e2e["pipeline_ms_per_step"] = pipe["ms_per_step"]
+            e2e["l2"] = ("pipelined: no flush (every step's inputs arrive from pinned host memory and the alternating "
+                         "device workspaces, %.0f MB each, exceed the 126 MB L2); serial_value: flushed between steps"
+                         % (nbytes / 1e6))
         del dws
 
     # ---- (e1) untimed: the ranks' images gathered to rank 0 == a single-GPU render of the whole batch ----
